@@ -1,0 +1,311 @@
+#!/usr/bin/env python3
+"""bench.py — Gcell-updates/s of the fp32 Yee E+H leapfrog step on B200.
+
+Default workload = BASELINE config 2 (configs[1]): 256^3 heterogeneous
+dielectric (eps_r ~ U[1,4] seed 1 -> per-cell Cb, Ca = Da = 1, Db = S), PEC,
+Gaussian Ez point source at the centre. One "step" = one full leapfrog time
+step (Ampere, PEC, source, Faraday) over the whole grid. Fields (6 x 67 MB)
+plus the Cb array exceed the 126 MB L2, so no L2 flush is needed between
+steps (stated in config).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+                  [--impl ours|reference] [--variant fused|naive]
+
+Prints ONE JSON line (rank 0). N>1: launched under torchrun, one rank per GPU.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gcell-updates/s (fp32 Yee E+H step)"
+UNIT = "Gcell/s"
+
+# name: (nx, ny, nz_per_gpu, eps_seed, sigma_seed, field_seed, source, config_steps, label)
+CONFIGS = {
+    "c1": (128, 128, 128, -1, -1, None, True, 200, "config1 vacuum cube 128^3, PEC, Gaussian Ez source"),
+    "c2": (256, 256, 256, 1, -1, None, True, 500,
+           "config2 heterogeneous dielectric 256^3 (eps_r U[1,4] seed 1), PEC, Gaussian Ez source"),
+    "c3": (512, 512, 512, 2, 2, 3, False, 100,
+           "config3 lossy random medium 512^3 (seeds 2/3), PEC, no source"),
+    "c4": (1024, 1024, 512, 4, -1, None, True, 200,
+           "config4 slab 1024x1024x512 (eps_r seed 4), PEC, Gaussian Ez source"),
+    "c5": (1024, 1024, 256, 5, 5, 6, False, 100,
+           "config5 weak-scaling box 1024x1024x(256*G) lossy (seeds 5/6), PEC, no source"),
+}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(nx, ny, nz, budget_s=10.0, max_steps=None):
+    """The reference's own CPU path (oracle/_ref: yeeblock Simulation<float>,
+    Tiled split 1x16x16, all host cores, quiescent skip off) on the same grid.
+    The reference has no per-cell coefficients, so it runs the vacuum
+    coefficient set on that grid. Falls back to the C oracle port."""
+    from oracle import pyoracle as O
+    cores = os.cpu_count() or 1
+    f = O.fill_fields(nx, ny, nz, 1, threads=cores)
+    if O.have_ref():
+        split = (1, min(16, ny), min(16, nz))
+        O.ref_simulation(nx, ny, nz, f, 1, variant="tiled", split=split, workers=cores)  # warm
+        steps, secs = 0, 0.0
+        while secs < budget_s and (max_steps is None or steps < max_steps):
+            s, _ = O.ref_simulation(nx, ny, nz, f, 1, variant="tiled", split=split, workers=cores)
+            secs += s
+            steps += 1
+        return {"value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores,
+                "kind": "reference",
+                "sample": f"yeeblock Simulation<float> Tiled split 1x{split[1]}x{split[2]}, {cores} workers, "
+                          f"{nx}x{ny}x{nz} grid, {steps} steps, vacuum coefficients (the reference has "
+                          f"no per-cell Ca/Cb), quiescent skip off; time from RunStats.total_seconds"}
+    co = O.Coeffs(nx, ny, nz)
+    O.run(nx, ny, nz, f, co, 1, threads=cores)
+    steps, secs = 0, 0.0
+    while secs < budget_s and (max_steps is None or steps < max_steps):
+        t = time.perf_counter()
+        O.run(nx, ny, nz, f, co, 1, threads=cores)
+        secs += time.perf_counter() - t
+        steps += 1
+    return {"value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"C oracle port (OpenMP {cores} threads) {nx}x{ny}x{nz}, {steps} steps"}
+
+
+def load_traffic(cfg, variant):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return t.get(f"{cfg}:{variant}")
+    except Exception:
+        return None
+
+
+def load_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="fused", choices=["fused", "naive"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    nx, ny, nzg, es, ss, fs, has_src, cfg_steps, label = CONFIGS[args.config]
+    nz = nzg  # per-GPU slab depth (weak scaling: every rank runs its own slab)
+    cells = nx * ny * nz
+
+    config = {"workload": label, "grid": [nx, ny, nz], "steps_config": cfg_steps,
+              "per_gpu_grid": [nx, ny, nz], "parallelism": f"replicas{world}" if world > 1 else "single",
+              "l2": "working set > 126 MB L2 (no flush needed)" if cells * 28 > 126e6 else
+                    "working set fits L2; L2 not flushed (informational)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference_rate(nx, ny, nz, budget_s=1e9, max_steps=max(1, args.steps))
+        line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": config, "cpu_baseline": ref,
+                "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_1301_4539_b200 as Y
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    variant = Y.VARIANT_FUSED if args.variant == "fused" else Y.VARIANT_NAIVE
+
+    sim = Y.Simulation(nx, ny, nz, device=local, variant=variant)
+    sim.generate_medium(es, ss)
+    table = None
+    if has_src:
+        from paper_1301_4539_b200 import S  # noqa: F401
+        t = np.arange(cfg_steps + args.steps + args.warmup + 16, dtype=np.float64)
+        table = np.exp(-((t - 40.0) / 12.0) ** 2).astype(np.float32)
+        sim.add_source(Y.EZ, nx // 2, ny // 2, nz // 2, table)
+    if fs is not None:
+        sim.fill(fs)
+    sim.run(args.warmup)
+    info0 = sim.info()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sim.set_kernel_timing(True)
+    ms = sim.run_timed(args.steps)
+    info1 = sim.info()
+    sim.set_kernel_timing(False)
+    clocks = sampler.stop()
+    torch.cuda.synchronize()
+    if dist:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+
+    launches = info1["kernel_launches"] - info0["kernel_launches"]
+    value = cells * world * args.steps / (ms * 1e-3) / 1e9
+    bpc = info1["bytes_per_cell_update"]
+    kern_ms = info1["main_kernel_ms"] / max(1, info1["main_kernel_timed"])
+    peak, peak_src = load_peak()
+    achieved = bpc * cells / (kern_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": load_traffic(args.config, args.variant),
+                "kernel": "k_fused (one E+H sweep)" if variant == 0 else "naive step (4 kernels)",
+                "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,
+                "peak_source": peak_src,
+                "step_ms_share_of_kernel": kern_ms / (ms / args.steps)}
+    config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
+                   "grid": [info1["grid_x"], info1["grid_y"], info1["grid_z"]],
+                   "n_cell_arrays": info1["n_cell_arrays"]})
+
+    # e2e through the public API with host buffers: run_simulation semantics
+    # (upload state + coefficients, advance the config's step count, download).
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda shape: torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+        host_f = [pin(Y.comp_extents(nx, ny, nz, c)[::-1]) for c in range(6)]
+        if fs is not None:
+            Y.host_fields(nx, ny, nz, fs, out=host_f)
+        else:
+            for a in host_f:
+                a[...] = 0.0
+        # per-cell coefficient arrays the caller supplies from host memory
+        cell_arrays = {}
+        if es >= 0:
+            want = (Y.CB,) if ss < 0 else (Y.CA, Y.CB, Y.DA, Y.DB)
+            med = Y.host_medium(nx, ny, nz, es, ss,
+                                out=[pin((nz, ny, nx)) if q in want else None for q in range(4)])
+            cell_arrays = {q: med[q] for q in want}
+        e_steps = cfg_steps
+        with Y.Simulation(nx, ny, nz, device=local, variant=variant) as s2:
+            if table is not None:
+                s2.add_source(Y.EZ, nx // 2, ny // 2, nz // 2, table)
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for q, a in cell_arrays.items():
+                s2.set_cell_coeffs(q, a)
+            s2.upload(host_f)
+            s2.run(e_steps)
+            out = s2.download()
+            t1 = time.perf_counter()
+        dt = t1 - t0
+        if dist:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        h2d = sum(a.nbytes for a in host_f) + sum(a.nbytes for a in cell_arrays.values())
+        d2h = sum(a.nbytes for a in out)
+        e2e = {"value": cells * world * e_steps / dt / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
+               "steps": e_steps, "wall_s": dt,
+               "path": "Simulation: set_cell_coeffs + upload (dense host) -> run(config steps) -> download"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_rate(nx, ny, nz, budget_s=10.0)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

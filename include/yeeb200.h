@@ -1,0 +1,166 @@
+/*
+ * yeeb200.h — C-ABI of libyeeb200.so, the B200 (sm_100a) implementation of
+ * the reference yeeblock Standard leapfrog step (arXiv 1301.4539 hot path).
+ *
+ * Plain C: opaque handle, plain pointers and sizes, int status codes. The
+ * C++ shim include/yeeb200/yeeblock.hpp maps the codes back onto the
+ * reference's exception types and re-exposes the reference API names.
+ *
+ * Each entry point cites the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/yeeblock/).
+ *
+ * Field arrays crossing this boundary use the reference's dense Array3
+ * layout of each component: extents from staggering.hpp:34-39
+ *   ex nx x (ny+1) x (nz+1)   ey (nx+1) x ny x (nz+1)   ez (nx+1) x (ny+1) x nz
+ *   hx (nx+1) x ny x nz       hy nx x (ny+1) x nz       hz nx x ny x (nz+1)
+ * and index (k*ny_c + j)*nx_c + i (array3.hpp:104-107). Per-cell
+ * coefficient arrays are nx*ny*nz in the same cell order.
+ *
+ * Threading: one host thread per handle at a time (like FieldSet /
+ * Simulation). Work is enqueued on the handle's CUDA stream;
+ * calls that return data to the host synchronise that stream.
+ */
+#ifndef YEEB200_H
+#define YEEB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define YB_ABI_VERSION 1
+
+/* Status codes. The shim maps INVALID_ARGUMENT -> std::invalid_argument,
+ * OUT_OF_RANGE -> std::out_of_range, the rest -> std::runtime_error. */
+enum {
+  YB_OK = 0,
+  YB_INVALID_ARGUMENT = 1,
+  YB_OUT_OF_RANGE = 2,
+  YB_RUNTIME_ERROR = 3,
+  YB_CUDA_ERROR = 4
+};
+
+/* Components, in the reference's canonical order (staggering.hpp:12). */
+enum { YB_EX = 0, YB_EY, YB_EZ, YB_HX, YB_HY, YB_HZ };
+
+/* Per-cell coefficient selectors (extension; the reference has none). */
+enum { YB_CA = 0, YB_CB = 1, YB_DA = 2, YB_DB = 3 };
+
+/* Step implementations. */
+enum {
+  YB_VARIANT_FUSED = 0, /* one z-march sweep per step: TMA-staged planes, E+H fused */
+  YB_VARIANT_NAIVE = 1  /* one thread per DoF, separate E/PEC/source/H launches */
+};
+
+typedef struct yb_sim yb_sim;
+
+typedef struct {
+  int nx, ny, nz; /* cells per axis (GridSpec, grid.hpp:17-43) */
+  int device;     /* CUDA device ordinal */
+  int variant;    /* YB_VARIANT_* */
+  int zchunk;     /* fused: z planes per CTA; 0 = auto */
+  int reserved[6];
+} yb_desc;
+
+typedef struct {
+  int64_t step_index;      /* completed steps (FieldSet::step_index, fields.hpp:24) */
+  int64_t steps;           /* steps advanced through this handle */
+  int64_t kernel_launches; /* kernels launched by yb_advance so far */
+  double main_kernel_ms;   /* summed device time of the main sweep kernel (timing on) */
+  int64_t main_kernel_timed;
+  int n_cell_arrays;       /* per-cell coefficient arrays read by the step (0..4) */
+  int variant;
+  int stages;              /* fused: TMA ring depth */
+  int grid_x, grid_y, grid_z;
+  int zchunk;
+  double bytes_per_cell_update; /* algorithmic HBM bytes per cell-update, one sweep */
+  size_t device_bytes;     /* device memory held by the handle */
+} yb_info;
+
+/* Last error message of the calling thread ("" if none). */
+const char* yb_last_error(void);
+int yb_abi_version(void);
+
+/* Simulation<Real> ctor (runner.hpp:208-234) minus the CPU tiling: allocates
+ * device-resident padded SoA fields (zeroed, step_index 0). Coefficients
+ * start as Ca = Da = 1, Cb/Db = per-axis arrays filled with 0 (call
+ * yb_set_axis_coeffs, the build_coefficients replacement). */
+int yb_create(const yb_desc* desc, yb_sim** out);
+int yb_destroy(yb_sim* sim);
+
+/* Coefficients<Real>{cdx,cdy,cdz} (grid.hpp:79-103): the reference's one
+ * coefficient set, used by both curls where no per-cell Cb/Db is set. */
+int yb_set_axis_coeffs(yb_sim* sim, const float* cdx, const float* cdy, const float* cdz);
+
+/* Per-cell coefficients (extension). which = YB_CA/YB_DA: `cells` (nx*ny*nz)
+ * or NULL to use the scalar `uniform`. which = YB_CB/YB_DB: `cells` or NULL
+ * to fall back to the per-axis arrays. Update forms (reference operand
+ * order, kernels.hpp:27-63):
+ *   e = Ca*e + (Cb*(a-b) - Cb*(c-d)),  h = Da*h + (Db*(a-b) - Db*(c-d)).
+ * An uploaded array whose values are all equal is stored as a uniform
+ * value (Ca/Da scalar; Cb/Db as a constant per-axis set) - bit-identical,
+ * one array fewer to stream. */
+int yb_set_cell_coeffs(yb_sim* sim, int which, const float* cells, float uniform);
+
+/* Device-side generation of the pinned seeded medium (include/yeeb200_inputs.h):
+ * eps_seed < 0 -> eps = 1; sigma_seed < 0 -> sigma = 0. With sigma = 0 the
+ * Ca/Da arrays are exactly 1 and Db exactly S, so only Cb is stored. */
+int yb_generate_medium(yb_sim* sim, int64_t eps_seed, int64_t sigma_seed);
+
+/* Host-side generators of the same pinned inputs, for callers that feed the
+ * drop-in from host memory (no handle, no GPU needed). Any of the four
+ * coefficient outputs may be NULL. Dense reference layouts. */
+int yb_host_medium(int nx, int ny, int nz, int64_t eps_seed, int64_t sigma_seed, float* ca,
+                   float* cb, float* da, float* db);
+int yb_host_field(int nx, int ny, int nz, uint64_t seed, int comp, float* dense);
+
+/* FieldSet readout/writeback (fields.hpp:21-67). Dense reference layout. */
+int yb_upload_field(yb_sim* sim, int comp, const float* dense);
+int yb_download_field(yb_sim* sim, int comp, float* dense);
+/* FieldSet::zero() (fields.hpp:60-63) and seeded init (yeeb200_inputs.h). */
+int yb_zero_fields(yb_sim* sim);
+int yb_fill_fields(yb_sim* sim, uint64_t seed);
+int yb_set_step_index(yb_sim* sim, int64_t step_index);
+int yb_get_step_index(yb_sim* sim, int64_t* step_index);
+
+/* Soft point source on one E DoF (SourceSpec + inject_current,
+ * source.hpp:33-68): comp(i,j,k) += table[step] at each step < n, after
+ * Ampere and PEC, before Faraday. Position must be strictly interior
+ * (SourceSpec::validate, source.hpp:43-55). At most YB_MAX_SOURCES. */
+#define YB_MAX_SOURCES 8
+int yb_add_source(yb_sim* sim, int comp, int i, int j, int k, const float* table, int64_t n);
+int yb_clear_sources(yb_sim* sim);
+
+/* Simulation::run(n) time loop (runner.hpp:243-266) with the Standard step
+ * (schedule.hpp:171-210): advances step_index by n. Asynchronous on the
+ * handle's stream. */
+int yb_advance(yb_sim* sim, int64_t nsteps);
+int yb_synchronize(yb_sim* sim);
+/* yb_advance bracketed by CUDA events on the handle's stream; *ms = elapsed. */
+int yb_advance_timed(yb_sim* sim, int64_t nsteps, float* ms);
+
+/* Range operations (kernels.hpp:129-155), in place on the current state.
+ * box = {xlo,xhi,ylo,yhi,zlo,zhi} in node index space, must lie inside
+ * [0,nx]x[0,ny]x[0,nz] (detail::check_range, kernels.hpp:118-122) else
+ * YB_OUT_OF_RANGE. NULL box = whole domain. */
+int yb_apply_ampere_range(yb_sim* sim, const int* box);
+int yb_apply_faraday_range(yb_sim* sim, const int* box);
+int yb_apply_pec_boundary(yb_sim* sim);
+
+/* field_digest (fields.hpp:151-166): FNV-1a-64 over the dense Ex..Hz bytes. */
+int yb_field_digest(yb_sim* sim, uint64_t* out);
+
+/* Work on a caller-owned stream (e.g. torch.cuda.current_stream()); NULL
+ * restores the handle's own stream. */
+int yb_set_stream(yb_sim* sim, void* cuda_stream);
+/* Accumulate per-launch device time of the main sweep kernel into yb_info. */
+int yb_set_kernel_timing(yb_sim* sim, int on);
+int yb_get_info(yb_sim* sim, yb_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* YEEB200_H */

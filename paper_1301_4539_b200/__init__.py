@@ -1,0 +1,315 @@
+"""paper_1301_4539_b200 — B200-native Yee FDTD leapfrog step (arXiv 1301.4539 hot path).
+
+Python front end over the C-ABI library ``libyeeb200.so`` (include/yeeb200.h),
+used by the tests and bench.py. The reference-facing drop-in for C++ callers is
+``include/yeeb200/yeeblock.hpp``; this module mirrors the same surface:
+``Simulation(nx, ny, nz)`` owns device-resident padded SoA state,
+``run(n)`` advances ``step_index`` (runner.hpp:243-266), fields cross the
+boundary in the reference's dense Array3 layout (array3.hpp:104-107).
+
+There is no CPU fallback: if the CUDA library is missing or no GPU is present
+every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libyeeb200.so")
+CSRC = os.path.join(HERE, "csrc")
+
+EX, EY, EZ, HX, HY, HZ = range(6)
+COMP_NAMES = ("ex", "ey", "ez", "hx", "hy", "hz")
+CA, CB, DA, DB = range(4)
+VARIANT_FUSED, VARIANT_NAIVE = 0, 1
+S_BITS = 0x3F1252DB
+S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt(3))
+
+# C-ABI exported symbols (include/yeeb200.h) — checked by tests.
+ABI_SYMBOLS = (
+    "yb_last_error", "yb_abi_version", "yb_create", "yb_destroy", "yb_set_axis_coeffs",
+    "yb_set_cell_coeffs", "yb_generate_medium", "yb_upload_field", "yb_download_field",
+    "yb_zero_fields", "yb_fill_fields", "yb_set_step_index", "yb_get_step_index",
+    "yb_add_source", "yb_clear_sources", "yb_advance", "yb_synchronize", "yb_advance_timed",
+    "yb_apply_ampere_range", "yb_apply_faraday_range", "yb_apply_pec_boundary",
+    "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
+    "yb_host_medium", "yb_host_field",
+)
+
+
+class YeeError(RuntimeError):
+    pass
+
+
+class YeeInvalidArgument(YeeError, ValueError):
+    pass
+
+
+class YeeOutOfRange(YeeError, IndexError):
+    pass
+
+
+class _Desc(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("device", C.c_int),
+                ("variant", C.c_int), ("zchunk", C.c_int), ("reserved", C.c_int * 6)]
+
+
+class Info(C.Structure):
+    _fields_ = [("step_index", C.c_int64), ("steps", C.c_int64), ("kernel_launches", C.c_int64),
+                ("main_kernel_ms", C.c_double), ("main_kernel_timed", C.c_int64),
+                ("n_cell_arrays", C.c_int), ("variant", C.c_int), ("stages", C.c_int),
+                ("grid_x", C.c_int), ("grid_y", C.c_int), ("grid_z", C.c_int), ("zchunk", C.c_int),
+                ("bytes_per_cell_update", C.c_double), ("device_bytes", C.c_size_t)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_f32p = C.POINTER(C.c_float)
+_lib = None
+
+
+def build(verbose=False):
+    """Compile libyeeb200.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    r = subprocess.run(["make", "-C", CSRC, "-j3"], capture_output=not verbose, text=True)
+    if r.returncode != 0:
+        raise YeeError("libyeeb200 build failed:\n" + (r.stdout or "") + (r.stderr or ""))
+
+
+def lib():
+    """Load libyeeb200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise YeeError(f"{LIB_PATH} missing: run paper_1301_4539_b200.build()")
+        L = C.CDLL(LIB_PATH)
+        L.yb_last_error.restype = C.c_char_p
+        vp = C.c_void_p
+        L.yb_create.argtypes = [C.POINTER(_Desc), C.POINTER(vp)]
+        L.yb_destroy.argtypes = [vp]
+        L.yb_set_axis_coeffs.argtypes = [vp, _f32p, _f32p, _f32p]
+        L.yb_set_cell_coeffs.argtypes = [vp, C.c_int, _f32p, C.c_float]
+        L.yb_generate_medium.argtypes = [vp, C.c_int64, C.c_int64]
+        L.yb_upload_field.argtypes = [vp, C.c_int, _f32p]
+        L.yb_download_field.argtypes = [vp, C.c_int, _f32p]
+        L.yb_zero_fields.argtypes = [vp]
+        L.yb_fill_fields.argtypes = [vp, C.c_uint64]
+        L.yb_set_step_index.argtypes = [vp, C.c_int64]
+        L.yb_get_step_index.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.yb_add_source.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, _f32p, C.c_int64]
+        L.yb_clear_sources.argtypes = [vp]
+        L.yb_advance.argtypes = [vp, C.c_int64]
+        L.yb_synchronize.argtypes = [vp]
+        L.yb_advance_timed.argtypes = [vp, C.c_int64, C.POINTER(C.c_float)]
+        L.yb_apply_ampere_range.argtypes = [vp, C.POINTER(C.c_int)]
+        L.yb_apply_faraday_range.argtypes = [vp, C.POINTER(C.c_int)]
+        L.yb_apply_pec_boundary.argtypes = [vp]
+        L.yb_field_digest.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.yb_set_stream.argtypes = [vp, vp]
+        L.yb_set_kernel_timing.argtypes = [vp, C.c_int]
+        L.yb_get_info.argtypes = [vp, C.POINTER(Info)]
+        L.yb_host_medium.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                     _f32p, _f32p, _f32p, _f32p]
+        L.yb_host_field.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _f32p]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib().yb_last_error().decode()
+    if rc == 1:
+        raise YeeInvalidArgument(msg)
+    if rc == 2:
+        raise YeeOutOfRange(msg)
+    raise YeeError(f"status {rc}: {msg}")
+
+
+def comp_extents(nx, ny, nz, comp):
+    """(ex, ey, ez) extents of one component (staggering.hpp:34-39)."""
+    n = (nx, ny, nz)
+    axis = comp % 3
+    electric = comp < 3
+    return tuple(n[a] + (1 if (electric and a != axis) or (not electric and a == axis) else 0)
+                 for a in range(3))
+
+
+def _fp(a):
+    return a.ctypes.data_as(_f32p)
+
+
+def _f32c(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class Simulation:
+    """Device-resident Yee state + Standard-step driver (runner.hpp:205-266 mirror).
+
+    Coefficients default to the reference unit grid: cdx = cdy = cdz = S
+    (make_uniform_grid<float>(n, 1, 1, 0.99) + build_coefficients).
+    """
+
+    def __init__(self, nx, ny, nz, device=0, variant=VARIANT_FUSED, zchunk=0, cdx=None, cdy=None,
+                 cdz=None):
+        self.nx, self.ny, self.nz = nx, ny, nz
+        h = C.c_void_p()
+        d = _Desc(nx, ny, nz, device, variant, zchunk)
+        _check(lib().yb_create(C.byref(d), C.byref(h)))
+        self._h = h
+        self.set_axis_coeffs(np.full(nx, S, np.float32) if cdx is None else cdx,
+                             np.full(ny, S, np.float32) if cdy is None else cdy,
+                             np.full(nz, S, np.float32) if cdz is None else cdz)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().yb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # coefficients ---------------------------------------------------------
+    def set_axis_coeffs(self, cdx, cdy, cdz):
+        cdx, cdy, cdz = _f32c(cdx), _f32c(cdy), _f32c(cdz)
+        assert cdx.size == self.nx and cdy.size == self.ny and cdz.size == self.nz
+        _check(lib().yb_set_axis_coeffs(self._h, _fp(cdx), _fp(cdy), _fp(cdz)))
+
+    def set_cell_coeffs(self, which, cells=None, uniform=1.0):
+        if cells is None:
+            _check(lib().yb_set_cell_coeffs(self._h, which, None, uniform))
+        else:
+            cells = _f32c(cells)
+            assert cells.size == self.nx * self.ny * self.nz
+            _check(lib().yb_set_cell_coeffs(self._h, which, _fp(cells), uniform))
+
+    def generate_medium(self, eps_seed=-1, sigma_seed=-1):
+        _check(lib().yb_generate_medium(self._h, eps_seed, sigma_seed))
+
+    # fields -----------------------------------------------------------------
+    def upload(self, fields):
+        for c in range(6):
+            a = _f32c(fields[c])
+            assert a.shape == comp_extents(self.nx, self.ny, self.nz, c)[::-1], (c, a.shape)
+            _check(lib().yb_upload_field(self._h, c, _fp(a)))
+
+    def download(self):
+        out = []
+        for c in range(6):
+            a = np.empty(comp_extents(self.nx, self.ny, self.nz, c)[::-1], np.float32)
+            _check(lib().yb_download_field(self._h, c, _fp(a)))
+            out.append(a)
+        return out
+
+    def zero(self):
+        _check(lib().yb_zero_fields(self._h))
+
+    def fill(self, seed):
+        _check(lib().yb_fill_fields(self._h, seed))
+
+    @property
+    def step_index(self):
+        v = C.c_int64()
+        _check(lib().yb_get_step_index(self._h, C.byref(v)))
+        return v.value
+
+    @step_index.setter
+    def step_index(self, v):
+        _check(lib().yb_set_step_index(self._h, v))
+
+    # sources / stepping ----------------------------------------------------
+    def add_source(self, comp, i, j, k, table):
+        t = _f32c(table)
+        _check(lib().yb_add_source(self._h, comp, i, j, k, _fp(t) if t.size else None, t.size))
+
+    def clear_sources(self):
+        _check(lib().yb_clear_sources(self._h))
+
+    def run(self, nsteps, sync=True):
+        _check(lib().yb_advance(self._h, nsteps))
+        if sync:
+            self.synchronize()
+
+    def run_timed(self, nsteps):
+        ms = C.c_float()
+        _check(lib().yb_advance_timed(self._h, nsteps, C.byref(ms)))
+        return ms.value
+
+    def synchronize(self):
+        _check(lib().yb_synchronize(self._h))
+
+    def apply_ampere_range(self, box=None):
+        b = None if box is None else (C.c_int * 6)(*box)
+        _check(lib().yb_apply_ampere_range(self._h, b))
+
+    def apply_faraday_range(self, box=None):
+        b = None if box is None else (C.c_int * 6)(*box)
+        _check(lib().yb_apply_faraday_range(self._h, b))
+
+    def apply_pec_boundary(self):
+        _check(lib().yb_apply_pec_boundary(self._h))
+
+    def digest(self):
+        v = C.c_uint64()
+        _check(lib().yb_field_digest(self._h, C.byref(v)))
+        return v.value
+
+    def set_stream(self, stream_ptr):
+        _check(lib().yb_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def set_kernel_timing(self, on):
+        _check(lib().yb_set_kernel_timing(self._h, 1 if on else 0))
+
+    def info(self):
+        i = Info()
+        _check(lib().yb_get_info(self._h, C.byref(i)))
+        return i.as_dict()
+
+
+def host_medium(nx, ny, nz, eps_seed, sigma_seed, out=None):
+    """Pinned seeded medium on the host: (ca, cb, da, db) dense (nz, ny, nx) arrays."""
+    out = out or [np.empty((nz, ny, nx), np.float32) for _ in range(4)]
+    _check(lib().yb_host_medium(nx, ny, nz, eps_seed, sigma_seed,
+                                *[None if a is None else _fp(a) for a in out]))
+    return out
+
+
+def host_fields(nx, ny, nz, seed, out=None):
+    """Pinned seeded fields on the host (dense reference layout)."""
+    out = out or [np.empty(comp_extents(nx, ny, nz, c)[::-1], np.float32) for c in range(6)]
+    for c in range(6):
+        _check(lib().yb_host_field(nx, ny, nz, seed, c, _fp(out[c])))
+    return out
+
+
+def run_simulation(nx, ny, nz, fields, nsteps, step0=0, sources=(), medium=None, cells=None,
+                   variant=VARIANT_FUSED, device=0):
+    """run_simulation (runner.hpp:349-362) mirror: copy the host state in, advance, copy out.
+
+    medium=(eps_seed, sigma_seed) generates the pinned medium on the device;
+    cells={CA: arr, ...} uploads per-cell coefficient arrays instead.
+    Returns the new host state (list of six dense arrays)."""
+    with Simulation(nx, ny, nz, device=device, variant=variant) as sim:
+        if medium is not None:
+            sim.generate_medium(*medium)
+        for w, a in (cells or {}).items():
+            sim.set_cell_coeffs(w, a)
+        for s in sources:
+            sim.add_source(*s)
+        sim.upload(fields)
+        sim.step_index = step0
+        sim.run(nsteps)
+        return sim.download()

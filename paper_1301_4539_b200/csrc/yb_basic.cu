@@ -1,0 +1,253 @@
+// yb_basic.cu — per-DoF kernels (the NAIVE variant and the reference range
+// operations), the boundary-face kernel of the FUSED variant, and the
+// device-side seeded initialisers.
+//
+// Reference semantics followed (paths under /root/reference/proj/include/yeeblock):
+//   Ampere  update_e_dof kernels.hpp:27-44 over curl_updatable_box staggering.hpp:70-77
+//   Faraday update_h_dof kernels.hpp:46-63 over comp_extents staggering.hpp:44-49
+//   PEC     apply_pec_boundary kernels.hpp:146-155 / pec_boxes staggering.hpp:81-86
+//   Source  inject_current source.hpp:61-68
+#include <cuda_runtime.h>
+
+#include "../../include/yeeb200_inputs.h"
+#include "yb_device.cuh"
+#include "yb_launch.h"
+
+namespace yb {
+
+namespace {
+
+__device__ __forceinline__ float coefA(const float* cell, float s, long long p) {
+  return cell ? cell[p] : s;
+}
+__device__ __forceinline__ float coefB(const float* cell, const float* axis, int ax, long long p) {
+  return cell ? cell[p] : axis[ax];
+}
+
+struct Box {
+  int xlo, xhi, ylo, yhi, zlo, zhi;
+};
+
+__device__ __forceinline__ bool in_box(const Box& b, int i, int j, int k) {
+  return i >= b.xlo && i < b.xhi && j >= b.ylo && j < b.yhi && k >= b.zlo && k < b.zhi;
+}
+
+// One thread per node-box point (i,j,k), all three E components.
+__global__ void k_naive_ampere(Geo g, Fields F, CoefArgs co, Box b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i > g.nx || !in_box(b, i, j, k)) return;
+  const long long p = gidx(g, i, j, k);
+  float *ex = F.f[0], *ey = F.f[1], *ez = F.f[2];
+  const float *hx = F.f[3], *hy = F.f[4], *hz = F.f[5];
+  const float A = coefA(co.cell[0], co.ca_s, p);
+  const bool ji = j >= 1 && j < g.ny, ki = k >= 1 && k < g.nz, ii = i >= 1 && i < g.nx;
+  if (i < g.nx && ji && ki)  // ex: (h,n,n)
+    ex[p] = yee_upd(A, ex[p], coefB(co.cell[1], co.cdy_e, j, p), hz[p], hz[p - g.PX],
+                    coefB(co.cell[1], co.cdz_e, k, p), hy[p], hy[p - g.plane]);
+  if (ii && j < g.ny && ki)  // ey: (n,h,n)
+    ey[p] = yee_upd(A, ey[p], coefB(co.cell[1], co.cdz_e, k, p), hx[p], hx[p - g.plane],
+                    coefB(co.cell[1], co.cdx_e, i, p), hz[p], hz[p - 1]);
+  if (ii && ji && k < g.nz)  // ez: (n,n,h)
+    ez[p] = yee_upd(A, ez[p], coefB(co.cell[1], co.cdx_e, i, p), hy[p], hy[p - 1],
+                    coefB(co.cell[1], co.cdy_e, j, p), hx[p], hx[p - g.PX]);
+}
+
+__global__ void k_naive_faraday(Geo g, Fields F, CoefArgs co, Box b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i > g.nx || !in_box(b, i, j, k)) return;
+  const long long p = gidx(g, i, j, k);
+  const float *ex = F.f[0], *ey = F.f[1], *ez = F.f[2];
+  float *hx = F.f[3], *hy = F.f[4], *hz = F.f[5];
+  const float A = coefA(co.cell[2], co.da_s, p);
+  if (j < g.ny && k < g.nz)  // hx: (nx+1) x ny x nz
+    hx[p] = yee_upd(A, hx[p], coefB(co.cell[3], co.cdz_h, k, p), ey[p + g.plane], ey[p],
+                    coefB(co.cell[3], co.cdy_h, j, p), ez[p + g.PX], ez[p]);
+  if (i < g.nx && k < g.nz)  // hy: nx x (ny+1) x nz
+    hy[p] = yee_upd(A, hy[p], coefB(co.cell[3], co.cdx_h, i, p), ez[p + 1], ez[p],
+                    coefB(co.cell[3], co.cdz_h, k, p), ex[p + g.plane], ex[p]);
+  if (i < g.nx && j < g.ny)  // hz: nx x ny x (nz+1)
+    hz[p] = yee_upd(A, hz[p], coefB(co.cell[3], co.cdy_h, j, p), ex[p + g.PX], ex[p],
+                    coefB(co.cell[3], co.cdx_h, i, p), ey[p + 1], ey[p]);
+}
+
+// Tangential E on the six faces := +0 (node-axis planes 0 and n).
+__global__ void k_naive_pec(Geo g, Fields F) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i > g.nx) return;
+  const long long p = gidx(g, i, j, k);
+  const bool bi = i == 0 || i == g.nx, bj = j == 0 || j == g.ny, bk = k == 0 || k == g.nz;
+  if (i < g.nx && (bj || bk)) F.f[0][p] = 0.0f;
+  if (j < g.ny && (bi || bk)) F.f[1][p] = 0.0f;
+  if (k < g.nz && (bi || bj)) F.f[2][p] = 0.0f;
+}
+
+__global__ void k_sources(Geo g, Fields F, SrcArgs s) {
+  if (threadIdx.x != 0) return;
+  for (int q = 0; q < s.n; ++q) {
+    float* a = F.f[s.comp[q]];
+    const long long p = gidx(g, s.i[q], s.j[q], s.k[q]);
+    a[p] = __fadd_rn(a[p], s.val[q]);
+  }
+}
+
+// FUSED-variant companion: the DoFs on the three upper faces (i=nx, j=ny,
+// k=nz) that the cell-box sweep does not own. Tangential E there is PEC
+// (written +0); the normal H (hx at i=nx, hy at j=ny, hz at k=nz) reads only
+// those PEC zeros, so its update is Da*h + (Db*(0-0) - Db*(0-0)), computed
+// in exactly that form. Reads `in`, writes `out` (disjoint from the sweep).
+__global__ void k_faces(Geo g, Fields in, Fields out, CoefArgs co) {
+  const long long nxf = (long long)(g.ny + 1) * (g.nz + 1);
+  const long long nyf = (long long)(g.nx + 1) * (g.nz + 1);
+  const long long nzf = (long long)(g.nx + 1) * (g.ny + 1);
+  const long long total = nxf + nyf + nzf;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    if (t < nxf) {
+      const int j = (int)(t % (g.ny + 1)), k = (int)(t / (g.ny + 1)), i = g.nx;
+      const long long p = gidx(g, i, j, k);
+      if (j < g.ny) out.f[1][p] = 0.0f;
+      if (k < g.nz) out.f[2][p] = 0.0f;
+      if (j < g.ny && k < g.nz)
+        out.f[3][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in.f[3][p],
+                              coefB(co.cell[3], co.cdz_h, k, p), 0.0f, 0.0f,
+                              coefB(co.cell[3], co.cdy_h, j, p), 0.0f, 0.0f);
+    } else if (t < nxf + nyf) {
+      const long long u = t - nxf;
+      const int i = (int)(u % (g.nx + 1)), k = (int)(u / (g.nx + 1)), j = g.ny;
+      const long long p = gidx(g, i, j, k);
+      if (i < g.nx) out.f[0][p] = 0.0f;
+      if (k < g.nz) out.f[2][p] = 0.0f;
+      if (i < g.nx && k < g.nz)
+        out.f[4][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in.f[4][p],
+                              coefB(co.cell[3], co.cdx_h, i, p), 0.0f, 0.0f,
+                              coefB(co.cell[3], co.cdz_h, k, p), 0.0f, 0.0f);
+    } else {
+      const long long u = t - nxf - nyf;
+      const int i = (int)(u % (g.nx + 1)), j = (int)(u / (g.nx + 1)), k = g.nz;
+      const long long p = gidx(g, i, j, k);
+      if (i < g.nx) out.f[0][p] = 0.0f;
+      if (j < g.ny) out.f[1][p] = 0.0f;
+      if (i < g.nx && j < g.ny)
+        out.f[5][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in.f[5][p],
+                              coefB(co.cell[3], co.cdy_h, j, p), 0.0f, 0.0f,
+                              coefB(co.cell[3], co.cdx_h, i, p), 0.0f, 0.0f);
+    }
+  }
+}
+
+__device__ __forceinline__ void comp_ext(const Geo& g, int c, int e[3]) {
+  const int n[3] = {g.nx, g.ny, g.nz};
+  const int axis = c % 3;
+  for (int a = 0; a < 3; ++a) {
+    const bool node = c < 3 ? (a != axis) : (a == axis);
+    e[a] = n[a] + (node ? 1 : 0);
+  }
+}
+
+// Seeded fields over each component's extents (dense reference index).
+__global__ void k_fill_fields(Geo g, Fields F, uint64_t seed) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i > g.nx) return;
+  const long long p = gidx(g, i, j, k);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    int e[3];
+    comp_ext(g, c, e);
+    if (i < e[0] && j < e[1] && k < e[2]) {
+      const uint64_t dense = ((uint64_t)k * e[1] + j) * e[0] + i;
+      F.f[c][p] = yb_field_value(seed, c, dense);
+    }
+  }
+}
+
+// Pinned medium over the node box with clamped cell index.
+__global__ void k_medium(Geo g, float* ca, float* cb, float* da, float* db, long long eps_seed,
+                         long long sigma_seed, float S) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i > g.nx) return;
+  const int ci = min(i, g.nx - 1), cj = min(j, g.ny - 1), ck = min(k, g.nz - 1);
+  const uint64_t cell = ((uint64_t)ck * g.ny + cj) * g.nx + ci;
+  const yb_cell_coeffs q = yb_cell_coeffs_at(eps_seed, sigma_seed, cell, S);
+  const long long p = gidx(g, i, j, k);
+  if (ca) ca[p] = q.ca;
+  if (cb) cb[p] = q.cb;
+  if (da) da[p] = q.da;
+  if (db) db[p] = q.db;
+}
+
+// After a dense upload into [0,nx)x[0,ny)x[0,nz): fill the clamped
+// duplicates at i=nx, j=ny, k=nz.
+__global__ void k_clamp_fill(Geo g, float* a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i > g.nx) return;
+  if (i < g.nx && j < g.ny && k < g.nz) return;
+  a[gidx(g, i, j, k)] = a[gidx(g, min(i, g.nx - 1), min(j, g.ny - 1), min(k, g.nz - 1))];
+}
+
+dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + 1 + bx - 1) / bx, g.ny + 1, g.nz + 1); }
+
+}  // namespace
+
+cudaError_t launch_naive_ampere(const Geo& g, const Fields& F, const CoefArgs& co, const int* box,
+                                cudaStream_t st) {
+  const Box b{box[0], box[1], box[2], box[3], box[4], box[5]};
+  k_naive_ampere<<<node_grid(g, 128), 128, 0, st>>>(g, F, co, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_naive_faraday(const Geo& g, const Fields& F, const CoefArgs& co, const int* box,
+                                 cudaStream_t st) {
+  const Box b{box[0], box[1], box[2], box[3], box[4], box[5]};
+  k_naive_faraday<<<node_grid(g, 128), 128, 0, st>>>(g, F, co, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_naive_pec(const Geo& g, const Fields& F, cudaStream_t st) {
+  k_naive_pec<<<node_grid(g, 128), 128, 0, st>>>(g, F);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sources(const Geo& g, const Fields& F, const SrcArgs& s, cudaStream_t st) {
+  k_sources<<<1, 32, 0, st>>>(g, F, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_faces(const Geo& g, const Fields& in, const Fields& out, const CoefArgs& co,
+                         int num_sms, cudaStream_t st) {
+  const long long total = (long long)(g.ny + 1) * (g.nz + 1) + (long long)(g.nx + 1) * (g.nz + 1) +
+                          (long long)(g.nx + 1) * (g.ny + 1);
+  long long blocks = (total + 255) / 256;
+  if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
+  k_faces<<<(unsigned)blocks, 256, 0, st>>>(g, in, out, co);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_fields(const Geo& g, const Fields& F, uint64_t seed, cudaStream_t st) {
+  k_fill_fields<<<node_grid(g, 128), 128, 0, st>>>(g, F, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_medium(const Geo& g, float* ca, float* cb, float* da, float* db,
+                          long long eps_seed, long long sigma_seed, float S, cudaStream_t st) {
+  k_medium<<<node_grid(g, 128), 128, 0, st>>>(g, ca, cb, da, db, eps_seed, sigma_seed, S);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_clamp_fill(const Geo& g, float* a, cudaStream_t st) {
+  k_clamp_fill<<<node_grid(g, 128), 128, 0, st>>>(g, a);
+  return cudaGetLastError();
+}
+
+}  // namespace yb

@@ -1,0 +1,778 @@
+// yb_capi.cu — the C-ABI of libyeeb200.so (include/yeeb200.h): device-resident
+// padded SoA state, coefficient management, TMA descriptor setup and the
+// Standard-step time loop. Host side of the B200 path; no CPU compute path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/yeeb200.h"
+#include "../../include/yeeb200_inputs.h"
+#include "yb_launch.h"
+
+using yb::Geo;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define YB_CU(expr)                                                                       \
+  do {                                                                                    \
+    const cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(YB_CUDA_ERROR, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                              \
+  } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+struct Src {
+  int comp, i, j, k;
+  std::vector<float> table;
+};
+
+struct TimerPair {
+  cudaEvent_t a, b;
+};
+
+int comp_ext(const Geo& g, int c, int e[3]) {
+  const int n[3] = {g.nx, g.ny, g.nz};
+  const int axis = c % 3;
+  for (int a = 0; a < 3; ++a) {
+    const bool node = c < 3 ? (a != axis) : (a == axis);
+    e[a] = n[a] + (node ? 1 : 0);
+  }
+  return 0;
+}
+
+}  // namespace
+
+struct yb_sim {
+  Geo g{};
+  int device = 0, variant = YB_VARIANT_FUSED, zchunk_req = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  float* buf[2][6] = {};
+  int cur = 0;
+  float* cell[4] = {};  // per-cell arrays (nullptr = uniform / axis)
+  float ca_s = 1.0f, da_s = 1.0f;
+  bool cb_uniform = false, db_uniform = false;
+  float cb_u = 0.f, db_u = 0.f;
+  std::vector<float> axis_ref[3];  // reference per-axis coefficients (host copy)
+  float* axis_dev[6] = {};         // cdx_e, cdy_e, cdz_e, cdx_h, cdy_h, cdz_h
+  int axis_len[3] = {};
+  std::vector<Src> sources;
+  int64_t step_index = 0, steps = 0, launches = 0;
+  yb::TMaps tm[2];
+  bool tm_valid = false;
+  bool timing = false;
+  std::vector<TimerPair> timers;
+  size_t timers_used = 0;
+  double kernel_ms = 0.0;
+  int64_t kernel_timed = 0;
+  size_t dev_bytes = 0;
+  int stages = 0;
+  dim3 grid{1, 1, 1};
+  int zchunk = 0;
+};
+
+namespace {
+
+int cell_mask(const yb_sim* s) {
+  int m = 0;
+  for (int q = 0; q < 4; ++q)
+    if (s->cell[q]) m |= 1 << q;
+  return m;
+}
+
+int popcount4(int m) { return (m & 1) + ((m >> 1) & 1) + ((m >> 2) & 1) + ((m >> 3) & 1); }
+
+int upload_axis(yb_sim* s) {
+  for (int side = 0; side < 2; ++side) {
+    const bool uni = side == 0 ? s->cb_uniform : s->db_uniform;
+    const float uv = side == 0 ? s->cb_u : s->db_u;
+    for (int a = 0; a < 3; ++a) {
+      std::vector<float> h(s->axis_len[a], 0.0f);
+      const int n = a == 0 ? s->g.nx : (a == 1 ? s->g.ny : s->g.nz);
+      for (int q = 0; q < n; ++q) h[q] = uni ? uv : s->axis_ref[a][q];
+      YB_CU(cudaMemcpyAsync(s->axis_dev[side * 3 + a], h.data(), h.size() * sizeof(float),
+                            cudaMemcpyHostToDevice, s->stream));
+    }
+  }
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+yb::CoefArgs coef_args(const yb_sim* s) {
+  yb::CoefArgs c{};
+  for (int q = 0; q < 4; ++q) c.cell[q] = s->cell[q];
+  c.ca_s = s->ca_s;
+  c.da_s = s->da_s;
+  c.cdx_e = s->axis_dev[0];
+  c.cdy_e = s->axis_dev[1];
+  c.cdz_e = s->axis_dev[2];
+  c.cdx_h = s->axis_dev[3];
+  c.cdy_h = s->axis_dev[4];
+  c.cdz_h = s->axis_dev[5];
+  return c;
+}
+
+yb::Fields fields_of(const yb_sim* s, int b) {
+  yb::Fields F;
+  for (int c = 0; c < 6; ++c) F.f[c] = s->buf[b][c];
+  return F;
+}
+
+int encode_map(CUtensorMap* m, const Geo& g, float* base) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.PX * 4, (cuuint64_t)g.plane * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)yb::kBY, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return YB_OK;
+}
+
+// (Re)build TMA descriptors and the launch shape for the current coefficient set.
+int prepare_fused(yb_sim* s) {
+  if (s->tm_valid) return YB_OK;
+  const int mask = cell_mask(s);
+  const int narr = 6 + popcount4(mask);
+  for (int b = 0; b < 2; ++b) {
+    int q = 0;
+    for (int c = 0; c < 6; ++c)
+      if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->buf[b][c])) return rc;
+    for (int a = 0; a < 4; ++a)
+      if (s->cell[a])
+        if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->cell[a])) return rc;
+  }
+  const size_t avail = 227 * 1024;
+  int S = 5;
+  while (S > 2 && yb::fused_smem_bytes(narr, S) > avail) --S;
+  s->stages = S;
+  const int tx = (s->g.nx + yb::kTX - 1) / yb::kTX;
+  const int ty = (s->g.ny + yb::kTY - 1) / yb::kTY;
+  int zc = s->zchunk_req;
+  if (zc <= 0) {
+    // minimise waves x (planes per chunk + ~1.3 extra planes per chunk)
+    const long long T = (long long)tx * ty;
+    double best = 1e300;
+    for (int Z = 1; Z <= s->g.nz; ++Z) {
+      const int len = (s->g.nz + Z - 1) / Z;
+      const int Zr = (s->g.nz + len - 1) / len;
+      const long long waves = (T * Zr + s->num_sms - 1) / s->num_sms;
+      const double cost = (double)waves * (len + 1.3);
+      if (cost < best - 1e-9) {
+        best = cost;
+        zc = len;
+      }
+    }
+  }
+  zc = std::min(std::max(zc, 1), s->g.nz);
+  s->zchunk = zc;
+  s->grid = dim3(tx, ty, (s->g.nz + zc - 1) / zc);
+  s->tm_valid = true;
+  return YB_OK;
+}
+
+yb::SrcArgs sources_at(const yb_sim* s, int64_t step) {
+  yb::SrcArgs a{};
+  for (const Src& q : s->sources) {
+    if (step < 0 || step >= (int64_t)q.table.size()) continue;
+    a.comp[a.n] = q.comp;
+    a.i[a.n] = q.i;
+    a.j[a.n] = q.j;
+    a.k[a.n] = q.k;
+    a.val[a.n] = q.table[step];
+    ++a.n;
+  }
+  return a;
+}
+
+int collect_timers(yb_sim* s) {
+  if (s->timers_used == 0) return YB_OK;
+  YB_CU(cudaStreamSynchronize(s->stream));
+  for (size_t q = 0; q < s->timers_used; ++q) {
+    float ms = 0.f;
+    YB_CU(cudaEventElapsedTime(&ms, s->timers[q].a, s->timers[q].b));
+    s->kernel_ms += ms;
+    ++s->kernel_timed;
+  }
+  s->timers_used = 0;
+  return YB_OK;
+}
+
+int step_fused(yb_sim* s) {
+  const int nxt = s->cur ^ 1;
+  yb::FusedArgs a{};
+  a.g = s->g;
+  a.nstages = s->stages;
+  a.zchunk = s->zchunk;
+  a.co = coef_args(s);
+  for (int c = 0; c < 6; ++c) {
+    a.in[c] = s->buf[s->cur][c];
+    a.out[c] = s->buf[nxt][c];
+  }
+  a.src = sources_at(s, s->step_index);
+  const int mask = cell_mask(s);
+  const size_t smem = yb::fused_smem_bytes(6 + popcount4(mask), s->stages);
+  TimerPair* tp = nullptr;
+  if (s->timing) {
+    if (s->timers_used == s->timers.size()) {
+      TimerPair p;
+      YB_CU(cudaEventCreate(&p.a));
+      YB_CU(cudaEventCreate(&p.b));
+      s->timers.push_back(p);
+    }
+    tp = &s->timers[s->timers_used++];
+    YB_CU(cudaEventRecord(tp->a, s->stream));
+  }
+  YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, s->grid, smem, s->stream));
+  if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
+  YB_CU(yb::launch_faces(s->g, fields_of(s, s->cur), fields_of(s, nxt), a.co, s->num_sms,
+                         s->stream));
+  s->launches += 2;
+  s->cur = nxt;
+  if (s->timers_used >= 4096) return collect_timers(s);
+  return YB_OK;
+}
+
+int step_naive(yb_sim* s) {
+  const int box[6] = {0, s->g.nx + 1, 0, s->g.ny + 1, 0, s->g.nz + 1};
+  const yb::Fields F = fields_of(s, s->cur);
+  const yb::CoefArgs co = coef_args(s);
+  TimerPair* tp = nullptr;
+  if (s->timing) {
+    if (s->timers_used == s->timers.size()) {
+      TimerPair p;
+      YB_CU(cudaEventCreate(&p.a));
+      YB_CU(cudaEventCreate(&p.b));
+      s->timers.push_back(p);
+    }
+    tp = &s->timers[s->timers_used++];
+    YB_CU(cudaEventRecord(tp->a, s->stream));
+  }
+  YB_CU(yb::launch_naive_ampere(s->g, F, co, box, s->stream));
+  YB_CU(yb::launch_naive_pec(s->g, F, s->stream));
+  const yb::SrcArgs src = sources_at(s, s->step_index);
+  int n = 3;
+  if (src.n) {
+    YB_CU(yb::launch_sources(s->g, F, src, s->stream));
+    ++n;
+  }
+  YB_CU(yb::launch_naive_faraday(s->g, F, co, box, s->stream));
+  if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
+  s->launches += n;
+  if (s->timers_used >= 4096) return collect_timers(s);
+  return YB_OK;
+}
+
+int check_comp(int comp) {
+  if (comp < 0 || comp > 5) return fail(YB_INVALID_ARGUMENT, "component %d out of [0,5]", comp);
+  return YB_OK;
+}
+
+int copy_dense(yb_sim* s, int comp, float* dev, const float* hsrc, float* hdst) {
+  int e[3];
+  comp_ext(s->g, comp, e);
+  cudaMemcpy3DParms p = {};
+  p.extent = make_cudaExtent((size_t)e[0] * 4, e[1], e[2]);
+  if (hsrc) {
+    p.srcPtr = make_cudaPitchedPtr(const_cast<float*>(hsrc), (size_t)e[0] * 4, e[0], e[1]);
+    p.dstPtr = make_cudaPitchedPtr(dev, (size_t)s->g.PX * 4, s->g.PX, s->g.PY);
+    p.kind = cudaMemcpyHostToDevice;
+  } else {
+    p.srcPtr = make_cudaPitchedPtr(dev, (size_t)s->g.PX * 4, s->g.PX, s->g.PY);
+    p.dstPtr = make_cudaPitchedPtr(hdst, (size_t)e[0] * 4, e[0], e[1]);
+    p.kind = cudaMemcpyDeviceToHost;
+  }
+  YB_CU(cudaMemcpy3DAsync(&p, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+float courant() {
+  const uint32_t b = YB_S_BITS;
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* yb_last_error(void) { return g_err.c_str(); }
+int yb_abi_version(void) { return YB_ABI_VERSION; }
+
+int yb_create(const yb_desc* d, yb_sim** out) {
+  if (!d || !out) return fail(YB_INVALID_ARGUMENT, "yb_create: null argument");
+  *out = nullptr;
+  if (d->nx < 1 || d->ny < 1 || d->nz < 1)
+    return fail(YB_INVALID_ARGUMENT, "GridSpec: cell counts must be positive");
+  if (d->ny > 65000 || d->nz > 65000 || d->nx > (1 << 24))
+    return fail(YB_INVALID_ARGUMENT, "grid too large for this build");
+  if (d->variant != YB_VARIANT_FUSED && d->variant != YB_VARIANT_NAIVE)
+    return fail(YB_INVALID_ARGUMENT, "unknown variant %d", d->variant);
+  YB_CU(cudaSetDevice(d->device));
+  yb_sim* s = new yb_sim;
+  s->device = d->device;
+  s->variant = d->variant;
+  s->zchunk_req = d->zchunk;
+  Geo& g = s->g;
+  g.nx = d->nx;
+  g.ny = d->ny;
+  g.nz = d->nz;
+  g.PX = ((d->nx + 1 + 31) / 32) * 32;
+  g.PY = d->ny + 1;
+  g.PZ = d->nz + 1;
+  g.plane = (long long)g.PX * g.PY;
+  g.total = g.plane * (g.PZ + 2);  // +2 guard planes for masked over-reads
+  int dev_sms = 0;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, d->device);
+  if (dev_sms > 0) s->num_sms = dev_sms;
+  auto bail = [&](int rc) {
+    yb_destroy(s);
+    return rc;
+  };
+  if (cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(YB_CUDA_ERROR, "stream create failed"));
+  s->stream = s->own_stream;
+  const size_t bytes = (size_t)g.total * sizeof(float);
+  for (int b = 0; b < 2; ++b)
+    for (int c = 0; c < 6; ++c) {
+      if (cudaMalloc(&s->buf[b][c], bytes) != cudaSuccess)
+        return bail(fail(YB_CUDA_ERROR, "cudaMalloc of %zu bytes failed", bytes));
+      s->dev_bytes += bytes;
+      if (cudaMemsetAsync(s->buf[b][c], 0, bytes, s->stream) != cudaSuccess)
+        return bail(fail(YB_CUDA_ERROR, "memset failed"));
+    }
+  const int ns[3] = {g.nx, g.ny, g.nz};
+  for (int a = 0; a < 3; ++a) {
+    s->axis_len[a] = ((ns[a] + yb::kTX) / yb::kTX + 1) * yb::kTX + 64;
+    s->axis_ref[a].assign(ns[a], 0.0f);
+  }
+  for (int q = 0; q < 6; ++q) {
+    const size_t ab = (size_t)s->axis_len[q % 3] * sizeof(float);
+    if (cudaMalloc(&s->axis_dev[q], ab) != cudaSuccess)
+      return bail(fail(YB_CUDA_ERROR, "cudaMalloc failed"));
+    s->dev_bytes += ab;
+  }
+  if (int rc = upload_axis(s)) return bail(rc);
+  static bool limits_set = false;
+  if (!limits_set) {
+    if (yb::fused_set_smem_limits() != cudaSuccess)
+      return bail(fail(YB_CUDA_ERROR, "cudaFuncSetAttribute failed"));
+    limits_set = true;
+  }
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess)
+    return bail(fail(YB_CUDA_ERROR, "init sync failed"));
+  *out = s;
+  return YB_OK;
+}
+
+int yb_destroy(yb_sim* s) {
+  if (!s) return YB_OK;
+  cudaSetDevice(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (int b = 0; b < 2; ++b)
+    for (int c = 0; c < 6; ++c) cudaFree(s->buf[b][c]);
+  for (int q = 0; q < 4; ++q) cudaFree(s->cell[q]);
+  for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
+  for (auto& t : s->timers) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  if (s->own_stream) cudaStreamDestroy(s->own_stream);
+  delete s;
+  return YB_OK;
+}
+
+int yb_set_axis_coeffs(yb_sim* s, const float* cdx, const float* cdy, const float* cdz) {
+  if (!s || !cdx || !cdy || !cdz) return fail(YB_INVALID_ARGUMENT, "null argument");
+  YB_CU(cudaSetDevice(s->device));
+  s->axis_ref[0].assign(cdx, cdx + s->g.nx);
+  s->axis_ref[1].assign(cdy, cdy + s->g.ny);
+  s->axis_ref[2].assign(cdz, cdz + s->g.nz);
+  return upload_axis(s);
+}
+
+int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
+  YB_CU(cudaSetDevice(s->device));
+  const long long n = (long long)s->g.nx * s->g.ny * s->g.nz;
+  bool all_equal = false;
+  float v = uniform;
+  if (cells) {
+    all_equal = true;
+    v = cells[0];
+    for (long long q = 1; q < n && all_equal; ++q)
+      if (std::memcmp(&cells[q], &v, 4) != 0) all_equal = false;
+  }
+  s->tm_valid = false;
+  if (!cells || all_equal) {
+    if (s->cell[which]) {
+      YB_CU(cudaFree(s->cell[which]));
+      s->cell[which] = nullptr;
+      s->dev_bytes -= (size_t)s->g.total * 4;
+    }
+    if (which == YB_CA) s->ca_s = v;
+    if (which == YB_DA) s->da_s = v;
+    if (which == YB_CB) {
+      s->cb_uniform = cells != nullptr;
+      s->cb_u = v;
+    }
+    if (which == YB_DB) {
+      s->db_uniform = cells != nullptr;
+      s->db_u = v;
+    }
+    if (which == YB_CB || which == YB_DB) return upload_axis(s);
+    return YB_OK;
+  }
+  if (which == YB_CB) s->cb_uniform = false;
+  if (which == YB_DB) s->db_uniform = false;
+  if (!s->cell[which]) {
+    YB_CU(cudaMalloc(&s->cell[which], (size_t)s->g.total * 4));
+    YB_CU(cudaMemsetAsync(s->cell[which], 0, (size_t)s->g.total * 4, s->stream));
+    s->dev_bytes += (size_t)s->g.total * 4;
+  }
+  cudaMemcpy3DParms p = {};
+  p.extent = make_cudaExtent((size_t)s->g.nx * 4, s->g.ny, s->g.nz);
+  p.srcPtr = make_cudaPitchedPtr(const_cast<float*>(cells), (size_t)s->g.nx * 4, s->g.nx, s->g.ny);
+  p.dstPtr = make_cudaPitchedPtr(s->cell[which], (size_t)s->g.PX * 4, s->g.PX, s->g.PY);
+  p.kind = cudaMemcpyHostToDevice;
+  YB_CU(cudaMemcpy3DAsync(&p, s->stream));
+  YB_CU(yb::launch_clamp_fill(s->g, s->cell[which], s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_generate_medium(yb_sim* s, int64_t eps_seed, int64_t sigma_seed) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  const float S = courant();
+  s->tm_valid = false;
+  auto ensure = [&](int q) -> int {
+    if (!s->cell[q]) {
+      YB_CU(cudaMalloc(&s->cell[q], (size_t)s->g.total * 4));
+      YB_CU(cudaMemsetAsync(s->cell[q], 0, (size_t)s->g.total * 4, s->stream));
+      s->dev_bytes += (size_t)s->g.total * 4;
+    }
+    return YB_OK;
+  };
+  auto drop = [&](int q) -> int {
+    if (s->cell[q]) {
+      YB_CU(cudaFree(s->cell[q]));
+      s->cell[q] = nullptr;
+      s->dev_bytes -= (size_t)s->g.total * 4;
+    }
+    return YB_OK;
+  };
+  if (eps_seed < 0 && sigma_seed < 0) {  // vacuum: the grid's own coefficients
+    for (int q = 0; q < 4; ++q)
+      if (int rc = drop(q)) return rc;
+    s->ca_s = s->da_s = 1.0f;
+    s->cb_uniform = s->db_uniform = false;
+    return upload_axis(s);
+  }
+  if (sigma_seed < 0) {  // lossless dielectric: Ca = Da = 1, Db = S exactly
+    for (int q : {YB_CA, YB_DA, YB_DB})
+      if (int rc = drop(q)) return rc;
+    if (int rc = ensure(YB_CB)) return rc;
+    s->ca_s = s->da_s = 1.0f;
+    s->cb_uniform = false;
+    s->db_uniform = true;
+    s->db_u = S;
+    YB_CU(yb::launch_medium(s->g, nullptr, s->cell[YB_CB], nullptr, nullptr, eps_seed, sigma_seed,
+                            S, s->stream));
+    return upload_axis(s);
+  }
+  for (int q = 0; q < 4; ++q)
+    if (int rc = ensure(q)) return rc;
+  s->cb_uniform = s->db_uniform = false;
+  YB_CU(yb::launch_medium(s->g, s->cell[0], s->cell[1], s->cell[2], s->cell[3], eps_seed,
+                          sigma_seed, S, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_host_medium(int nx, int ny, int nz, int64_t eps_seed, int64_t sigma_seed, float* ca,
+                   float* cb, float* da, float* db) {
+  if (nx < 1 || ny < 1 || nz < 1) return fail(YB_INVALID_ARGUMENT, "bad grid");
+  const float S = courant();
+  const long long n = (long long)nx * ny * nz;
+  for (long long q = 0; q < n; ++q) {
+    const yb_cell_coeffs c = yb_cell_coeffs_at(eps_seed, sigma_seed, (uint64_t)q, S);
+    if (ca) ca[q] = c.ca;
+    if (cb) cb[q] = c.cb;
+    if (da) da[q] = c.da;
+    if (db) db[q] = c.db;
+  }
+  return YB_OK;
+}
+
+int yb_host_field(int nx, int ny, int nz, uint64_t seed, int comp, float* dense) {
+  if (nx < 1 || ny < 1 || nz < 1 || !dense) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  if (int rc = check_comp(comp)) return rc;
+  Geo g{};
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = nz;
+  int e[3];
+  comp_ext(g, comp, e);
+  const long long n = (long long)e[0] * e[1] * e[2];
+  for (long long q = 0; q < n; ++q) dense[q] = yb_field_value(seed, comp, (uint64_t)q);
+  return YB_OK;
+}
+
+int yb_upload_field(yb_sim* s, int comp, const float* dense) {
+  if (!s || !dense) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (int rc = check_comp(comp)) return rc;
+  YB_CU(cudaSetDevice(s->device));
+  return copy_dense(s, comp, s->buf[s->cur][comp], dense, nullptr);
+}
+
+int yb_download_field(yb_sim* s, int comp, float* dense) {
+  if (!s || !dense) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (int rc = check_comp(comp)) return rc;
+  YB_CU(cudaSetDevice(s->device));
+  return copy_dense(s, comp, s->buf[s->cur][comp], nullptr, dense);
+}
+
+int yb_zero_fields(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  for (int c = 0; c < 6; ++c)
+    YB_CU(cudaMemsetAsync(s->buf[s->cur][c], 0, (size_t)s->g.total * 4, s->stream));
+  s->step_index = 0;
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_fill_fields(yb_sim* s, uint64_t seed) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(yb::launch_fill_fields(s->g, fields_of(s, s->cur), seed, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_set_step_index(yb_sim* s, int64_t v) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (v < 0) return fail(YB_INVALID_ARGUMENT, "negative step index");
+  s->step_index = v;
+  return YB_OK;
+}
+
+int yb_get_step_index(yb_sim* s, int64_t* v) {
+  if (!s || !v) return fail(YB_INVALID_ARGUMENT, "null argument");
+  *v = s->step_index;
+  return YB_OK;
+}
+
+int yb_add_source(yb_sim* s, int comp, int i, int j, int k, const float* table, int64_t n) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (comp < 0 || comp > 2) return fail(YB_INVALID_ARGUMENT, "SourceSpec: component must be electric");
+  if (n < 0 || (n > 0 && !table)) return fail(YB_INVALID_ARGUMENT, "SourceSpec: bad table");
+  if ((int)s->sources.size() >= YB_MAX_SOURCES)
+    return fail(YB_INVALID_ARGUMENT, "at most %d sources", YB_MAX_SOURCES);
+  // strictly interior (source.hpp:43-55): node axes 1..n-1, the half axis 1..n-2
+  const int idx[3] = {i, j, k};
+  const int ns[3] = {s->g.nx, s->g.ny, s->g.nz};
+  for (int a = 0; a < 3; ++a) {
+    const bool node = a != comp;
+    const int lo = 1, hi = node ? ns[a] : ns[a] - 1;
+    if (idx[a] < lo || idx[a] >= hi) return fail(YB_INVALID_ARGUMENT, "SourceSpec: position not interior");
+  }
+  Src q{comp, i, j, k, std::vector<float>(table, table + n)};
+  s->sources.push_back(std::move(q));
+  return YB_OK;
+}
+
+int yb_clear_sources(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  s->sources.clear();
+  return YB_OK;
+}
+
+int yb_advance(yb_sim* s, int64_t nsteps) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
+  YB_CU(cudaSetDevice(s->device));
+  if (s->variant == YB_VARIANT_FUSED)
+    if (int rc = prepare_fused(s)) return rc;
+  for (int64_t t = 0; t < nsteps; ++t) {
+    const int rc = s->variant == YB_VARIANT_FUSED ? step_fused(s) : step_naive(s);
+    if (rc) return rc;
+    ++s->step_index;
+    ++s->steps;
+  }
+  return YB_OK;
+}
+
+int yb_synchronize(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return collect_timers(s);
+}
+
+int yb_advance_timed(yb_sim* s, int64_t nsteps, float* ms) {
+  if (!s || !ms) return fail(YB_INVALID_ARGUMENT, "null argument");
+  YB_CU(cudaSetDevice(s->device));
+  if (s->variant == YB_VARIANT_FUSED)
+    if (int rc = prepare_fused(s)) return rc;
+  cudaEvent_t a, b;
+  YB_CU(cudaEventCreate(&a));
+  YB_CU(cudaEventCreate(&b));
+  YB_CU(cudaEventRecord(a, s->stream));
+  int rc = yb_advance(s, nsteps);
+  if (rc == YB_OK) {
+    YB_CU(cudaEventRecord(b, s->stream));
+    YB_CU(cudaEventSynchronize(b));
+    YB_CU(cudaEventElapsedTime(ms, a, b));
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return rc;
+}
+
+static int check_box(const yb_sim* s, const int* box, int out[6]) {
+  const int full[6] = {0, s->g.nx + 1, 0, s->g.ny + 1, 0, s->g.nz + 1};
+  if (!box) {
+    std::memcpy(out, full, sizeof full);
+    return YB_OK;
+  }
+  const bool empty = box[1] <= box[0] || box[3] <= box[2] || box[5] <= box[4];
+  if (!empty && (box[0] < 0 || box[1] > full[1] || box[2] < 0 || box[3] > full[3] || box[4] < 0 ||
+                 box[5] > full[5]))
+    return fail(YB_OUT_OF_RANGE, "range out of bounds");
+  std::memcpy(out, box, 6 * sizeof(int));
+  return YB_OK;
+}
+
+int yb_apply_ampere_range(yb_sim* s, const int* box) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  int b[6];
+  if (int rc = check_box(s, box, b)) return fail(rc, "apply_ampere_range: range out of bounds");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(yb::launch_naive_ampere(s->g, fields_of(s, s->cur), coef_args(s), b, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_apply_faraday_range(yb_sim* s, const int* box) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  int b[6];
+  if (int rc = check_box(s, box, b)) return fail(rc, "apply_faraday_range: range out of bounds");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(yb::launch_naive_faraday(s->g, fields_of(s, s->cur), coef_args(s), b, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_apply_pec_boundary(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(yb::launch_naive_pec(s->g, fields_of(s, s->cur), s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_field_digest(yb_sim* s, uint64_t* out) {
+  if (!s || !out) return fail(YB_INVALID_ARGUMENT, "null argument");
+  uint64_t h = 1469598103934665603ull;
+  std::vector<float> host;
+  for (int c = 0; c < 6; ++c) {
+    int e[3];
+    comp_ext(s->g, c, e);
+    host.resize((size_t)e[0] * e[1] * e[2]);
+    if (int rc = yb_download_field(s, c, host.data())) return rc;
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(host.data());
+    for (size_t q = 0; q < host.size() * 4; ++q) {
+      h ^= b[q];
+      h *= 1099511628211ull;
+    }
+  }
+  *out = h;
+  return YB_OK;
+}
+
+int yb_set_stream(yb_sim* s, void* stream) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  s->stream = stream ? static_cast<cudaStream_t>(stream) : s->own_stream;
+  return YB_OK;
+}
+
+int yb_set_kernel_timing(yb_sim* s, int on) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (int rc = collect_timers(s)) return rc;
+  s->timing = on != 0;
+  s->kernel_ms = 0.0;
+  s->kernel_timed = 0;
+  return YB_OK;
+}
+
+int yb_get_info(yb_sim* s, yb_info* info) {
+  if (!s || !info) return fail(YB_INVALID_ARGUMENT, "null argument");
+  YB_CU(cudaSetDevice(s->device));
+  if (int rc = collect_timers(s)) return rc;
+  if (s->variant == YB_VARIANT_FUSED)
+    if (int rc = prepare_fused(s)) return rc;
+  std::memset(info, 0, sizeof *info);
+  info->step_index = s->step_index;
+  info->steps = s->steps;
+  info->kernel_launches = s->launches;
+  info->main_kernel_ms = s->kernel_ms;
+  info->main_kernel_timed = s->kernel_timed;
+  info->n_cell_arrays = popcount4(cell_mask(s));
+  info->variant = s->variant;
+  info->stages = s->stages;
+  info->grid_x = (int)s->grid.x;
+  info->grid_y = (int)s->grid.y;
+  info->grid_z = (int)s->grid.z;
+  info->zchunk = s->zchunk;
+  info->bytes_per_cell_update = 48.0 + 4.0 * info->n_cell_arrays;
+  info->device_bytes = s->dev_bytes;
+  return YB_OK;
+}
+
+}  // extern "C"

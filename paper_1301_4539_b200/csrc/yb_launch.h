@@ -1,0 +1,61 @@
+// yb_launch.h — host-side launch wrappers shared between the kernel TUs and
+// the C-ABI implementation (yb_capi.cu). Internal; not part of the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "yb_device.cuh"
+
+namespace yb {
+
+// Fused sweep geometry (yb_fused.cu).
+constexpr int kTX = 128;            // owned cells along x per CTA (32 lanes x float4)
+constexpr int kTY = 8;              // owned rows per CTA; warp kTY computes the +y halo row
+constexpr int kWarps = kTY + 1;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kBX = kTX + 8;        // staged box: x0-4 .. x0+TX+3 (16-byte TMA rows)
+constexpr int kBY = kTY + 2;        // staged box: y0-1 .. y0+TY
+constexpr int kSlot = ((kBX * kBY * 4 + 127) / 128) * 32;  // floats per array slot (128-B aligned)
+constexpr int kEW = kTX + 4;        // E-plane buffer row pitch (TX owned + 1 halo column)
+constexpr int kEPlane = kEW * (kTY + 1);
+constexpr int kMaxArrays = 10;      // 6 fields + up to 4 per-cell coefficient arrays
+
+struct TMaps {
+  CUtensorMap m[kMaxArrays];  // read side: ex..hz of the current state, then cell coeffs
+};
+
+struct FusedArgs {
+  Geo g;
+  int nstages;
+  int zchunk;
+  CoefArgs co;
+  const float* in[6];
+  float* out[6];
+  SrcArgs src;
+};
+
+// smem bytes of the fused kernel for `narr` staged arrays and `stages` ring depth.
+inline size_t fused_smem_bytes(int narr, int stages) {
+  return (size_t)stages * narr * kSlot * 4 + (size_t)9 * kEPlane * 4 + (size_t)stages * 8;
+}
+
+// cell_mask bit q set <=> coefficient array q (Ca,Cb,Da,Db) is per-cell.
+cudaError_t launch_fused(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid,
+                         size_t smem, cudaStream_t st);
+cudaError_t fused_set_smem_limits();
+
+cudaError_t launch_naive_ampere(const Geo& g, const Fields& F, const CoefArgs& co, const int* box,
+                                cudaStream_t st);
+cudaError_t launch_naive_faraday(const Geo& g, const Fields& F, const CoefArgs& co, const int* box,
+                                 cudaStream_t st);
+cudaError_t launch_naive_pec(const Geo& g, const Fields& F, cudaStream_t st);
+cudaError_t launch_sources(const Geo& g, const Fields& F, const SrcArgs& s, cudaStream_t st);
+cudaError_t launch_faces(const Geo& g, const Fields& in, const Fields& out, const CoefArgs& co,
+                         int num_sms, cudaStream_t st);
+cudaError_t launch_fill_fields(const Geo& g, const Fields& F, uint64_t seed, cudaStream_t st);
+cudaError_t launch_medium(const Geo& g, float* ca, float* cb, float* da, float* db,
+                          long long eps_seed, long long sigma_seed, float S, cudaStream_t st);
+cudaError_t launch_clamp_fill(const Geo& g, float* a, cudaStream_t st);
+
+}  // namespace yb

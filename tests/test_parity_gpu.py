@@ -1,0 +1,278 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the C oracle, the
+golden fixtures generated from the compiled reference, and the reference's
+known-answer tests. The bar is bit-exact (every component, every bit): the
+product path is always built in bit-exact form (explicit _rn arithmetic,
+--fmad=false), so the 1e-5 max-relative-error tolerance of north_star is
+also checked (trivially) where stated."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-5  # north_star: max |d| / max |ref| per component
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def gfields(d, prefix):
+    return [np.ascontiguousarray(d[f"{prefix}_{c}"]) for c in ("ex", "ey", "ez", "hx", "hy", "hz")]
+
+
+def assert_bits(a, b, what=""):
+    for c, (x, y) in enumerate(zip(a, b)):
+        assert x.shape == y.shape, (what, c)
+        bad = np.nonzero(x.view(np.uint32) != y.view(np.uint32))
+        assert bad[0].size == 0, f"{what}: comp {c} differs at {len(bad[0])} DoFs, first (k,j,i)=" \
+                                 f"{[int(v[0]) for v in bad]}: {x[tuple(v[0] for v in bad)]} vs " \
+                                 f"{y[tuple(v[0] for v in bad)]}"
+
+
+VARIANTS = [0, 1]  # fused, naive
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_golden_axis_src(yb, variant):
+    d = load("axis_src")
+    nx, ny, nz = (int(v) for v in d["dims"])
+    c, i, j, k = (int(v) for v in d["src"])
+    with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+        sim.add_source(c, i, j, k, d["table"])
+        sim.upload(gfields(d, "in"))
+        sim.run(int(d["steps"]))
+        assert_bits(sim.download(), gfields(d, "out"), "axis_src")
+        assert sim.digest() == int(d["digest"])
+        assert sim.step_index == int(d["steps"])
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_golden_stretched(yb, variant):
+    d = load("stretched")
+    nx, ny, nz = (int(v) for v in d["dims"])
+    with yb.Simulation(nx, ny, nz, variant=variant, cdx=d["cdx"], cdy=d["cdy"], cdz=d["cdz"]) as sim:
+        sim.upload(gfields(d, "in"))
+        sim.run(int(d["steps"]))
+        assert_bits(sim.download(), gfields(d, "out"), "stretched")
+        assert sim.digest() == int(d["digest"])
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_golden_reference_source(yb, variant):
+    d = load("sim_refsrc")
+    nx, ny, nz = (int(v) for v in d["dims"])
+    c, i, j, k = (int(v) for v in d["src"])
+    with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+        sim.add_source(c, i, j, k, d["table"])
+        sim.run(int(d["steps"]))
+        assert_bits(sim.download(), gfields(d, "out"), "sim_refsrc")
+        assert sim.digest() == int(d["digest"])
+
+
+def test_kat_range_ops(yb):
+    n = 4
+    h = np.full(n, 0.5, np.float32)
+    with yb.Simulation(n, n, n, cdx=h, cdy=h, cdz=h) as sim:
+        f = [np.zeros(yb.comp_extents(n, n, n, c)[::-1], np.float32) for c in range(6)]
+        f[5][2, 2, 2] = 1.0
+        sim.upload(f)
+        sim.apply_ampere_range()
+        assert_bits(sim.download(), gfields(load("kat_hz"), "out"), "kat_hz")
+        for name, comp, idx in (("ey", 1, (2, 1, 1)), ("ez", 2, (1, 2, 1))):
+            f = [np.zeros(yb.comp_extents(n, n, n, c)[::-1], np.float32) for c in range(6)]
+            f[comp][idx] = 1.0
+            sim.upload(f)
+            sim.apply_faraday_range()
+            assert_bits(sim.download(), gfields(load("kat_faraday"), name), "kat_faraday")
+        # uniform H has zero curl (kernel_test.cpp:74-82)
+        f = [np.zeros(yb.comp_extents(n, n, n, c)[::-1], np.float32) for c in range(6)]
+        for c in (3, 4, 5):
+            f[c][...] = 3.25
+        sim.upload(f)
+        sim.apply_ampere_range()
+        assert_bits(sim.download(), f, "uniform H")
+        # PEC zeroes exactly the shell (kernel_test.cpp:152-165)
+        for c in range(3):
+            f[c][...] = 1.0
+        sim.upload(f)
+        sim.apply_pec_boundary()
+        g = sim.download()
+        for c in range(3):
+            ext = yb.comp_extents(n, n, n, c)
+            kk, jj, ii = np.meshgrid(*[np.arange(e) for e in ext[::-1]], indexing="ij")
+            idx = (ii, jj, kk)
+            inner = np.ones(g[c].shape, bool)
+            for a in range(3):
+                if a != c:
+                    inner &= (idx[a] >= 1) & (idx[a] <= n - 1)
+            assert np.array_equal(g[c], inner.astype(np.float32))
+
+
+def test_range_errors(yb):
+    with yb.Simulation(4, 4, 4) as sim:
+        with pytest.raises(yb.YeeOutOfRange):
+            sim.apply_ampere_range((0, 6, 0, 4, 0, 4))  # kernel_test.cpp:136-138
+        with pytest.raises(yb.YeeOutOfRange):
+            sim.apply_faraday_range((0, 6, 0, 4, 0, 4))
+        sim.apply_ampere_range((0, 2, 0, 2, 0, 2))  # sub-box is fine
+        with pytest.raises(yb.YeeInvalidArgument):
+            sim.add_source(2, 2, 0, 2, np.ones(3, np.float32))  # on the boundary
+        with pytest.raises(yb.YeeInvalidArgument):
+            sim.add_source(3, 2, 2, 2, np.ones(3, np.float32))  # magnetic
+        with pytest.raises(yb.YeeInvalidArgument):
+            sim.run(-1)
+
+
+def oracle_run(oracle, nx, ny, nz, f, steps, medium=None, src=None, cd=None):
+    co = oracle.Coeffs(nx, ny, nz)
+    if cd is not None:
+        co = oracle.Coeffs(nx, ny, nz, cdx=cd[0], cdy=cd[1], cdz=cd[2])
+    if medium is not None:
+        ca, cb, da, db = oracle.cell_coeffs(nx, ny, nz, *medium)
+        co = oracle.Coeffs(nx, ny, nz, ca=ca, cb=cb, da=da, db=db)
+    srcs = [oracle.Source(*src)] if src is not None else None
+    oracle.run(nx, ny, nz, f, co, steps, sources=srcs)
+    return f
+
+
+CASES = {
+    # name: (nx, ny, nz, steps, eps_seed, sigma_seed, field_seed, source?)
+    "c1_vacuum_src": (40, 40, 40, 60, -1, -1, None, True),
+    "c2_dielectric_src": (48, 40, 36, 60, 1, -1, None, True),
+    "c3_lossy_fields": (64, 48, 40, 25, 2, 2, 3, False),
+    "c4_slab_src": (136, 72, 40, 20, 4, -1, None, True),
+    "c5_lossy_fields": (96, 64, 48, 15, 5, 5, 6, False),
+    "odd_sizes": (37, 29, 23, 17, 7, 7, 8, True),
+    "thin_x": (1, 9, 11, 9, 9, 9, 10, False),
+    "thin_y": (21, 1, 7, 9, 9, 9, 10, False),
+    "thin_z": (19, 13, 1, 9, 9, 9, 10, False),
+    "two_tiles_partial": (133, 17, 9, 11, 3, 3, 4, True),
+}
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_configs_vs_oracle(yb, oracle, name, variant):
+    nx, ny, nz, steps, es, ss, fs, has_src = CASES[name]
+    src = None
+    if has_src and nx > 2 and ny > 2 and nz > 2:
+        src = (2, nx // 2, ny // 2, nz // 2, oracle.gauss_table(steps))
+    f = oracle.fill_fields(nx, ny, nz, fs) if fs is not None else oracle.zeros_state(nx, ny, nz)
+    with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+        sim.generate_medium(es, ss)
+        if src is not None:
+            sim.add_source(*src[:4], src[4])
+        if fs is not None:
+            sim.fill(fs)
+            assert_bits(sim.download(), f, "device fill")
+        sim.run(steps)
+        got = sim.download()
+    want = oracle_run(oracle, nx, ny, nz, f, steps, medium=(es, ss) if es >= 0 or ss >= 0 else None,
+                      src=src)
+    assert max(oracle.max_rel_err(got, want)) <= TOL
+    assert_bits(got, want, name)
+
+
+@pytest.mark.parametrize("zchunk", [1, 3, 7, 64])
+def test_zchunks_bit_identical(yb, oracle, zchunk):
+    nx, ny, nz, steps = 40, 24, 30, 9
+    f = oracle.fill_fields(nx, ny, nz, 41)
+    with yb.Simulation(nx, ny, nz, zchunk=zchunk) as sim:
+        sim.generate_medium(42, 43)
+        sim.upload(f)
+        sim.run(steps)
+        got = sim.download()
+    assert_bits(got, oracle_run(oracle, nx, ny, nz, f, steps, medium=(42, 43)), f"zchunk={zchunk}")
+
+
+def test_uploaded_coefficients_match_generated(yb, oracle):
+    nx, ny, nz = 33, 20, 18
+    ca, cb, da, db = oracle.cell_coeffs(nx, ny, nz, 11, 12)
+    f = oracle.fill_fields(nx, ny, nz, 13)
+    with yb.Simulation(nx, ny, nz) as sim:
+        for w, a in zip((yb.CA, yb.CB, yb.DA, yb.DB), (ca, cb, da, db)):
+            sim.set_cell_coeffs(w, a)
+        sim.upload(f)
+        sim.run(8)
+        assert sim.info()["n_cell_arrays"] == 4
+        got = sim.download()
+    assert_bits(got, oracle_run(oracle, nx, ny, nz, f, 8, medium=(11, 12)), "uploaded coeffs")
+
+
+def test_uniform_arrays_compressed(yb, oracle):
+    nx, ny, nz = 24, 20, 16
+    S = yb.S
+    f = oracle.fill_fields(nx, ny, nz, 3)
+    with yb.Simulation(nx, ny, nz) as sim:
+        sim.set_cell_coeffs(yb.CA, np.ones((nz, ny, nx), np.float32))
+        sim.set_cell_coeffs(yb.CB, np.full((nz, ny, nx), S, np.float32))
+        assert sim.info()["n_cell_arrays"] == 0
+        sim.upload(f)
+        sim.run(5)
+        got = sim.download()
+    assert_bits(got, oracle_run(oracle, nx, ny, nz, f, 5), "compressed")
+
+
+def test_zero_steps_and_resume(yb, oracle):
+    nx, ny, nz = 30, 22, 14
+    f = oracle.fill_fields(nx, ny, nz, 77)
+    tab = oracle.gauss_table(20)
+    with yb.Simulation(nx, ny, nz) as sim:
+        sim.generate_medium(5, 5)
+        sim.upload(f)
+        sim.run(0)
+        assert_bits(sim.download(), f, "0 steps")  # PEC planes untouched before a step
+        sim.add_source(1, 15, 11, 7, tab)
+        sim.run(5)
+        mid = sim.download()
+        sim.run(7)
+        got = sim.download()
+        assert sim.step_index == 12
+    with yb.Simulation(nx, ny, nz) as sim:  # checkpoint / resume: upload mid-state at step 5
+        sim.generate_medium(5, 5)
+        sim.add_source(1, 15, 11, 7, tab)
+        sim.upload(mid)
+        sim.step_index = 5
+        sim.run(7)
+        assert_bits(sim.download(), got, "resume")
+    want = oracle_run(oracle, nx, ny, nz, f, 12, medium=(5, 5), src=(1, 15, 11, 7, tab))
+    assert_bits(got, want, "resume vs oracle")
+
+
+def test_full_config1_vs_oracle(yb, oracle):
+    """BASELINE config 1 at full size: 128^3 vacuum, zero fields, PEC, Gaussian
+    Ez source at the centre, 200 steps. Bit-exact against the oracle (which is
+    bit-exact against the reference kernels on this path)."""
+    n, steps = 128, 200
+    tab = oracle.gauss_table(steps)
+    with yb.Simulation(n, n, n) as sim:
+        sim.add_source(2, n // 2, n // 2, n // 2, tab)
+        sim.run(steps)
+        got = sim.download()
+        dig = sim.digest()
+    want = oracle_run(oracle, n, n, n, oracle.zeros_state(n, n, n), steps,
+                      src=(2, n // 2, n // 2, n // 2, tab))
+    assert_bits(got, want, "config1")
+    assert dig == oracle.digest(n, n, n, want)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_full_size_fused_equals_naive(yb, cfg):
+    """Full-size configs 3 (512^3 lossy, 100 steps) and 5 (1024x1024x256 at one
+    GPU, 100 steps): the fused z-march equals the independent per-DoF path bit
+    for bit (size-independent property; the oracle covers the cut-downs)."""
+    if cfg == "c3":
+        nx, ny, nz, es, ss, fs, steps = 512, 512, 512, 2, 2, 3, 100
+    else:
+        nx, ny, nz, es, ss, fs, steps = 1024, 1024, 256, 5, 5, 6, 100
+    digs = []
+    for variant in VARIANTS:
+        with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+            sim.generate_medium(es, ss)
+            sim.fill(fs)
+            sim.run(steps)
+            digs.append(sim.digest())
+    assert digs[0] == digs[1]
