@@ -115,25 +115,25 @@ def cpu_reference_rate(nx, ny, nz, budget_s=10.0, max_steps=None):
     f = O.fill_fields(nx, ny, nz, 1, threads=cores)
     if O.have_ref():
         split = (1, min(16, ny), min(16, nz))
-        O.ref_simulation(nx, ny, nz, f, 1, variant="tiled", split=split, workers=cores)  # warm
-        steps, secs = 0, 0.0
-        while secs < budget_s and (max_steps is None or steps < max_steps):
-            s, _ = O.ref_simulation(nx, ny, nz, f, 1, variant="tiled", split=split, workers=cores)
-            secs += s
-            steps += 1
+        s0, _ = O.ref_simulation(nx, ny, nz, f, 2, variant="tiled", split=split, workers=cores)
+        steps = max(1, int(budget_s * 2 / max(s0, 1e-6)))  # one call of ~budget_s
+        if max_steps is not None:
+            steps = min(steps, max_steps)
+        secs, _ = O.ref_simulation(nx, ny, nz, f, steps, variant="tiled", split=split, workers=cores)
         return {"value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores,
                 "kind": "reference",
                 "sample": f"yeeblock Simulation<float> Tiled split 1x{split[1]}x{split[2]}, {cores} workers, "
                           f"{nx}x{ny}x{nz} grid, {steps} steps, vacuum coefficients (the reference has "
                           f"no per-cell Ca/Cb), quiescent skip off; time from RunStats.total_seconds"}
     co = O.Coeffs(nx, ny, nz)
-    O.run(nx, ny, nz, f, co, 1, threads=cores)
-    steps, secs = 0, 0.0
-    while secs < budget_s and (max_steps is None or steps < max_steps):
-        t = time.perf_counter()
-        O.run(nx, ny, nz, f, co, 1, threads=cores)
-        secs += time.perf_counter() - t
-        steps += 1
+    t = time.perf_counter()
+    O.run(nx, ny, nz, f, co, 2, threads=cores)
+    steps = max(1, int(budget_s * 2 / max(time.perf_counter() - t, 1e-6)))
+    if max_steps is not None:
+        steps = min(steps, max_steps)
+    t = time.perf_counter()
+    O.run(nx, ny, nz, f, co, steps, threads=cores)
+    secs = time.perf_counter() - t
     return {"value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"C oracle port (OpenMP {cores} threads) {nx}x{ny}x{nz}, {steps} steps"}
 
@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--variant", default="fused", choices=["fused", "naive"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--zchunk", type=int, default=0, help="fused: z planes per work item (0 = auto)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     nx, ny, nzg, es, ss, fs, has_src, cfg_steps, label = CONFIGS[args.config]
@@ -180,7 +181,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        ref = cpu_reference_rate(nx, ny, nz, budget_s=1e9, max_steps=max(1, args.steps))
+        ref = cpu_reference_rate(nx, ny, nz, budget_s=60.0, max_steps=max(1, args.steps))
         line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -200,7 +201,7 @@ def main():
     torch.cuda.set_device(local)
     variant = Y.VARIANT_FUSED if args.variant == "fused" else Y.VARIANT_NAIVE
 
-    sim = Y.Simulation(nx, ny, nz, device=local, variant=variant)
+    sim = Y.Simulation(nx, ny, nz, device=local, variant=variant, zchunk=args.zchunk)
     sim.generate_medium(es, ss)
     table = None
     if has_src:
@@ -266,7 +267,7 @@ def main():
                                 out=[pin((nz, ny, nx)) if q in want else None for q in range(4)])
             cell_arrays = {q: med[q] for q in want}
         e_steps = cfg_steps
-        with Y.Simulation(nx, ny, nz, device=local, variant=variant) as s2:
+        with Y.Simulation(nx, ny, nz, device=local, variant=variant, zchunk=args.zchunk) as s2:
             if table is not None:
                 s2.add_source(Y.EZ, nx // 2, ny // 2, nz // 2, table)
             if dist:

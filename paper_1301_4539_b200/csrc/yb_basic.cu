@@ -17,13 +17,6 @@ namespace yb {
 
 namespace {
 
-__device__ __forceinline__ float coefA(const float* cell, float s, long long p) {
-  return cell ? cell[p] : s;
-}
-__device__ __forceinline__ float coefB(const float* cell, const float* axis, int ax, long long p) {
-  return cell ? cell[p] : axis[ax];
-}
-
 struct Box {
   int xlo, xhi, ylo, yhi, zlo, zhi;
 };
@@ -102,43 +95,10 @@ __global__ void k_sources(Geo g, Fields F, SrcArgs s) {
 // those PEC zeros, so its update is Da*h + (Db*(0-0) - Db*(0-0)), computed
 // in exactly that form. Reads `in`, writes `out` (disjoint from the sweep).
 __global__ void k_faces(Geo g, Fields in, Fields out, CoefArgs co) {
-  const long long nxf = (long long)(g.ny + 1) * (g.nz + 1);
-  const long long nyf = (long long)(g.nx + 1) * (g.nz + 1);
-  const long long nzf = (long long)(g.nx + 1) * (g.ny + 1);
-  const long long total = nxf + nyf + nzf;
+  const long long total = face_points(g);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    if (t < nxf) {
-      const int j = (int)(t % (g.ny + 1)), k = (int)(t / (g.ny + 1)), i = g.nx;
-      const long long p = gidx(g, i, j, k);
-      if (j < g.ny) out.f[1][p] = 0.0f;
-      if (k < g.nz) out.f[2][p] = 0.0f;
-      if (j < g.ny && k < g.nz)
-        out.f[3][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in.f[3][p],
-                              coefB(co.cell[3], co.cdz_h, k, p), 0.0f, 0.0f,
-                              coefB(co.cell[3], co.cdy_h, j, p), 0.0f, 0.0f);
-    } else if (t < nxf + nyf) {
-      const long long u = t - nxf;
-      const int i = (int)(u % (g.nx + 1)), k = (int)(u / (g.nx + 1)), j = g.ny;
-      const long long p = gidx(g, i, j, k);
-      if (i < g.nx) out.f[0][p] = 0.0f;
-      if (k < g.nz) out.f[2][p] = 0.0f;
-      if (i < g.nx && k < g.nz)
-        out.f[4][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in.f[4][p],
-                              coefB(co.cell[3], co.cdx_h, i, p), 0.0f, 0.0f,
-                              coefB(co.cell[3], co.cdz_h, k, p), 0.0f, 0.0f);
-    } else {
-      const long long u = t - nxf - nyf;
-      const int i = (int)(u % (g.nx + 1)), j = (int)(u / (g.nx + 1)), k = g.nz;
-      const long long p = gidx(g, i, j, k);
-      if (i < g.nx) out.f[0][p] = 0.0f;
-      if (j < g.ny) out.f[1][p] = 0.0f;
-      if (i < g.nx && j < g.ny)
-        out.f[5][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in.f[5][p],
-                              coefB(co.cell[3], co.cdy_h, j, p), 0.0f, 0.0f,
-                              coefB(co.cell[3], co.cdx_h, i, p), 0.0f, 0.0f);
-    }
-  }
+       t += (long long)gridDim.x * blockDim.x)
+    face_point(g, in.f, out.f, co, t);
 }
 
 __device__ __forceinline__ void comp_ext(const Geo& g, int c, int e[3]) {

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -105,6 +106,9 @@ struct yb_sim {
   int stages = 0;
   dim3 grid{1, 1, 1};
   int zchunk = 0;
+  int ntx = 1, nty = 1, nitems = 1;
+  unsigned long long* sched = nullptr;  // device work counter of the fused kernel
+  unsigned long long sched_base = 0;
 };
 
 namespace {
@@ -161,9 +165,12 @@ int encode_map(CUtensorMap* m, const Geo& g, float* base) {
   const cuuint64_t strides[2] = {(cuuint64_t)g.PX * 4, (cuuint64_t)g.plane * 4};
   const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)yb::kBY, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
+  // YB_L2PROMO=0..3 (tuning knob): none / 64B / 128B / 256B L2 promotion
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* e = std::getenv("YB_L2PROMO")) promo = (CUtensorMapL2promotion)std::atoi(e);
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return YB_OK;
 }
@@ -182,21 +189,28 @@ int prepare_fused(yb_sim* s) {
         if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->cell[a])) return rc;
   }
   const size_t avail = 227 * 1024;
-  int S = 5;
+  // Ring depth: measured best at 4 stages (<= 7 arrays) / 3 (more), i.e.
+  // ~150-165 KB in flight per SM; deeper rings lost DRAM efficiency.
+  int S = narr <= 7 ? 4 : 3;
+  if (const char* e = std::getenv("YB_STAGES")) S = std::max(2, std::min(6, std::atoi(e)));
   while (S > 2 && yb::fused_smem_bytes(narr, S) > avail) --S;
   s->stages = S;
   const int tx = (s->g.nx + yb::kTX - 1) / yb::kTX;
   const int ty = (s->g.ny + yb::kTY - 1) / yb::kTY;
   int zc = s->zchunk_req;
   if (zc <= 0) {
-    // minimise waves x (planes per chunk + ~1.3 extra planes per chunk)
+    // Persistent CTAs (one per SM) stride over T*Z items. Minimise the
+    // busiest CTA's planes: ceil(T*Z/G) items of (len + ~1.2) planes, the
+    // extra being the prologue/epilogue planes a chunk boundary re-reads.
     const long long T = (long long)tx * ty;
     double best = 1e300;
     for (int Z = 1; Z <= s->g.nz; ++Z) {
       const int len = (s->g.nz + Z - 1) / Z;
       const int Zr = (s->g.nz + len - 1) / len;
-      const long long waves = (T * Zr + s->num_sms - 1) / s->num_sms;
-      const double cost = (double)waves * (len + 1.3);
+      const long long rounds = (T * Zr + s->num_sms - 1) / s->num_sms;
+      // (1 + len/400): shorter items keep concurrently running neighbours
+      // closer in z (halo rows hit L2) and balance better; measured.
+      const double cost = (double)rounds * (len + (Zr > 1 ? 1.2 : 0.0)) * (1.0 + len / 400.0);
       if (cost < best - 1e-9) {
         best = cost;
         zc = len;
@@ -205,7 +219,13 @@ int prepare_fused(yb_sim* s) {
   }
   zc = std::min(std::max(zc, 1), s->g.nz);
   s->zchunk = zc;
-  s->grid = dim3(tx, ty, (s->g.nz + zc - 1) / zc);
+  s->ntx = tx;
+  s->nty = ty;
+  s->nitems = tx * ty * ((s->g.nz + zc - 1) / zc);
+  // YB_CTAS_PER_ITEM=1 (debug/A-B): one CTA per work item instead of persistent CTAs
+  const char* one = std::getenv("YB_CTAS_PER_ITEM");
+  const int ctas = (one && one[0] == '1') ? s->nitems : std::min(s->nitems, s->num_sms);
+  s->grid = dim3(ctas, 1, 1);
   s->tm_valid = true;
   return YB_OK;
 }
@@ -243,6 +263,11 @@ int step_fused(yb_sim* s) {
   a.g = s->g;
   a.nstages = s->stages;
   a.zchunk = s->zchunk;
+  a.ntx = s->ntx;
+  a.nty = s->nty;
+  a.nitems = s->nitems;
+  a.sched = s->sched;
+  a.sched_base = s->sched_base;
   a.co = coef_args(s);
   for (int c = 0; c < 6; ++c) {
     a.in[c] = s->buf[s->cur][c];
@@ -263,10 +288,9 @@ int step_fused(yb_sim* s) {
     YB_CU(cudaEventRecord(tp->a, s->stream));
   }
   YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, s->grid, smem, s->stream));
+  s->sched_base += (unsigned long long)s->nitems + s->grid.x;  // every CTA's last fetch fails
   if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
-  YB_CU(yb::launch_faces(s->g, fields_of(s, s->cur), fields_of(s, nxt), a.co, s->num_sms,
-                         s->stream));
-  s->launches += 2;
+  s->launches += 1;
   s->cur = nxt;
   if (s->timers_used >= 4096) return collect_timers(s);
   return YB_OK;
@@ -393,6 +417,9 @@ int yb_create(const yb_desc* d, yb_sim** out) {
       return bail(fail(YB_CUDA_ERROR, "cudaMalloc failed"));
     s->dev_bytes += ab;
   }
+  if (cudaMalloc(&s->sched, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemsetAsync(s->sched, 0, sizeof(unsigned long long), s->stream) != cudaSuccess)
+    return bail(fail(YB_CUDA_ERROR, "scheduler counter alloc failed"));
   if (int rc = upload_axis(s)) return bail(rc);
   static bool limits_set = false;
   if (!limits_set) {
@@ -414,6 +441,7 @@ int yb_destroy(yb_sim* s) {
     for (int c = 0; c < 6; ++c) cudaFree(s->buf[b][c]);
   for (int q = 0; q < 4; ++q) cudaFree(s->cell[q]);
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
+  cudaFree(s->sched);
   for (auto& t : s->timers) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);

@@ -56,4 +56,54 @@ __device__ __forceinline__ long long gidx(const Geo& g, int i, int j, int k) {
   return ((long long)k * g.PY + j) * g.PX + i;
 }
 
+__device__ __forceinline__ float coefA(const float* cell, float s, long long p) {
+  return cell ? cell[p] : s;
+}
+__device__ __forceinline__ float coefB(const float* cell, const float* axis, int ax, long long p) {
+  return cell ? cell[p] : axis[ax];
+}
+
+// DoFs on the three upper faces (i=nx, j=ny, k=nz) that the cell-box sweep
+// does not own. Tangential E there is PEC (written +0); the normal H (hx at
+// i=nx, hy at j=ny, hz at k=nz) reads only those PEC zeros, so its update is
+// Da*h + (Db*(0-0) - Db*(0-0)), computed in exactly that form. Reads `in`,
+// writes `out` (disjoint from the sweep's writes).
+__device__ __forceinline__ long long face_points(const Geo& g) {
+  return (long long)(g.ny + 1) * (g.nz + 1) + (long long)(g.nx + 1) * (g.nz + 1) +
+         (long long)(g.nx + 1) * (g.ny + 1);
+}
+
+__device__ __forceinline__ void face_point(const Geo& g, const float* const* in,
+                                           float* const* out, const CoefArgs& co, long long t) {
+  const long long nxf = (long long)(g.ny + 1) * (g.nz + 1);
+  const long long nyf = (long long)(g.nx + 1) * (g.nz + 1);
+  if (t < nxf) {
+    const int j = (int)(t % (g.ny + 1)), k = (int)(t / (g.ny + 1)), i = g.nx;
+    const long long p = gidx(g, i, j, k);
+    if (j < g.ny) out[1][p] = 0.0f;
+    if (k < g.nz) out[2][p] = 0.0f;
+    if (j < g.ny && k < g.nz)
+      out[3][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in[3][p], coefB(co.cell[3], co.cdz_h, k, p),
+                          0.0f, 0.0f, coefB(co.cell[3], co.cdy_h, j, p), 0.0f, 0.0f);
+  } else if (t < nxf + nyf) {
+    const long long u = t - nxf;
+    const int i = (int)(u % (g.nx + 1)), k = (int)(u / (g.nx + 1)), j = g.ny;
+    const long long p = gidx(g, i, j, k);
+    if (i < g.nx) out[0][p] = 0.0f;
+    if (k < g.nz) out[2][p] = 0.0f;
+    if (i < g.nx && k < g.nz)
+      out[4][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in[4][p], coefB(co.cell[3], co.cdx_h, i, p),
+                          0.0f, 0.0f, coefB(co.cell[3], co.cdz_h, k, p), 0.0f, 0.0f);
+  } else {
+    const long long u = t - nxf - nyf;
+    const int i = (int)(u % (g.nx + 1)), j = (int)(u / (g.nx + 1)), k = g.nz;
+    const long long p = gidx(g, i, j, k);
+    if (i < g.nx) out[0][p] = 0.0f;
+    if (j < g.ny) out[1][p] = 0.0f;
+    if (i < g.nx && j < g.ny)
+      out[5][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in[5][p], coefB(co.cell[3], co.cdy_h, j, p),
+                          0.0f, 0.0f, coefB(co.cell[3], co.cdx_h, i, p), 0.0f, 0.0f);
+  }
+}
+
 }  // namespace yb

@@ -1,21 +1,25 @@
 // yb_fused.cu — the FUSED one-sweep Yee step for sm_100a.
 //
-// One CTA owns a kTX x kTY column of cells (x,y) and marches a z-chunk of
-// planes. Per plane k it
-//   1. waits for the TMA-staged plane k of all read arrays (ex..hz of the
-//      current state + the per-cell coefficient arrays), box x0-4..x0+TX+3,
-//      y0-1..y0+TY, landed in a ring of `nstages` shared-memory stages by
-//      cp.async.bulk.tensor + mbarrier complete_tx;
-//   2. computes E^{n+1} on plane k for the owned cells plus the +x column and
-//      +y row halo (update_e_dof, kernels.hpp:27-44, PEC folded in as "not
-//      curl-updatable -> +0", staggering.hpp:70-86, sources added after it,
-//      schedule.hpp:175-199), keeps it in a 3-deep shared plane buffer and
-//      writes the owned part to the next state;
-//   3. computes H^{n+3/2} on plane k-1 (update_h_dof, kernels.hpp:46-63) from
-//      E^{n+1} planes k-1 (with halo) and k (own, registers) and the H / Da /
-//      Db values of plane k-1 the same threads read one iteration earlier.
+// Work item = a kTX x kTY column of cells (x,y) times a z-chunk of planes.
+// Persistent CTAs (one per SM) take items from a global atomic counter.
+// Warp kTY is the producer: one lane streams, per plane, a box
+// x0-4..x0+TX+3, y0-1..y0+TY of every read array (ex..hz of the current
+// state + the per-cell coefficient arrays) into a ring of `nstages` shared
+// stages with cp.async.bulk.tensor, completion on a "full" mbarrier.
+// Warps 0..kTY-1 are independent z-marching row units: warp w owns row
+// j = y0+w and per plane k
+//   1. computes E^{n+1}(k) on row j (update_e_dof, kernels.hpp:27-44, PEC
+//      folded in as "not curl-updatable -> +0", staggering.hpp:70-86,
+//      sources added after it, schedule.hpp:175-199), plus the E values of
+//      the +y row (ex, ez) and +x column (ey, ez) that its H update needs -
+//      recomputed redundantly, so no warp ever waits for another;
+//   2. releases the stage (one arrive per warp on the "empty" mbarrier);
+//   3. computes H^{n+3/2}(k-1) on row j (update_h_dof, kernels.hpp:46-63)
+//      from registers only: E(k-1) with its halo, E(k), H(k-1), Da/Db(k-1).
+// Warp kTY+1 updates the DoFs of the three upper faces (face_point)
+// concurrently, so one launch performs the whole Standard step.
 // This is planeAmpere(k); planeFaraday(k-1) of the paper's one-sweep scheme
-// with the +x/+y E halo recomputed instead of exchanged.
+// (PAPER.md:683-692).
 // State is double-buffered (read `in`, write `out`), so CTAs never race on
 // halo values; DRAM traffic is one read + one write of each field plus one
 // read of each per-cell coefficient array per step.
@@ -101,224 +105,294 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_fused(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm) {
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
   constexpr int S_CA = 6, S_CB = 6 + CAC, S_DA = 6 + CAC + CBC, S_DB = 6 + CAC + CBC + DAC;
+  constexpr uint32_t kBoxBytes = kBX * kBY * 4;
+  constexpr int kQ = 8;  // item queue depth (> max stages)
   extern __shared__ __align__(128) float smem[];
 
   const Geo& g = a.g;
   const CoefArgs& co = a.co;
   const int S = a.nstages;
   float* stages = smem;
-  float* enew = smem + (size_t)S * NARR * kSlot;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(enew + 9 * kEPlane);
-
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * NARR * kSlot);
+  uint64_t* empty = full + S;
+  int* item_q = reinterpret_cast<int*>(empty + S);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-  const int kz0 = blockIdx.z * a.zchunk;
-  const int kz1 = min(kz0 + a.zchunk, g.nz);
-  const bool top = (kz1 == g.nz);
-  const int kend = top ? g.nz - 1 : kz1;  // non-top chunks stream plane kz1 for E(kz1)
-  const int L = kend - kz0 + 1;
+  const int T = a.ntx * a.nty;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kTY);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  auto issue = [&](int it) {
-    const int s = it % S;
-    const uint32_t bar = smem_u32(&bars[s]);
-    mbar_expect_tx(bar, (uint32_t)(NARR * kBX * kBY * 4));
+  // ======================= producer warp ===================================
+  // Items are numbered chunk-major and handed out in order, so the items in
+  // flight form a contiguous window: concurrently running CTAs hold
+  // neighbouring tiles at the same z and their halo rows meet in L2.
+  // Element 0 of an item with kz0 > 0 is the prologue plane kz0-1 (hx, hy
+  // only); then planes kz0..kend. The item index reaches the consumers
+  // through item_q, published by the (release) arrive on the item's first
+  // full barrier; -1 (no work left) is published by a plain arrive.
+  if (w == kTY + 1) {  // face warp: the upper-face DoFs (face_point)
+    const long long nf = face_points(g);
+    for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL)
+      face_point(g, a.in, a.out, co, t);
+    return;
+  }
+  if (w == kTY) {
+    if (l != 0) return;
+    int p_item = -1, p_e = 0, p_nE = 0, p_seq = 0;
+    for (int q = 0;; ++q) {
+      const int s = q % S;
+      if (q >= S) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((q / S) - 1) & 1));
+      const uint32_t bar = smem_u32(&full[s]);
+      if (p_item < 0) {
+        const unsigned long long v = atomicAdd(a.sched, 1ull) - a.sched_base;
+        const int it = v < (unsigned long long)a.nitems ? (int)v : -1;
+        item_q[p_seq % kQ] = it;
+        ++p_seq;
+        if (it < 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+          return;
+        }
+        p_item = it;
+        p_e = 0;
+        const int kz0 = (it / T) * a.zchunk;
+        const int kz1 = min(kz0 + a.zchunk, g.nz);
+        p_nE = (kz0 > 0 ? 1 : 0) + ((kz1 == g.nz) ? g.nz - 1 : kz1) - kz0 + 1;
+      }
+      const int chunk = p_item / T, tile = p_item - chunk * T;
+      const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
+      const int kz0 = chunk * a.zchunk;
+      const int pro = kz0 > 0 ? 1 : 0;
+      float* dst = stages + (size_t)s * NARR * kSlot;
+      if (pro && p_e == 0) {
+        mbar_expect_tx(bar, 2 * kBoxBytes);
+        tma_load_3d(smem_u32(dst + 3 * kSlot), &tm.m[3], x0 - 4, y0 - 1, kz0 - 1, bar);
+        tma_load_3d(smem_u32(dst + 4 * kSlot), &tm.m[4], x0 - 4, y0 - 1, kz0 - 1, bar);
+      } else {
+        const int k = kz0 + p_e - pro;
+        mbar_expect_tx(bar, NARR * kBoxBytes);
 #pragma unroll
-    for (int q = 0; q < NARR; ++q)
-      tma_load_3d(smem_u32(stages + ((size_t)s * NARR + q) * kSlot), &tm.m[q], x0 - 4, y0 - 1,
-                  kz0 + it, bar);
-  };
-  if (threadIdx.x == 0) {
-    const int n0 = S < L ? S : L;
-    for (int it = 0; it < n0; ++it) issue(it);
+        for (int qq = 0; qq < NARR; ++qq)
+          tma_load_3d(smem_u32(dst + qq * kSlot), &tm.m[qq], x0 - 4, y0 - 1, k, bar);
+      }
+      if (++p_e == p_nE) p_item = -1;
+    }
   }
 
-  const int j = y0 + w;  // w == kTY: the +y halo row
-  const int i0 = x0 + 4 * l;
-  const int ih = x0 + kTX;  // +x halo column (lane 31 only)
-  const int r = w + 1, c = 4 + 4 * l;
+  // ======================= consumer warps ==================================
+  const int r = w + 1, rn = w + 2, c = 4 + 4 * l;  // smem row of j, j+1; col of i0
   const bool hl = (l == 31);
-
-  // Per-thread constants: axis coefficients and masks.
-  const float cdy_e = co.cdy_e[j], cdy_h = co.cdy_h[j];
-  const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
-  const float cdx_e_h = co.cdx_e[ih];
-  const bool jin = j >= 1 && j < g.ny, jlt = j < g.ny;
-
-  // H of plane k-1 at the positions this thread updates (prologue: kz0-1).
-  float4 phx = make_float4(0.f, 0.f, 0.f, 0.f), phy = phx, phz = phx, pda = phx, pdb = phx;
-  float hph_x = 0.f, hph_y = 0.f;  // halo column hx, hy (lane 31)
-  if (kz0 > 0 && j <= g.ny) {
-    const long long p = gidx(g, i0, j, kz0 - 1);
-    phx = ldg4(a.in[3] + p);
-    phy = ldg4(a.in[4] + p);
-    if (hl && ih <= g.nx) {
-      const long long ph = gidx(g, ih, j, kz0 - 1);
-      hph_x = __ldg(a.in[3] + ph);
-      hph_y = __ldg(a.in[4] + ph);
-    }
-  }
-
-  auto h_phase = [&](int kh, const float* ep, float4 exk, float4 eyk) {
-    // ep: E^{n+1} plane kh (3 comps, pitch kEW). exk/eyk: own E^{n+1} at kh+1.
-    const float* pex = ep;
-    const float* pey = ep + kEPlane;
-    const float* pez = ep + 2 * kEPlane;
-    const float4 ex_h = lds4(pex + w * kEW + 4 * l);
-    const float4 ex_jp = lds4(pex + (w + 1) * kEW + 4 * l);
-    const float4 ey_h = lds4(pey + w * kEW + 4 * l);
-    const float4 ey_ip = shift_ip(ey_h, l, pey[w * kEW + kTX]);
-    const float4 ez_h = lds4(pez + w * kEW + 4 * l);
-    const float4 ez_jp = lds4(pez + (w + 1) * kEW + 4 * l);
-    const float4 ez_ip = shift_ip(ez_h, l, pez[w * kEW + kTX]);
-    const float cdz_h = co.cdz_h[kh];
-    float4 hx, hy, hz;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float A = DAC ? elc(pda, q) : co.da_s;
-      const float B = elc(pdb, q);
-      // hx(i,j,k) += cdz[k]*(ey(k+1)-ey(k)) - cdy[j]*(ez(j+1)-ez(j))
-      el(hx, q) = yee_upd(A, elc(phx, q), DBC ? B : cdz_h, elc(eyk, q), elc(ey_h, q),
-                          DBC ? B : cdy_h, elc(ez_jp, q), elc(ez_h, q));
-      // hy(i,j,k) += cdx[i]*(ez(i+1)-ez(i)) - cdz[k]*(ex(k+1)-ex(k))
-      el(hy, q) = yee_upd(A, elc(phy, q), DBC ? B : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
-                          DBC ? B : cdz_h, elc(exk, q), elc(ex_h, q));
-      // hz(i,j,k) += cdy[j]*(ex(j+1)-ex(j)) - cdx[i]*(ey(i+1)-ey(i))
-      el(hz, q) = yee_upd(A, elc(phz, q), DBC ? B : cdy_h, elc(ex_jp, q), elc(ex_h, q),
-                          DBC ? B : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
-    }
-    if (jlt) {
-      const long long p = gidx(g, i0, j, kh);
-      store_row4(a.out[3], p, i0, g.nx, hx);
-      store_row4(a.out[4], p, i0, g.nx, hy);
-      store_row4(a.out[5], p, i0, g.nx, hz);
-    }
+  constexpr int cc = 4 + kTX;  // smem col of the +x halo column
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  int cs = 0, c_seq = 0;
+  bool peeked = false;
+  auto wait_elem = [&]() -> int {
+    const int s = cs % S;
+    if (!peeked) mbar_wait(smem_u32(&full[s]), (uint32_t)((cs / S) & 1));
+    peeked = false;
+    ++cs;
+    return s;
+  };
+  auto release = [&](int s) {
+    __syncwarp();
+    if (l == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
+                             : "memory");
   };
 
-  float4 exn, eyn;
-  for (int it = 0; it < L; ++it) {
-    const int k = kz0 + it;
-    const int s = it % S;
-    mbar_wait(smem_u32(&bars[s]), (uint32_t)((it / S) & 1));
-    const float* st = stages + (size_t)s * NARR * kSlot;
-#define SM(q, rr, cc) (st + (q) * kSlot + (rr) * kBX + (cc))
+  for (;;) {
+    mbar_wait(smem_u32(&full[cs % S]), (uint32_t)((cs / S) & 1));
+    peeked = true;
+    const int item = item_q[c_seq % kQ];
+    ++c_seq;
+    if (item < 0) break;
+    const int chunk = item / T, tile = item - chunk * T;
+    const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
+    const int kz0 = chunk * a.zchunk;
+    const int kz1 = min(kz0 + a.zchunk, g.nz);
+    const bool top = (kz1 == g.nz);
+    const int kend = top ? g.nz - 1 : kz1;
 
-    // ---------------- E phase: plane k, rows y0..y0+TY, cols x0..x0+TX ----
-    const float cdz_e = co.cdz_e[k];
-    const bool kin = k >= 1 && k < g.nz;
-    const float4 ex = lds4(SM(0, r, c)), ey = lds4(SM(1, r, c)), ez = lds4(SM(2, r, c));
-    const float4 hx = lds4(SM(3, r, c)), hx_jm = lds4(SM(3, r - 1, c));
-    const float4 hy = lds4(SM(4, r, c));
-    const float4 hz = lds4(SM(5, r, c)), hz_jm = lds4(SM(5, r - 1, c));
-    const float4 hy_im = shift_im(hy, l, *SM(4, r, c - 1));
-    const float4 hz_im = shift_im(hz, l, *SM(5, r, c - 1));
-    float4 ca4 = make_float4(0.f, 0.f, 0.f, 0.f), cb4 = ca4;
-    if (CAC) ca4 = lds4(SM(S_CA, r, c));
-    if (CBC) cb4 = lds4(SM(S_CB, r, c));
-    float4 ezn;
+    const int j = y0 + w, jn = j + 1;
+    const int i0 = x0 + 4 * l;
+    const int ih = x0 + kTX;  // +x halo column (lane 31)
+    const float cdy_e = co.cdy_e[j], cdy_en = co.cdy_e[jn], cdy_h = co.cdy_h[j];
+    const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
+    const float cdx_e_h = co.cdx_e[ih];
+    const bool jin = j >= 1 && j < g.ny, jlt = j < g.ny;
+    const bool jnin = jn < g.ny;  // jn >= 1 always
+    const bool ih_in = ih >= 1 && ih < g.nx;
+
+    // carried state: H(k-1) (own row, hy of row j+1, hx of the halo column),
+    // Da/Db(k-1), E(k-1) own row / +y row (ex, ez) / +x column (ey, ez)
+    float4 phx = z4, phy = z4, phz = z4, phy_n = z4, pda = z4, pdb = z4;
+    float phx_c = 0.f;
+    float4 pex = z4, pey = z4, pez = z4, pex_n = z4, pez_n = z4;
+    float pey_c = 0.f, pez_c = 0.f;
+
+    auto h_row = [&](int kh, float4 exk, float4 eyk) {
+      const float4 ey_ip = shift_ip(pey, l, pey_c);
+      const float4 ez_ip = shift_ip(pez, l, pez_c);
+      const float cdz_h = co.cdz_h[kh];
+      float4 hx, hy, hz;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + q;
-      const float A = CAC ? elc(ca4, q) : co.ca_s;
-      const float B = elc(cb4, q);
-      const bool iin = i >= 1 && i < g.nx;
-      el(exn, q) = (i < g.nx && jin && kin)
-                       ? yee_upd(A, elc(ex, q), CBC ? B : cdy_e, elc(hz, q), elc(hz_jm, q),
-                                 CBC ? B : cdz_e, elc(hy, q), elc(phy, q))
-                       : 0.f;
-      el(eyn, q) = (iin && jlt && kin)
-                       ? yee_upd(A, elc(ey, q), CBC ? B : cdz_e, elc(hx, q), elc(phx, q),
-                                 CBC ? B : elc(cdx_e, q), elc(hz, q), elc(hz_im, q))
-                       : 0.f;
-      el(ezn, q) = (iin && jin)
-                       ? yee_upd(A, elc(ez, q), CBC ? B : elc(cdx_e, q), elc(hy, q),
-                                 elc(hy_im, q), CBC ? B : cdy_e, elc(hx, q), elc(hx_jm, q))
-                       : 0.f;
+      for (int q = 0; q < 4; ++q) {
+        const float A = DAC ? elc(pda, q) : co.da_s;
+        const float B = elc(pdb, q);
+        // hx(i,j,k) += cdz[k]*(ey(k+1)-ey(k)) - cdy[j]*(ez(j+1)-ez(j))
+        el(hx, q) = yee_upd(A, elc(phx, q), DBC ? B : cdz_h, elc(eyk, q), elc(pey, q),
+                            DBC ? B : cdy_h, elc(pez_n, q), elc(pez, q));
+        // hy(i,j,k) += cdx[i]*(ez(i+1)-ez(i)) - cdz[k]*(ex(k+1)-ex(k))
+        el(hy, q) = yee_upd(A, elc(phy, q), DBC ? B : elc(cdx_h, q), elc(ez_ip, q), elc(pez, q),
+                            DBC ? B : cdz_h, elc(exk, q), elc(pex, q));
+        // hz(i,j,k) += cdy[j]*(ex(j+1)-ex(j)) - cdx[i]*(ey(i+1)-ey(i))
+        el(hz, q) = yee_upd(A, elc(phz, q), DBC ? B : cdy_h, elc(pex_n, q), elc(pex, q),
+                            DBC ? B : elc(cdx_h, q), elc(ey_ip, q), elc(pey, q));
+      }
+      if (jlt) {
+        const long long p = gidx(g, i0, j, kh);
+        store_row4(a.out[3], p, i0, g.nx, hx);
+        store_row4(a.out[4], p, i0, g.nx, hy);
+        store_row4(a.out[5], p, i0, g.nx, hz);
+      }
+    };
+
+    if (kz0 > 0) {  // prologue element: H^{n+1/2} on plane kz0-1
+      const int s = wait_elem();
+      const float* st = stages + (size_t)s * NARR * kSlot;
+      phx = lds4(st + 3 * kSlot + r * kBX + c);
+      phy = lds4(st + 4 * kSlot + r * kBX + c);
+      phy_n = lds4(st + 4 * kSlot + rn * kBX + c);
+      if (hl) phx_c = st[3 * kSlot + r * kBX + cc];
+      release(s);
     }
-    // soft sources (after PEC, before Faraday): comp(i,j,k) += val
-    for (int q = 0; q < a.src.n; ++q) {
-      if (a.src.k[q] != k || a.src.j[q] != j) continue;
-      const int d = a.src.i[q] - i0;
-      const float v = a.src.val[q];
+
+    for (int k = kz0; k <= kend; ++k) {
+      const int s = wait_elem();
+      const float* st = stages + (size_t)s * NARR * kSlot;
+#define SM(q, rr, col) (st + (q) * kSlot + (rr) * kBX + (col))
+      const float cdz_e = co.cdz_e[k];
+      const bool kin = k >= 1 && k < g.nz;
+      // own row j
+      const float4 ex = lds4(SM(0, r, c)), ey = lds4(SM(1, r, c)), ez = lds4(SM(2, r, c));
+      const float4 hx = lds4(SM(3, r, c)), hy = lds4(SM(4, r, c)), hz = lds4(SM(5, r, c));
+      const float4 hx_jm = lds4(SM(3, r - 1, c)), hz_jm = lds4(SM(5, r - 1, c));
+      const float4 hy_im = shift_im(hy, l, *SM(4, r, c - 1));
+      const float4 hz_im = shift_im(hz, l, *SM(5, r, c - 1));
+      // +y row j+1 (ex, ez only)
+      const float4 ex_n = lds4(SM(0, rn, c)), ez_n = lds4(SM(2, rn, c));
+      const float4 hx_n = lds4(SM(3, rn, c)), hy_n = lds4(SM(4, rn, c)), hz_n = lds4(SM(5, rn, c));
+      const float4 hy_n_im = shift_im(hy_n, l, *SM(4, rn, c - 1));
+      float4 ca4 = z4, cb4 = z4, ca4n = z4, cb4n = z4, da4 = pda, db4 = pdb;
+      if (CAC) {
+        ca4 = lds4(SM(S_CA, r, c));
+        ca4n = lds4(SM(S_CA, rn, c));
+      }
+      if (CBC) {
+        cb4 = lds4(SM(S_CB, r, c));
+        cb4n = lds4(SM(S_CB, rn, c));
+      }
+      if (DAC) da4 = lds4(SM(S_DA, r, c));
+      if (DBC) db4 = lds4(SM(S_DB, r, c));
+      float4 exw, eyw, ezw, exn, ezn;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (d != e) continue;
-        if (a.src.comp[q] == 0) el(exn, e) = __fadd_rn(el(exn, e), v);
-        if (a.src.comp[q] == 1) el(eyn, e) = __fadd_rn(el(eyn, e), v);
-        if (a.src.comp[q] == 2) el(ezn, e) = __fadd_rn(el(ezn, e), v);
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q;
+        const bool iin = i >= 1 && i < g.nx, ilt = i < g.nx;
+        const float A = CAC ? elc(ca4, q) : co.ca_s;
+        const float B = elc(cb4, q);
+        const float An = CAC ? elc(ca4n, q) : co.ca_s;
+        const float Bn = elc(cb4n, q);
+        el(exw, q) = (ilt && jin && kin)
+                         ? yee_upd(A, elc(ex, q), CBC ? B : cdy_e, elc(hz, q), elc(hz_jm, q),
+                                   CBC ? B : cdz_e, elc(hy, q), elc(phy, q))
+                         : 0.f;
+        el(eyw, q) = (iin && jlt && kin)
+                         ? yee_upd(A, elc(ey, q), CBC ? B : cdz_e, elc(hx, q), elc(phx, q),
+                                   CBC ? B : elc(cdx_e, q), elc(hz, q), elc(hz_im, q))
+                         : 0.f;
+        el(ezw, q) = (iin && jin)
+                         ? yee_upd(A, elc(ez, q), CBC ? B : elc(cdx_e, q), elc(hy, q),
+                                   elc(hy_im, q), CBC ? B : cdy_e, elc(hx, q), elc(hx_jm, q))
+                         : 0.f;
+        el(exn, q) = (ilt && jnin && kin)
+                         ? yee_upd(An, elc(ex_n, q), CBC ? Bn : cdy_en, elc(hz_n, q), elc(hz, q),
+                                   CBC ? Bn : cdz_e, elc(hy_n, q), elc(phy_n, q))
+                         : 0.f;
+        el(ezn, q) = (iin && jnin)
+                         ? yee_upd(An, elc(ez_n, q), CBC ? Bn : elc(cdx_e, q), elc(hy_n, q),
+                                   elc(hy_n_im, q), CBC ? Bn : cdy_en, elc(hx_n, q), elc(hx, q))
+                         : 0.f;
       }
-    }
-    float* eb = enew + (it % 3) * 3 * kEPlane;
-    sts4(eb + w * kEW + 4 * l, exn);
-    sts4(eb + kEPlane + w * kEW + 4 * l, eyn);
-    sts4(eb + 2 * kEPlane + w * kEW + 4 * l, ezn);
-    // +x halo column i = x0+TX (lane 31): scalar form of the same update
-    float hh_x = 0.f, hh_y = 0.f;
-    if (hl) {
-      const int cc = 4 + kTX;
-      const float A = CAC ? *SM(S_CA, r, cc) : co.ca_s;
-      const float B = CBC ? *SM(S_CB, r, cc) : 0.f;
-      hh_x = *SM(3, r, cc);
-      hh_y = *SM(4, r, cc);
-      const float hzc = *SM(5, r, cc);
-      const bool iin = ih >= 1 && ih < g.nx;
-      float vx = (ih < g.nx && jin && kin)
-                     ? yee_upd(A, *SM(0, r, cc), CBC ? B : cdy_e, hzc, *SM(5, r - 1, cc),
-                               CBC ? B : cdz_e, hh_y, hph_y)
-                     : 0.f;
-      float vy = (iin && jlt && kin)
-                     ? yee_upd(A, *SM(1, r, cc), CBC ? B : cdz_e, hh_x, hph_x,
-                               CBC ? B : cdx_e_h, hzc, hz.w)
-                     : 0.f;
-      float vz = (iin && jin) ? yee_upd(A, *SM(2, r, cc), CBC ? B : cdx_e_h, hh_y, hy.w,
-                                        CBC ? B : cdy_e, hh_x, *SM(3, r - 1, cc))
-                              : 0.f;
-      for (int q = 0; q < a.src.n; ++q) {
-        if (a.src.k[q] != k || a.src.j[q] != j || a.src.i[q] != ih) continue;
-        if (a.src.comp[q] == 0) vx = __fadd_rn(vx, a.src.val[q]);
-        if (a.src.comp[q] == 1) vy = __fadd_rn(vy, a.src.val[q]);
-        if (a.src.comp[q] == 2) vz = __fadd_rn(vz, a.src.val[q]);
+      // +x halo column i = x0+TX, row j: ey, ez (lane 31)
+      float eyc = 0.f, ezc = 0.f, hx_c = 0.f;
+      if (hl) {
+        const float A = CAC ? *SM(S_CA, r, cc) : co.ca_s;
+        const float B = CBC ? *SM(S_CB, r, cc) : 0.f;
+        hx_c = *SM(3, r, cc);
+        const float hy_c = *SM(4, r, cc), hz_c = *SM(5, r, cc);
+        eyc = (ih_in && jlt && kin) ? yee_upd(A, *SM(1, r, cc), CBC ? B : cdz_e, hx_c, phx_c,
+                                              CBC ? B : cdx_e_h, hz_c, hz.w)
+                                    : 0.f;
+        ezc = (ih_in && jin) ? yee_upd(A, *SM(2, r, cc), CBC ? B : cdx_e_h, hy_c, hy.w,
+                                       CBC ? B : cdy_e, hx_c, *SM(3, r - 1, cc))
+                             : 0.f;
       }
-      eb[w * kEW + kTX] = vx;
-      eb[kEPlane + w * kEW + kTX] = vy;
-      eb[2 * kEPlane + w * kEW + kTX] = vz;
-    }
-    if (w < kTY && jlt && k < kz1) {
-      const long long p = gidx(g, i0, j, k);
-      store_row4(a.out[0], p, i0, g.nx, exn);
-      store_row4(a.out[1], p, i0, g.nx, eyn);
-      store_row4(a.out[2], p, i0, g.nx, ezn);
-    }
-    // H and coefficients of plane k at own positions, for the next H phase
-    float4 chz = hz;
-    float4 cda = pda, cdb = pdb;
-    if (DAC) cda = lds4(SM(S_DA, r, c));
-    if (DBC) cdb = lds4(SM(S_DB, r, c));
 #undef SM
-    __syncthreads();  // E plane k complete; stage s free for refill
-    if (threadIdx.x == 0 && it + S < L) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(it + S);
+      release(s);  // everything this warp needs from the stage is in registers
+      // soft sources (after PEC, before Faraday): comp(i,j,k) += val, for
+      // every copy of the DoF this warp computed
+      for (int q = 0; q < a.src.n; ++q) {
+        if (a.src.k[q] != k) continue;
+        const int sc = a.src.comp[q], si = a.src.i[q], sj = a.src.j[q];
+        const float v = a.src.val[q];
+        const int d = si - i0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (d != e) continue;
+          if (sj == j) {
+            if (sc == 0) el(exw, e) = __fadd_rn(el(exw, e), v);
+            if (sc == 1) el(eyw, e) = __fadd_rn(el(eyw, e), v);
+            if (sc == 2) el(ezw, e) = __fadd_rn(el(ezw, e), v);
+          }
+          if (sj == jn) {
+            if (sc == 0) el(exn, e) = __fadd_rn(el(exn, e), v);
+            if (sc == 2) el(ezn, e) = __fadd_rn(el(ezn, e), v);
+          }
+        }
+        if (hl && si == ih && sj == j) {
+          if (sc == 1) eyc = __fadd_rn(eyc, v);
+          if (sc == 2) ezc = __fadd_rn(ezc, v);
+        }
+      }
+      if (jlt && k < kz1) {
+        const long long p = gidx(g, i0, j, k);
+        store_row4(a.out[0], p, i0, g.nx, exw);
+        store_row4(a.out[1], p, i0, g.nx, eyw);
+        store_row4(a.out[2], p, i0, g.nx, ezw);
+      }
+      if (k > kz0) h_row(k - 1, exw, eyw);
+      pex = exw;
+      pey = eyw;
+      pez = ezw;
+      pex_n = exn;
+      pez_n = ezn;
+      pey_c = eyc;
+      pez_c = ezc;
+      phx = hx;
+      phy = hy;
+      phz = hz;
+      phy_n = hy_n;
+      phx_c = hx_c;
+      pda = da4;
+      pdb = db4;
     }
-    // ---------------- H phase: plane k-1 ------------------------------------
-    if (it >= 1 && w < kTY) h_phase(k - 1, enew + ((it - 1) % 3) * 3 * kEPlane, exn, eyn);
-    phx = hx;
-    phy = hy;
-    phz = chz;
-    pda = cda;
-    pdb = cdb;
-    hph_x = hh_x;
-    hph_y = hh_y;
-  }
-  // top chunk: H on plane nz-1 sees the PEC zeros of ex/ey at plane nz
-  if (top && w < kTY) {
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    h_phase(g.nz - 1, enew + ((L - 1) % 3) * 3 * kEPlane, z4, z4);
+    // top chunk: H on plane nz-1 sees the PEC zeros of ex/ey at plane nz
+    if (top) h_row(g.nz - 1, z4, z4);
   }
 }
 

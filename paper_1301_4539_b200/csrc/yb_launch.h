@@ -11,14 +11,12 @@ namespace yb {
 
 // Fused sweep geometry (yb_fused.cu).
 constexpr int kTX = 128;            // owned cells along x per CTA (32 lanes x float4)
-constexpr int kTY = 8;              // owned rows per CTA; warp kTY computes the +y halo row
-constexpr int kWarps = kTY + 1;
+constexpr int kTY = 8;              // owned rows per CTA = consumer warps; warp kTY = TMA producer
+constexpr int kWarps = kTY + 2;    // + producer warp + face warp
 constexpr int kThreads = 32 * kWarps;
 constexpr int kBX = kTX + 8;        // staged box: x0-4 .. x0+TX+3 (16-byte TMA rows)
 constexpr int kBY = kTY + 2;        // staged box: y0-1 .. y0+TY
 constexpr int kSlot = ((kBX * kBY * 4 + 127) / 128) * 32;  // floats per array slot (128-B aligned)
-constexpr int kEW = kTX + 4;        // E-plane buffer row pitch (TX owned + 1 halo column)
-constexpr int kEPlane = kEW * (kTY + 1);
 constexpr int kMaxArrays = 10;      // 6 fields + up to 4 per-cell coefficient arrays
 
 struct TMaps {
@@ -29,6 +27,10 @@ struct FusedArgs {
   Geo g;
   int nstages;
   int zchunk;
+  int ntx, nty;  // tiles along x, y
+  int nitems;    // work items = tiles * z-chunks, handed out by *sched
+  unsigned long long* sched;     // monotonic global work counter
+  unsigned long long sched_base; // counter value at this launch's start
   CoefArgs co;
   const float* in[6];
   float* out[6];
@@ -37,7 +39,7 @@ struct FusedArgs {
 
 // smem bytes of the fused kernel for `narr` staged arrays and `stages` ring depth.
 inline size_t fused_smem_bytes(int narr, int stages) {
-  return (size_t)stages * narr * kSlot * 4 + (size_t)9 * kEPlane * 4 + (size_t)stages * 8;
+  return (size_t)stages * narr * kSlot * 4 + (size_t)stages * 16 + 8 * 4;
 }
 
 // cell_mask bit q set <=> coefficient array q (Ca,Cb,Da,Db) is per-cell.

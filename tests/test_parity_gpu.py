@@ -176,9 +176,13 @@ def test_configs_vs_oracle(yb, oracle, name, variant):
     assert_bits(got, want, name)
 
 
-@pytest.mark.parametrize("zchunk", [1, 3, 7, 64])
-def test_zchunks_bit_identical(yb, oracle, zchunk):
-    nx, ny, nz, steps = 40, 24, 30, 9
+@pytest.mark.parametrize("shape,zchunk", [((40, 24, 30), 1), ((40, 24, 30), 3), ((40, 24, 30), 7),
+                                          ((40, 24, 30), 64), ((200, 64, 40), 2), ((130, 40, 33), 1),
+                                          ((256, 96, 21), 4)])
+def test_zchunks_bit_identical(yb, oracle, shape, zchunk):
+    """Persistent CTAs stride over (tile, z-chunk) items; with many items per
+    CTA the TMA ring runs across item boundaries (prologue/epilogue planes)."""
+    (nx, ny, nz), steps = shape, 9
     f = oracle.fill_fields(nx, ny, nz, 41)
     with yb.Simulation(nx, ny, nz, zchunk=zchunk) as sim:
         sim.generate_medium(42, 43)
