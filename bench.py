@@ -254,6 +254,7 @@ def main():
     if not args.no_e2e:
         pin = lambda shape: torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
         host_f = [pin(Y.comp_extents(nx, ny, nz, c)[::-1]) for c in range(6)]
+        host_out = [pin(Y.comp_extents(nx, ny, nz, c)[::-1]) for c in range(6)]
         if fs is not None:
             Y.host_fields(nx, ny, nz, fs, out=host_f)
         else:
@@ -278,7 +279,7 @@ def main():
                 s2.set_cell_coeffs(q, a)
             s2.upload(host_f)
             s2.run(e_steps)
-            out = s2.download()
+            out = s2.download(out=host_out)
             t1 = time.perf_counter()
         dt = t1 - t0
         if dist:

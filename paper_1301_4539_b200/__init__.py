@@ -206,13 +206,17 @@ class Simulation:
             assert a.shape == comp_extents(self.nx, self.ny, self.nz, c)[::-1], (c, a.shape)
             _check(lib().yb_upload_field(self._h, c, _fp(a)))
 
-    def download(self):
-        out = []
+    def download(self, out=None):
+        """Dense host copies of the six components (into `out` if given, e.g.
+        pinned buffers; fresh arrays otherwise)."""
+        res = []
         for c in range(6):
-            a = np.empty(comp_extents(self.nx, self.ny, self.nz, c)[::-1], np.float32)
+            shape = comp_extents(self.nx, self.ny, self.nz, c)[::-1]
+            a = np.empty(shape, np.float32) if out is None else out[c]
+            assert a.shape == shape and a.dtype == np.float32 and a.flags.c_contiguous
             _check(lib().yb_download_field(self._h, c, _fp(a)))
-            out.append(a)
-        return out
+            res.append(a)
+        return res
 
     def zero(self):
         _check(lib().yb_zero_fields(self._h))

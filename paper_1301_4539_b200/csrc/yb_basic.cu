@@ -156,6 +156,35 @@ __global__ void k_clamp_fill(Geo g, float* a) {
   a[gidx(g, i, j, k)] = a[gidx(g, min(i, g.nx - 1), min(j, g.ny - 1), min(k, g.nz - 1))];
 }
 
+// Dense (reference Array3 layout, extents e0 x e1 x e2) <-> padded node box.
+__global__ void k_scatter_dense(Geo g, int e0, int e1, int e2, const float* __restrict__ dense,
+                                float* __restrict__ padded) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i >= e0 || j >= e1 || k >= e2) return;
+  padded[gidx(g, i, j, k)] = dense[((long long)k * e1 + j) * e0 + i];
+}
+
+__global__ void k_gather_dense(Geo g, int e0, int e1, int e2, const float* __restrict__ padded,
+                               float* __restrict__ dense) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  if (i >= e0 || j >= e1 || k >= e2) return;
+  dense[((long long)k * e1 + j) * e0 + i] = padded[gidx(g, i, j, k)];
+}
+
+// *flag := 0 if any element's bit pattern differs from a[0].
+__global__ void k_all_equal(const float* __restrict__ a, long long n, int* flag) {
+  const unsigned v0 = __float_as_uint(a[0]);
+  bool same = true;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x)
+    same &= __float_as_uint(a[t]) == v0;
+  if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0) atomicExch(flag, 0);
+}
+
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + 1 + bx - 1) / bx, g.ny + 1, g.nz + 1); }
 
 }  // namespace
@@ -202,6 +231,25 @@ cudaError_t launch_fill_fields(const Geo& g, const Fields& F, uint64_t seed, cud
 cudaError_t launch_medium(const Geo& g, float* ca, float* cb, float* da, float* db,
                           long long eps_seed, long long sigma_seed, float S, cudaStream_t st) {
   k_medium<<<node_grid(g, 128), 128, 0, st>>>(g, ca, cb, da, db, eps_seed, sigma_seed, S);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_dense(const Geo& g, const int* e, const float* dense, float* padded,
+                                 cudaStream_t st) {
+  k_scatter_dense<<<dim3((e[0] + 127) / 128, e[1], e[2]), 128, 0, st>>>(g, e[0], e[1], e[2], dense,
+                                                                        padded);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded, float* dense,
+                                cudaStream_t st) {
+  k_gather_dense<<<dim3((e[0] + 127) / 128, e[1], e[2]), 128, 0, st>>>(g, e[0], e[1], e[2], padded,
+                                                                       dense);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_all_equal(const float* a, long long n, int* flag, int num_sms, cudaStream_t st) {
+  k_all_equal<<<num_sms * 4, 256, 0, st>>>(a, n, flag);
   return cudaGetLastError();
 }
 

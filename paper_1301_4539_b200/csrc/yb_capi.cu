@@ -109,6 +109,7 @@ struct yb_sim {
   int ntx = 1, nty = 1, nitems = 1;
   unsigned long long* sched = nullptr;  // device work counter of the fused kernel
   unsigned long long sched_base = 0;
+  int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
 };
 
 namespace {
@@ -268,6 +269,7 @@ int step_fused(yb_sim* s) {
   a.nitems = s->nitems;
   a.sched = s->sched;
   a.sched_base = s->sched_base;
+  a.store_policy = s->store_policy;
   a.co = coef_args(s);
   for (int c = 0; c < 6; ++c) {
     a.in[c] = s->buf[s->cur][c];
@@ -331,21 +333,25 @@ int check_comp(int comp) {
   return YB_OK;
 }
 
+// Host <-> device transfer of one dense reference-layout array through a
+// staging buffer: one linear cudaMemcpy at full link speed plus a device
+// scatter/gather into the padded node box (pitched 3D copies of short rows
+// run far below link speed). The staging buffer is the next-state buffer of
+// the same component, re-zeroed afterwards (its DoFs are rewritten by the
+// next step; its non-DoF positions must stay +0).
 int copy_dense(yb_sim* s, int comp, float* dev, const float* hsrc, float* hdst) {
   int e[3];
   comp_ext(s->g, comp, e);
-  cudaMemcpy3DParms p = {};
-  p.extent = make_cudaExtent((size_t)e[0] * 4, e[1], e[2]);
+  const size_t n = (size_t)e[0] * e[1] * e[2];
+  float* stage = s->buf[s->cur ^ 1][comp];
   if (hsrc) {
-    p.srcPtr = make_cudaPitchedPtr(const_cast<float*>(hsrc), (size_t)e[0] * 4, e[0], e[1]);
-    p.dstPtr = make_cudaPitchedPtr(dev, (size_t)s->g.PX * 4, s->g.PX, s->g.PY);
-    p.kind = cudaMemcpyHostToDevice;
+    YB_CU(cudaMemcpyAsync(stage, hsrc, n * 4, cudaMemcpyHostToDevice, s->stream));
+    YB_CU(yb::launch_scatter_dense(s->g, e, stage, dev, s->stream));
   } else {
-    p.srcPtr = make_cudaPitchedPtr(dev, (size_t)s->g.PX * 4, s->g.PX, s->g.PY);
-    p.dstPtr = make_cudaPitchedPtr(hdst, (size_t)e[0] * 4, e[0], e[1]);
-    p.kind = cudaMemcpyDeviceToHost;
+    YB_CU(yb::launch_gather_dense(s->g, e, dev, stage, s->stream));
+    YB_CU(cudaMemcpyAsync(hdst, stage, n * 4, cudaMemcpyDeviceToHost, s->stream));
   }
-  YB_CU(cudaMemcpy3DAsync(&p, s->stream));
+  YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
@@ -378,6 +384,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   s->device = d->device;
   s->variant = d->variant;
   s->zchunk_req = d->zchunk;
+  if (const char* e = std::getenv("YB_STPOL")) s->store_policy = std::atoi(e);
   Geo& g = s->g;
   g.nx = d->nx;
   g.ny = d->ny;
@@ -417,8 +424,8 @@ int yb_create(const yb_desc* d, yb_sim** out) {
       return bail(fail(YB_CUDA_ERROR, "cudaMalloc failed"));
     s->dev_bytes += ab;
   }
-  if (cudaMalloc(&s->sched, sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMemsetAsync(s->sched, 0, sizeof(unsigned long long), s->stream) != cudaSuccess)
+  if (cudaMalloc(&s->sched, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemsetAsync(s->sched, 0, 4 * sizeof(unsigned long long), s->stream) != cudaSuccess)
     return bail(fail(YB_CUDA_ERROR, "scheduler counter alloc failed"));
   if (int rc = upload_axis(s)) return bail(rc);
   static bool limits_set = false;
@@ -467,14 +474,23 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
   const long long n = (long long)s->g.nx * s->g.ny * s->g.nz;
   bool all_equal = false;
   float v = uniform;
+  float* stage = s->buf[s->cur ^ 1][0];  // staging (see copy_dense)
   if (cells) {
-    all_equal = true;
+    // linear upload, then a device check of uniformity (bit patterns)
+    YB_CU(cudaMemcpyAsync(stage, cells, (size_t)n * 4, cudaMemcpyHostToDevice, s->stream));
+    int* flag = reinterpret_cast<int*>(s->sched) + 2;  // scratch word next to the work counter
+    const int one = 1;
+    YB_CU(cudaMemcpyAsync(flag, &one, 4, cudaMemcpyHostToDevice, s->stream));
+    YB_CU(yb::launch_all_equal(stage, n, flag, s->num_sms, s->stream));
+    int same = 0;
+    YB_CU(cudaMemcpyAsync(&same, flag, 4, cudaMemcpyDeviceToHost, s->stream));
+    YB_CU(cudaStreamSynchronize(s->stream));
+    all_equal = same != 0;
     v = cells[0];
-    for (long long q = 1; q < n && all_equal; ++q)
-      if (std::memcmp(&cells[q], &v, 4) != 0) all_equal = false;
   }
   s->tm_valid = false;
   if (!cells || all_equal) {
+    if (cells) YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
     if (s->cell[which]) {
       YB_CU(cudaFree(s->cell[which]));
       s->cell[which] = nullptr;
@@ -500,13 +516,10 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
     YB_CU(cudaMemsetAsync(s->cell[which], 0, (size_t)s->g.total * 4, s->stream));
     s->dev_bytes += (size_t)s->g.total * 4;
   }
-  cudaMemcpy3DParms p = {};
-  p.extent = make_cudaExtent((size_t)s->g.nx * 4, s->g.ny, s->g.nz);
-  p.srcPtr = make_cudaPitchedPtr(const_cast<float*>(cells), (size_t)s->g.nx * 4, s->g.nx, s->g.ny);
-  p.dstPtr = make_cudaPitchedPtr(s->cell[which], (size_t)s->g.PX * 4, s->g.PX, s->g.PY);
-  p.kind = cudaMemcpyHostToDevice;
-  YB_CU(cudaMemcpy3DAsync(&p, s->stream));
+  const int ce[3] = {s->g.nx, s->g.ny, s->g.nz};
+  YB_CU(yb::launch_scatter_dense(s->g, ce, stage, s->cell[which], s->stream));
   YB_CU(yb::launch_clamp_fill(s->g, s->cell[which], s->stream));
+  YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }

@@ -90,9 +90,19 @@ __device__ __forceinline__ float4 shift_ip(float4 v, int lane, float right) {
   return make_float4(v.y, v.z, v.w, x);
 }
 
-__device__ __forceinline__ void store_row4(float* base, long long p, int i0, int nx, float4 v) {
+// 128-bit store with an L2 cache-policy hint (evict_first: the next-state
+// arrays are not read again in this launch, so they should not push the
+// halo rows neighbouring CTAs are about to read out of L2).
+__device__ __forceinline__ void stg4_hint(float* ptr, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
+__device__ __forceinline__ void store_row4(float* base, long long p, int i0, int nx, float4 v,
+                                           uint64_t pol) {
   if (i0 + 3 < nx) {
-    *reinterpret_cast<float4*>(base + p) = v;
+    stg4_hint(base + p, v, pol);
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -185,6 +195,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ======================= consumer warps ==================================
+  uint64_t st_pol;
+  if (a.store_policy == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(st_pol));
+  else if (a.store_policy == 2)
+    asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(st_pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(st_pol));
   const int r = w + 1, rn = w + 2, c = 4 + 4 * l;  // smem row of j, j+1; col of i0
   const bool hl = (l == 31);
   constexpr int cc = 4 + kTX;  // smem col of the +x halo column
@@ -255,9 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (jlt) {
         const long long p = gidx(g, i0, j, kh);
-        store_row4(a.out[3], p, i0, g.nx, hx);
-        store_row4(a.out[4], p, i0, g.nx, hy);
-        store_row4(a.out[5], p, i0, g.nx, hz);
+        store_row4(a.out[3], p, i0, g.nx, hx, st_pol);
+        store_row4(a.out[4], p, i0, g.nx, hy, st_pol);
+        store_row4(a.out[5], p, i0, g.nx, hz, st_pol);
       }
     };
 
@@ -371,9 +388,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (jlt && k < kz1) {
         const long long p = gidx(g, i0, j, k);
-        store_row4(a.out[0], p, i0, g.nx, exw);
-        store_row4(a.out[1], p, i0, g.nx, eyw);
-        store_row4(a.out[2], p, i0, g.nx, ezw);
+        store_row4(a.out[0], p, i0, g.nx, exw, st_pol);
+        store_row4(a.out[1], p, i0, g.nx, eyw, st_pol);
+        store_row4(a.out[2], p, i0, g.nx, ezw, st_pol);
       }
       if (k > kz0) h_row(k - 1, exw, eyw);
       pex = exw;

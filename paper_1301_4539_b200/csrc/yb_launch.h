@@ -31,6 +31,7 @@ struct FusedArgs {
   int nitems;    // work items = tiles * z-chunks, handed out by *sched
   unsigned long long* sched;     // monotonic global work counter
   unsigned long long sched_base; // counter value at this launch's start
+  int store_policy;              // L2 policy of next-state stores: 0 normal, 1 evict_first, 2 unchanged
   CoefArgs co;
   const float* in[6];
   float* out[6];
@@ -59,5 +60,10 @@ cudaError_t launch_fill_fields(const Geo& g, const Fields& F, uint64_t seed, cud
 cudaError_t launch_medium(const Geo& g, float* ca, float* cb, float* da, float* db,
                           long long eps_seed, long long sigma_seed, float S, cudaStream_t st);
 cudaError_t launch_clamp_fill(const Geo& g, float* a, cudaStream_t st);
+cudaError_t launch_scatter_dense(const Geo& g, const int* e, const float* dense, float* padded,
+                                 cudaStream_t st);
+cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded, float* dense,
+                                cudaStream_t st);
+cudaError_t launch_all_equal(const float* a, long long n, int* flag, int num_sms, cudaStream_t st);
 
 }  // namespace yb

@@ -63,3 +63,19 @@ def test_fails_loudly_without_gpu(yb):
 def test_invalid_arguments_rejected_before_gpu(yb):
     with pytest.raises(yb.YeeInvalidArgument):
         yb.Simulation(0, 8, 8)
+
+
+def build_shim_kat(tmp_path):
+    exe = os.path.join(str(tmp_path), "shim_kat")
+    r = subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "shim_kat.cpp"),
+                        "-L", os.path.join(ROOT, "paper_1301_4539_b200"), "-lyeeb200",
+                        "-Wl,-rpath," + os.path.join(ROOT, "paper_1301_4539_b200"), "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_cpp_shim_compiles(yb, tmp_path):
+    """The C++ drop-in (include/yeeb200/yeeblock.hpp) builds against the C-ABI."""
+    assert os.path.exists(build_shim_kat(tmp_path))

@@ -280,3 +280,14 @@ def test_full_size_fused_equals_naive(yb, cfg):
             sim.run(steps)
             digs.append(sim.digest())
     assert digs[0] == digs[1]
+
+
+def test_cpp_shim_known_answers(yb, tmp_path):
+    """The reference's Catch2 known-answer tests, restated in C++ against the
+    drop-in shim (tests/cpp/shim_kat.cpp), executed on the GPU."""
+    import subprocess
+    from tests.test_abi import build_shim_kat
+    exe = build_shim_kat(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "shim KATs ok" in r.stdout
