@@ -57,11 +57,13 @@ enum {
 typedef struct yb_sim yb_sim;
 
 typedef struct {
-  int nx, ny, nz; /* cells per axis (GridSpec, grid.hpp:17-43) */
+  int nx, ny, nz; /* cells per axis (GridSpec, grid.hpp:17-43); nz = this slab's depth */
   int device;     /* CUDA device ordinal */
   int variant;    /* YB_VARIANT_* */
-  int zchunk;     /* fused: z planes per CTA; 0 = auto */
-  int reserved[6];
+  int zchunk;     /* fused: z planes per work item; 0 = auto */
+  int z_offset;   /* z-slab mode: global index of local cell plane 0 (0 otherwise) */
+  int nz_global;  /* z-slab mode: global cell count along z (0 = nz, single domain) */
+  int reserved[4];
 } yb_desc;
 
 typedef struct {
@@ -151,6 +153,24 @@ int yb_apply_pec_boundary(yb_sim* sim);
 
 /* field_digest (fields.hpp:151-166): FNV-1a-64 over the dense Ex..Hz bytes. */
 int yb_field_digest(yb_sim* sim, uint64_t* out);
+
+/* z-slab decomposition (desc.nz_global > desc.nz; FUSED variant). The slab
+ * owns global cell planes [z_offset, z_offset+nz). Before each step the
+ * current state's ghost planes must be refreshed from the neighbours:
+ *   side 0 (bottom, rank below): send = my plane 0 of ex,ey,hx,hy,hz
+ *                                (5 planes); receive -> my ghost plane -1 (hx,hy)
+ *   side 1 (top, rank above):    send = my plane nz-1 of hx,hy (2 planes);
+ *                                receive -> my ghost plane nz (ex,ey,hx,hy,hz)
+ * Buffers are device memory of yb_halo_bytes(sim, side, 0|1) bytes
+ * (0: what this side sends, 1: what it receives); plane = PX*PY floats. A
+ * slab's dense field arrays are the local part of the global Array3 (node-z
+ * components carry nz+1 planes; the top one belongs to the rank above unless
+ * this is the global top). Per-cell coefficient uploads carry nz planes plus,
+ * below the global top, the first plane of the slab above. Axis coefficient
+ * cdz is the GLOBAL array (length nz_global). */
+int yb_halo_bytes(yb_sim* sim, int side, int receive, size_t* bytes);
+int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
+int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
 
 /* Work on a caller-owned stream (e.g. torch.cuda.current_stream()); NULL
  * restores the handle's own stream. */

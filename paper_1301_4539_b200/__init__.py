@@ -37,7 +37,7 @@ ABI_SYMBOLS = (
     "yb_add_source", "yb_clear_sources", "yb_advance", "yb_synchronize", "yb_advance_timed",
     "yb_apply_ampere_range", "yb_apply_faraday_range", "yb_apply_pec_boundary",
     "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
-    "yb_host_medium", "yb_host_field",
+    "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
 )
 
 
@@ -55,7 +55,8 @@ class YeeOutOfRange(YeeError, IndexError):
 
 class _Desc(C.Structure):
     _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("device", C.c_int),
-                ("variant", C.c_int), ("zchunk", C.c_int), ("reserved", C.c_int * 6)]
+                ("variant", C.c_int), ("zchunk", C.c_int), ("z_offset", C.c_int),
+                ("nz_global", C.c_int), ("reserved", C.c_int * 4)]
 
 
 class Info(C.Structure):
@@ -115,6 +116,9 @@ def lib():
         L.yb_host_medium.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
                                      _f32p, _f32p, _f32p, _f32p]
         L.yb_host_field.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _f32p]
+        L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
+        L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
+        L.yb_halo_unpack.argtypes = [vp, C.c_int, vp]
         _lib = L
     return _lib
 
@@ -155,15 +159,18 @@ class Simulation:
     """
 
     def __init__(self, nx, ny, nz, device=0, variant=VARIANT_FUSED, zchunk=0, cdx=None, cdy=None,
-                 cdz=None):
+                 cdz=None, z_offset=0, nz_global=0):
+        """nz_global > 0: this handle is the z-slab [z_offset, z_offset+nz) of a grid with
+        nz_global cell planes (halo exchange: halo_pack / halo_unpack, see slabs.py)."""
         self.nx, self.ny, self.nz = nx, ny, nz
+        self.z_offset, self.nz_global = z_offset, (nz_global or nz)
         h = C.c_void_p()
-        d = _Desc(nx, ny, nz, device, variant, zchunk)
+        d = _Desc(nx, ny, nz, device, variant, zchunk, z_offset, nz_global)
         _check(lib().yb_create(C.byref(d), C.byref(h)))
         self._h = h
         self.set_axis_coeffs(np.full(nx, S, np.float32) if cdx is None else cdx,
                              np.full(ny, S, np.float32) if cdy is None else cdy,
-                             np.full(nz, S, np.float32) if cdz is None else cdz)
+                             np.full(self.nz_global, S, np.float32) if cdz is None else cdz)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -185,7 +192,7 @@ class Simulation:
     # coefficients ---------------------------------------------------------
     def set_axis_coeffs(self, cdx, cdy, cdz):
         cdx, cdy, cdz = _f32c(cdx), _f32c(cdy), _f32c(cdz)
-        assert cdx.size == self.nx and cdy.size == self.ny and cdz.size == self.nz
+        assert cdx.size == self.nx and cdy.size == self.ny and cdz.size == self.nz_global
         _check(lib().yb_set_axis_coeffs(self._h, _fp(cdx), _fp(cdy), _fp(cdz)))
 
     def set_cell_coeffs(self, which, cells=None, uniform=1.0):
@@ -193,7 +200,8 @@ class Simulation:
             _check(lib().yb_set_cell_coeffs(self._h, which, None, uniform))
         else:
             cells = _f32c(cells)
-            assert cells.size == self.nx * self.ny * self.nz
+            at_top = self.z_offset + self.nz == self.nz_global
+            assert cells.size == self.nx * self.ny * (self.nz + (0 if at_top else 1))
             _check(lib().yb_set_cell_coeffs(self._h, which, _fp(cells), uniform))
 
     def generate_medium(self, eps_seed=-1, sigma_seed=-1):
@@ -273,6 +281,18 @@ class Simulation:
 
     def set_stream(self, stream_ptr):
         _check(lib().yb_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    # z-slab halo planes (device pointers, e.g. torch CUDA tensor .data_ptr())
+    def halo_bytes(self, side, receive):
+        v = C.c_size_t()
+        _check(lib().yb_halo_bytes(self._h, side, 1 if receive else 0, C.byref(v)))
+        return v.value
+
+    def halo_pack(self, side, dst_ptr):
+        _check(lib().yb_halo_pack(self._h, side, C.c_void_p(dst_ptr)))
+
+    def halo_unpack(self, side, src_ptr):
+        _check(lib().yb_halo_unpack(self._h, side, C.c_void_p(src_ptr)))
 
     def set_kernel_timing(self, on):
         _check(lib().yb_set_kernel_timing(self._h, 1 if on else 0))

@@ -101,8 +101,9 @@ __global__ void k_faces(Geo g, Fields in, Fields out, CoefArgs co) {
     face_point(g, in.f, out.f, co, t);
 }
 
+// Extents of component c on the GLOBAL grid (nz -> nzg).
 __device__ __forceinline__ void comp_ext(const Geo& g, int c, int e[3]) {
-  const int n[3] = {g.nx, g.ny, g.nz};
+  const int n[3] = {g.nx, g.ny, g.nzg};
   const int axis = c % 3;
   for (int a = 0; a < 3; ++a) {
     const bool node = c < 3 ? (a != axis) : (a == axis);
@@ -110,19 +111,21 @@ __device__ __forceinline__ void comp_ext(const Geo& g, int c, int e[3]) {
   }
 }
 
-// Seeded fields over each component's extents (dense reference index).
+// Seeded fields over each component's extents, hashed by the GLOBAL dense
+// reference index, so any z-slab partition generates the same state.
 __global__ void k_fill_fields(Geo g, Fields F, uint64_t seed) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   const int k = blockIdx.z;
   if (i > g.nx) return;
   const long long p = gidx(g, i, j, k);
+  const int kg = k + g.zoff;
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
     int e[3];
     comp_ext(g, c, e);
-    if (i < e[0] && j < e[1] && k < e[2]) {
-      const uint64_t dense = ((uint64_t)k * e[1] + j) * e[0] + i;
+    if (i < e[0] && j < e[1] && kg < e[2]) {
+      const uint64_t dense = ((uint64_t)kg * e[1] + j) * e[0] + i;
       F.f[c][p] = yb_field_value(seed, c, dense);
     }
   }
@@ -135,7 +138,7 @@ __global__ void k_medium(Geo g, float* ca, float* cb, float* da, float* db, long
   const int j = blockIdx.y;
   const int k = blockIdx.z;
   if (i > g.nx) return;
-  const int ci = min(i, g.nx - 1), cj = min(j, g.ny - 1), ck = min(k, g.nz - 1);
+  const int ci = min(i, g.nx - 1), cj = min(j, g.ny - 1), ck = min(k + g.zoff, g.nzg - 1);
   const uint64_t cell = ((uint64_t)ck * g.ny + cj) * g.nx + ci;
   const yb_cell_coeffs q = yb_cell_coeffs_at(eps_seed, sigma_seed, cell, S);
   const long long p = gidx(g, i, j, k);
@@ -145,15 +148,15 @@ __global__ void k_medium(Geo g, float* ca, float* cb, float* da, float* db, long
   if (db) db[p] = q.db;
 }
 
-// After a dense upload into [0,nx)x[0,ny)x[0,nz): fill the clamped
-// duplicates at i=nx, j=ny, k=nz.
-__global__ void k_clamp_fill(Geo g, float* a) {
+// After a dense upload into [0,nx)x[0,ny)x[0,kmax]: fill the clamped
+// duplicates at i=nx, j=ny and planes k > kmax.
+__global__ void k_clamp_fill(Geo g, float* a, int kmax) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   const int k = blockIdx.z;
   if (i > g.nx) return;
-  if (i < g.nx && j < g.ny && k < g.nz) return;
-  a[gidx(g, i, j, k)] = a[gidx(g, min(i, g.nx - 1), min(j, g.ny - 1), min(k, g.nz - 1))];
+  if (i < g.nx && j < g.ny && k <= kmax) return;
+  a[gidx(g, i, j, k)] = a[gidx(g, min(i, g.nx - 1), min(j, g.ny - 1), min(k, kmax))];
 }
 
 // Dense (reference Array3 layout, extents e0 x e1 x e2) <-> padded node box.
@@ -253,8 +256,8 @@ cudaError_t launch_all_equal(const float* a, long long n, int* flag, int num_sms
   return cudaGetLastError();
 }
 
-cudaError_t launch_clamp_fill(const Geo& g, float* a, cudaStream_t st) {
-  k_clamp_fill<<<node_grid(g, 128), 128, 0, st>>>(g, a);
+cudaError_t launch_clamp_fill(const Geo& g, float* a, int kmax, cudaStream_t st) {
+  k_clamp_fill<<<node_grid(g, 128), 128, 0, st>>>(g, a, kmax);
   return cudaGetLastError();
 }
 

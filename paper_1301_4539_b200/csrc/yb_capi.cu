@@ -129,8 +129,11 @@ int upload_axis(yb_sim* s) {
     const float uv = side == 0 ? s->cb_u : s->db_u;
     for (int a = 0; a < 3; ++a) {
       std::vector<float> h(s->axis_len[a], 0.0f);
-      const int n = a == 0 ? s->g.nx : (a == 1 ? s->g.ny : s->g.nz);
-      for (int q = 0; q < n; ++q) h[q] = uni ? uv : s->axis_ref[a][q];
+      // x, y: full arrays; z: local planes 0..nz of the global array (plane
+      // nz is the ghost plane's value below the global top)
+      const int off = a == 2 ? s->g.zoff : 0;
+      const int n = (int)s->axis_ref[a].size() - off;
+      for (int q = 0; q < n && q < s->axis_len[a]; ++q) h[q] = uni ? uv : s->axis_ref[a][off + q];
       YB_CU(cudaMemcpyAsync(s->axis_dev[side * 3 + a], h.data(), h.size() * sizeof(float),
                             cudaMemcpyHostToDevice, s->stream));
     }
@@ -162,14 +165,15 @@ yb::Fields fields_of(const yb_sim* s, int b) {
 int encode_map(CUtensorMap* m, const Geo& g, float* base) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ};
+  // z coordinate = local plane + 1: the allocation starts at ghost plane -1
+  const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ + 1};
   const cuuint64_t strides[2] = {(cuuint64_t)g.PX * 4, (cuuint64_t)g.plane * 4};
   const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)yb::kBY, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   // YB_L2PROMO=0..3 (tuning knob): none / 64B / 128B / 256B L2 promotion
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (const char* e = std::getenv("YB_L2PROMO")) promo = (CUtensorMapL2promotion)std::atoi(e);
-  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base - g.plane, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -238,7 +242,7 @@ yb::SrcArgs sources_at(const yb_sim* s, int64_t step) {
     a.comp[a.n] = q.comp;
     a.i[a.n] = q.i;
     a.j[a.n] = q.j;
-    a.k[a.n] = q.k;
+    a.k[a.n] = q.k - s->g.zoff;  // local plane (may be outside the slab)
     a.val[a.n] = q.table[step];
     ++a.n;
   }
@@ -351,7 +355,7 @@ int copy_dense(yb_sim* s, int comp, float* dev, const float* hsrc, float* hdst) 
     YB_CU(yb::launch_gather_dense(s->g, e, dev, stage, s->stream));
     YB_CU(cudaMemcpyAsync(hdst, stage, n * 4, cudaMemcpyDeviceToHost, s->stream));
   }
-  YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
+  YB_CU(cudaMemsetAsync(stage - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
@@ -379,6 +383,13 @@ int yb_create(const yb_desc* d, yb_sim** out) {
     return fail(YB_INVALID_ARGUMENT, "grid too large for this build");
   if (d->variant != YB_VARIANT_FUSED && d->variant != YB_VARIANT_NAIVE)
     return fail(YB_INVALID_ARGUMENT, "unknown variant %d", d->variant);
+  if (d->nz_global > 0 && (d->z_offset < 0 || d->z_offset + d->nz > d->nz_global))
+    return fail(YB_INVALID_ARGUMENT, "slab [%d,%d) outside the global grid of %d planes",
+                d->z_offset, d->z_offset + d->nz, d->nz_global);
+  if (d->nz_global <= 0 && d->z_offset != 0)
+    return fail(YB_INVALID_ARGUMENT, "z_offset needs nz_global");
+  if (d->nz_global > 0 && d->nz_global != d->nz && d->variant != YB_VARIANT_FUSED)
+    return fail(YB_INVALID_ARGUMENT, "z-slab mode needs the fused variant");
   YB_CU(cudaSetDevice(d->device));
   yb_sim* s = new yb_sim;
   s->device = d->device;
@@ -389,11 +400,13 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   g.nx = d->nx;
   g.ny = d->ny;
   g.nz = d->nz;
+  g.zoff = d->z_offset;
+  g.nzg = d->nz_global > 0 ? d->nz_global : d->nz;
   g.PX = ((d->nx + 1 + 31) / 32) * 32;
   g.PY = d->ny + 1;
   g.PZ = d->nz + 1;
   g.plane = (long long)g.PX * g.PY;
-  g.total = g.plane * (g.PZ + 2);  // +2 guard planes for masked over-reads
+  g.total = g.plane * (g.PZ + 3);  // ghost plane -1, planes 0..nz, 2 guard planes
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, d->device);
   if (dev_sms > 0) s->num_sms = dev_sms;
@@ -407,16 +420,18 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   const size_t bytes = (size_t)g.total * sizeof(float);
   for (int b = 0; b < 2; ++b)
     for (int c = 0; c < 6; ++c) {
-      if (cudaMalloc(&s->buf[b][c], bytes) != cudaSuccess)
+      float* p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess)
         return bail(fail(YB_CUDA_ERROR, "cudaMalloc of %zu bytes failed", bytes));
+      s->buf[b][c] = p + g.plane;
       s->dev_bytes += bytes;
-      if (cudaMemsetAsync(s->buf[b][c], 0, bytes, s->stream) != cudaSuccess)
+      if (cudaMemsetAsync(p, 0, bytes, s->stream) != cudaSuccess)
         return bail(fail(YB_CUDA_ERROR, "memset failed"));
     }
   const int ns[3] = {g.nx, g.ny, g.nz};
   for (int a = 0; a < 3; ++a) {
     s->axis_len[a] = ((ns[a] + yb::kTX) / yb::kTX + 1) * yb::kTX + 64;
-    s->axis_ref[a].assign(ns[a], 0.0f);
+    s->axis_ref[a].assign(a == 2 ? g.nzg : ns[a], 0.0f);  // z: the global array
   }
   for (int q = 0; q < 6; ++q) {
     const size_t ab = (size_t)s->axis_len[q % 3] * sizeof(float);
@@ -445,8 +460,10 @@ int yb_destroy(yb_sim* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (int b = 0; b < 2; ++b)
-    for (int c = 0; c < 6; ++c) cudaFree(s->buf[b][c]);
-  for (int q = 0; q < 4; ++q) cudaFree(s->cell[q]);
+    for (int c = 0; c < 6; ++c)
+      if (s->buf[b][c]) cudaFree(s->buf[b][c] - s->g.plane);
+  for (int q = 0; q < 4; ++q)
+    if (s->cell[q]) cudaFree(s->cell[q] - s->g.plane);
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
   for (auto& t : s->timers) {
@@ -463,7 +480,7 @@ int yb_set_axis_coeffs(yb_sim* s, const float* cdx, const float* cdy, const floa
   YB_CU(cudaSetDevice(s->device));
   s->axis_ref[0].assign(cdx, cdx + s->g.nx);
   s->axis_ref[1].assign(cdy, cdy + s->g.ny);
-  s->axis_ref[2].assign(cdz, cdz + s->g.nz);
+  s->axis_ref[2].assign(cdz, cdz + s->g.nzg);
   return upload_axis(s);
 }
 
@@ -471,7 +488,9 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
   YB_CU(cudaSetDevice(s->device));
-  const long long n = (long long)s->g.nx * s->g.ny * s->g.nz;
+  // slab mode below the global top: + the first cell plane of the slab above
+  const int nzc = yb::at_top(s->g) ? s->g.nz : s->g.nz + 1;
+  const long long n = (long long)s->g.nx * s->g.ny * nzc;
   bool all_equal = false;
   float v = uniform;
   float* stage = s->buf[s->cur ^ 1][0];  // staging (see copy_dense)
@@ -490,9 +509,9 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
   }
   s->tm_valid = false;
   if (!cells || all_equal) {
-    if (cells) YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
+    if (cells) YB_CU(cudaMemsetAsync(stage - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
     if (s->cell[which]) {
-      YB_CU(cudaFree(s->cell[which]));
+      YB_CU(cudaFree(s->cell[which] - s->g.plane));
       s->cell[which] = nullptr;
       s->dev_bytes -= (size_t)s->g.total * 4;
     }
@@ -512,14 +531,16 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
   if (which == YB_CB) s->cb_uniform = false;
   if (which == YB_DB) s->db_uniform = false;
   if (!s->cell[which]) {
-    YB_CU(cudaMalloc(&s->cell[which], (size_t)s->g.total * 4));
-    YB_CU(cudaMemsetAsync(s->cell[which], 0, (size_t)s->g.total * 4, s->stream));
+    float* p = nullptr;
+    YB_CU(cudaMalloc(&p, (size_t)s->g.total * 4));
+    YB_CU(cudaMemsetAsync(p, 0, (size_t)s->g.total * 4, s->stream));
+    s->cell[which] = p + s->g.plane;
     s->dev_bytes += (size_t)s->g.total * 4;
   }
-  const int ce[3] = {s->g.nx, s->g.ny, s->g.nz};
+  const int ce[3] = {s->g.nx, s->g.ny, nzc};
   YB_CU(yb::launch_scatter_dense(s->g, ce, stage, s->cell[which], s->stream));
-  YB_CU(yb::launch_clamp_fill(s->g, s->cell[which], s->stream));
-  YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
+  YB_CU(yb::launch_clamp_fill(s->g, s->cell[which], nzc - 1, s->stream));
+  YB_CU(cudaMemsetAsync(stage - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
@@ -531,15 +552,17 @@ int yb_generate_medium(yb_sim* s, int64_t eps_seed, int64_t sigma_seed) {
   s->tm_valid = false;
   auto ensure = [&](int q) -> int {
     if (!s->cell[q]) {
-      YB_CU(cudaMalloc(&s->cell[q], (size_t)s->g.total * 4));
-      YB_CU(cudaMemsetAsync(s->cell[q], 0, (size_t)s->g.total * 4, s->stream));
+      float* p = nullptr;
+      YB_CU(cudaMalloc(&p, (size_t)s->g.total * 4));
+      YB_CU(cudaMemsetAsync(p, 0, (size_t)s->g.total * 4, s->stream));
+      s->cell[q] = p + s->g.plane;
       s->dev_bytes += (size_t)s->g.total * 4;
     }
     return YB_OK;
   };
   auto drop = [&](int q) -> int {
     if (s->cell[q]) {
-      YB_CU(cudaFree(s->cell[q]));
+      YB_CU(cudaFree(s->cell[q] - s->g.plane));
       s->cell[q] = nullptr;
       s->dev_bytes -= (size_t)s->g.total * 4;
     }
@@ -620,7 +643,7 @@ int yb_zero_fields(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   YB_CU(cudaSetDevice(s->device));
   for (int c = 0; c < 6; ++c)
-    YB_CU(cudaMemsetAsync(s->buf[s->cur][c], 0, (size_t)s->g.total * 4, s->stream));
+    YB_CU(cudaMemsetAsync(s->buf[s->cur][c] - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   s->step_index = 0;
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
@@ -655,7 +678,7 @@ int yb_add_source(yb_sim* s, int comp, int i, int j, int k, const float* table, 
     return fail(YB_INVALID_ARGUMENT, "at most %d sources", YB_MAX_SOURCES);
   // strictly interior (source.hpp:43-55): node axes 1..n-1, the half axis 1..n-2
   const int idx[3] = {i, j, k};
-  const int ns[3] = {s->g.nx, s->g.ny, s->g.nz};
+  const int ns[3] = {s->g.nx, s->g.ny, s->g.nzg};
   for (int a = 0; a < 3; ++a) {
     const bool node = a != comp;
     const int lo = 1, hi = node ? ns[a] : ns[a] - 1;
@@ -728,8 +751,11 @@ static int check_box(const yb_sim* s, const int* box, int out[6]) {
   return YB_OK;
 }
 
+static bool slab_mode(const yb_sim* s) { return s->g.nzg != s->g.nz; }
+
 int yb_apply_ampere_range(yb_sim* s, const int* box) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   int b[6];
   if (int rc = check_box(s, box, b)) return fail(rc, "apply_ampere_range: range out of bounds");
   YB_CU(cudaSetDevice(s->device));
@@ -740,6 +766,7 @@ int yb_apply_ampere_range(yb_sim* s, const int* box) {
 
 int yb_apply_faraday_range(yb_sim* s, const int* box) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   int b[6];
   if (int rc = check_box(s, box, b)) return fail(rc, "apply_faraday_range: range out of bounds");
   YB_CU(cudaSetDevice(s->device));
@@ -750,6 +777,7 @@ int yb_apply_faraday_range(yb_sim* s, const int* box) {
 
 int yb_apply_pec_boundary(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   YB_CU(cudaSetDevice(s->device));
   YB_CU(yb::launch_naive_pec(s->g, fields_of(s, s->cur), s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
@@ -772,6 +800,55 @@ int yb_field_digest(yb_sim* s, uint64_t* out) {
     }
   }
   *out = h;
+  return YB_OK;
+}
+
+// z-slab halo planes (see include/yeeb200.h). Planes are contiguous
+// (PX*PY floats), so packing is one device-to-device copy per array.
+static const int kHaloDownComps[5] = {YB_EX, YB_EY, YB_HX, YB_HY, YB_HZ};
+static const int kHaloUpComps[2] = {YB_HX, YB_HY};
+
+int yb_halo_bytes(yb_sim* s, int side, int receive, size_t* bytes) {
+  if (!s || !bytes || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  // side 0 sends 5 planes down and receives 2; side 1 sends 2 up and receives 5
+  const int planes = (side == 0) != (receive != 0) ? 5 : 2;
+  *bytes = (size_t)planes * s->g.plane * sizeof(float);
+  return YB_OK;
+}
+
+int yb_halo_pack(yb_sim* s, int side, void* dst) {
+  if (!s || !dst || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  YB_CU(cudaSetDevice(s->device));
+  const size_t pb = (size_t)s->g.plane * sizeof(float);
+  char* out = static_cast<char*>(dst);
+  if (side == 0) {  // my plane 0 -> the rank below's top ghost
+    for (int q = 0; q < 5; ++q)
+      YB_CU(cudaMemcpyAsync(out + q * pb, s->buf[s->cur][kHaloDownComps[q]], pb,
+                            cudaMemcpyDeviceToDevice, s->stream));
+  } else {  // my plane nz-1 (hx, hy) -> the rank above's bottom ghost
+    for (int q = 0; q < 2; ++q)
+      YB_CU(cudaMemcpyAsync(out + q * pb, s->buf[s->cur][kHaloUpComps[q]] + (s->g.nz - 1) * s->g.plane,
+                            pb, cudaMemcpyDeviceToDevice, s->stream));
+  }
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_halo_unpack(yb_sim* s, int side, const void* src) {
+  if (!s || !src || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  YB_CU(cudaSetDevice(s->device));
+  const size_t pb = (size_t)s->g.plane * sizeof(float);
+  const char* in = static_cast<const char*>(src);
+  if (side == 0) {  // the rank below's plane nz-1 (hx, hy) -> my ghost plane -1
+    for (int q = 0; q < 2; ++q)
+      YB_CU(cudaMemcpyAsync(s->buf[s->cur][kHaloUpComps[q]] - s->g.plane, in + q * pb, pb,
+                            cudaMemcpyDeviceToDevice, s->stream));
+  } else {  // the rank above's plane 0 -> my ghost plane nz
+    for (int q = 0; q < 5; ++q)
+      YB_CU(cudaMemcpyAsync(s->buf[s->cur][kHaloDownComps[q]] + s->g.nz * s->g.plane, in + q * pb, pb,
+                            cudaMemcpyDeviceToDevice, s->stream));
+  }
+  YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
 

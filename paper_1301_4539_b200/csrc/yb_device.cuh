@@ -16,12 +16,19 @@ namespace yb {
 
 constexpr int kMaxSources = 8;
 
+// nz is the local slab depth; zoff/nzg place the slab in the global grid
+// (single GPU: zoff = 0, nzg = nz). Arrays carry one ghost plane below
+// local plane 0 (base pointer = allocation + one plane).
 struct Geo {
   int nx, ny, nz;
   int PX, PY, PZ;
   long long plane;  // PX*PY
-  long long total;  // floats per array incl. guard
+  long long total;  // floats per allocation: ghost + PZ planes + 2 guard planes
+  int zoff, nzg;    // global index of local plane 0, global cell count along z
 };
+
+__host__ __device__ __forceinline__ bool at_bottom(const Geo& g) { return g.zoff == 0; }
+__host__ __device__ __forceinline__ bool at_top(const Geo& g) { return g.zoff + g.nz == g.nzg; }
 
 struct SrcArgs {
   int n;
@@ -68,15 +75,20 @@ __device__ __forceinline__ float coefB(const float* cell, const float* axis, int
 // i=nx, hy at j=ny, hz at k=nz) reads only those PEC zeros, so its update is
 // Da*h + (Db*(0-0) - Db*(0-0)), computed in exactly that form. Reads `in`,
 // writes `out` (disjoint from the sweep's writes).
+// Owned node planes of the slab: 0..nz-1, plus plane nz at the global top.
+__device__ __forceinline__ int face_nk(const Geo& g) { return at_top(g) ? g.nz + 1 : g.nz; }
+
 __device__ __forceinline__ long long face_points(const Geo& g) {
-  return (long long)(g.ny + 1) * (g.nz + 1) + (long long)(g.nx + 1) * (g.nz + 1) +
-         (long long)(g.nx + 1) * (g.ny + 1);
+  const int nk = face_nk(g);
+  return (long long)(g.ny + 1) * nk + (long long)(g.nx + 1) * nk +
+         (at_top(g) ? (long long)(g.nx + 1) * (g.ny + 1) : 0LL);
 }
 
 __device__ __forceinline__ void face_point(const Geo& g, const float* const* in,
                                            float* const* out, const CoefArgs& co, long long t) {
-  const long long nxf = (long long)(g.ny + 1) * (g.nz + 1);
-  const long long nyf = (long long)(g.nx + 1) * (g.nz + 1);
+  const int nk = face_nk(g);
+  const long long nxf = (long long)(g.ny + 1) * nk;
+  const long long nyf = (long long)(g.nx + 1) * nk;
   if (t < nxf) {
     const int j = (int)(t % (g.ny + 1)), k = (int)(t / (g.ny + 1)), i = g.nx;
     const long long p = gidx(g, i, j, k);

@@ -172,23 +172,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         p_e = 0;
         const int kz0 = (it / T) * a.zchunk;
         const int kz1 = min(kz0 + a.zchunk, g.nz);
-        p_nE = (kz0 > 0 ? 1 : 0) + ((kz1 == g.nz) ? g.nz - 1 : kz1) - kz0 + 1;
+        const bool pro = kz0 > 0 || !at_bottom(g);
+        const int kend = (kz1 == g.nz && at_top(g)) ? g.nz - 1 : kz1;
+        p_nE = (pro ? 1 : 0) + kend - kz0 + 1;
       }
       const int chunk = p_item / T, tile = p_item - chunk * T;
       const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
       const int kz0 = chunk * a.zchunk;
-      const int pro = kz0 > 0 ? 1 : 0;
+      const int pro = (kz0 > 0 || !at_bottom(g)) ? 1 : 0;
       float* dst = stages + (size_t)s * NARR * kSlot;
+      // tensor z coordinate = local plane + 1 (ghost plane -1 is z = 0)
       if (pro && p_e == 0) {
         mbar_expect_tx(bar, 2 * kBoxBytes);
-        tma_load_3d(smem_u32(dst + 3 * kSlot), &tm.m[3], x0 - 4, y0 - 1, kz0 - 1, bar);
-        tma_load_3d(smem_u32(dst + 4 * kSlot), &tm.m[4], x0 - 4, y0 - 1, kz0 - 1, bar);
+        tma_load_3d(smem_u32(dst + 3 * kSlot), &tm.m[3], x0 - 4, y0 - 1, kz0, bar);
+        tma_load_3d(smem_u32(dst + 4 * kSlot), &tm.m[4], x0 - 4, y0 - 1, kz0, bar);
       } else {
         const int k = kz0 + p_e - pro;
         mbar_expect_tx(bar, NARR * kBoxBytes);
 #pragma unroll
         for (int qq = 0; qq < NARR; ++qq)
-          tma_load_3d(smem_u32(dst + qq * kSlot), &tm.m[qq], x0 - 4, y0 - 1, k, bar);
+          tma_load_3d(smem_u32(dst + qq * kSlot), &tm.m[qq], x0 - 4, y0 - 1, k + 1, bar);
       }
       if (++p_e == p_nE) p_item = -1;
     }
@@ -231,8 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
     const int kz0 = chunk * a.zchunk;
     const int kz1 = min(kz0 + a.zchunk, g.nz);
-    const bool top = (kz1 == g.nz);
-    const int kend = top ? g.nz - 1 : kz1;
+    const bool top = (kz1 == g.nz) && at_top(g);  // global top: E(nz) is PEC
+    const int kend = top ? g.nz - 1 : kz1;      // else stream plane kz1 (maybe the ghost)
 
     const int j = y0 + w, jn = j + 1;
     const int i0 = x0 + 4 * l;
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
 
-    if (kz0 > 0) {  // prologue element: H^{n+1/2} on plane kz0-1
+    if (kz0 > 0 || !at_bottom(g)) {  // prologue element: H^{n+1/2} on plane kz0-1
       const int s = wait_elem();
       const float* st = stages + (size_t)s * NARR * kSlot;
       phx = lds4(st + 3 * kSlot + r * kBX + c);
@@ -293,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* st = stages + (size_t)s * NARR * kSlot;
 #define SM(q, rr, col) (st + (q) * kSlot + (rr) * kBX + (col))
       const float cdz_e = co.cdz_e[k];
-      const bool kin = k >= 1 && k < g.nz;
+      const int kg = k + g.zoff;  // global plane (PEC at global z = 0, nzg)
+      const bool kin = kg >= 1 && kg < g.nzg;
       // own row j
       const float4 ex = lds4(SM(0, r, c)), ey = lds4(SM(1, r, c)), ez = lds4(SM(2, r, c));
       const float4 hx = lds4(SM(3, r, c)), hy = lds4(SM(4, r, c)), hz = lds4(SM(5, r, c));

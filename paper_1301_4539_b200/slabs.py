@@ -1,0 +1,78 @@
+"""z-slab domain decomposition across ranks (one GPU per rank, §8(e)).
+
+The grid is split along z into contiguous cell slabs [K_r, K_{r+1})
+(partition). Each step needs, per interface, one plane of H going up
+(hx, hy of the slab's last plane -> the slab above's ghost plane -1, read by
+its first E update, kernels.hpp:18-19 `k-1`) and one plane of state going
+down (ex, ey, hx, hy, hz of the slab's first plane -> the slab below's ghost
+plane nz, from which it recomputes E^{n+1} on that plane for its last H
+update, kernels.hpp:23-24 `k+1`). This is the paper's "2 fields per face"
+exchange plus the three fields the recompute reads.
+Decomposition changes no arithmetic: results are bit-identical to one domain.
+
+HaloExchange is transport-agnostic: it moves the planes with
+torch.distributed point-to-point ops (NCCL between GPUs, gloo on CPU in the
+tests). `sim` is anything with halo_bytes/halo_pack/halo_unpack (the CUDA
+Simulation, or the CPU slab oracle in tests).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def partition(nz_global: int, world: int):
+    """[(z_offset, nz_local)] per rank: contiguous, near-equal cell slabs."""
+    if world < 1 or nz_global < world:
+        raise ValueError(f"cannot split {nz_global} planes over {world} ranks")
+    bounds = [r * nz_global // world for r in range(world + 1)]
+    return [(bounds[r], bounds[r + 1] - bounds[r]) for r in range(world)]
+
+
+class HaloExchange:
+    """Per-step ghost-plane refresh between neighbouring slabs."""
+
+    def __init__(self, sim, rank: int, world: int, device, group=None):
+        self.sim, self.group = sim, group
+        self.below = rank - 1 if rank > 0 else None
+        self.above = rank + 1 if rank < world - 1 else None
+        self.device = torch.device(device)
+        self.buf = {}
+        for side, peer in ((0, self.below), (1, self.above)):
+            if peer is None:
+                continue
+            self.buf[side] = (
+                torch.empty(sim.halo_bytes(side, False), dtype=torch.uint8, device=self.device),
+                torch.empty(sim.halo_bytes(side, True), dtype=torch.uint8, device=self.device))
+        self.bytes_per_exchange = sum(s.numel() for s, _ in self.buf.values())
+
+    def exchange(self):
+        for side, (send, _) in self.buf.items():
+            self.sim.halo_pack(side, send.data_ptr())
+        ops = []
+        for side, (send, recv) in self.buf.items():
+            peer = self.below if side == 0 else self.above
+            ops.append(dist.P2POp(dist.isend, send, peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            if self.device.type == "cuda":
+                torch.cuda.synchronize(self.device)  # unpack runs on the sim's own stream
+        for side, (_, recv) in self.buf.items():
+            self.sim.halo_unpack(side, recv.data_ptr())
+
+
+def run_steps(sim, exchanger: HaloExchange, nsteps: int):
+    """Advance nsteps, refreshing ghost planes before every step."""
+    for _ in range(nsteps):
+        exchanger.exchange()
+        sim.run(1, sync=False)
+
+
+def owned_planes(comp: int, nz_local: int, at_top: bool) -> int:
+    """Planes of component `comp`'s dense slab array this rank owns: node-z
+    components (ex, ey, hz) have nz_local+1 planes; the last belongs to the
+    slab above unless this is the global top."""
+    node_z = comp in (0, 1, 5)
+    return nz_local + (1 if node_z and at_top else 0)

@@ -1,0 +1,193 @@
+"""z-slab decomposition (§8(e)). CPU: the slab semantics (ghost planes,
+recomputed top plane, global PEC) on the numpy slab oracle, and the
+HaloExchange protocol across 2 processes over gloo, both bit-exact against
+the single-domain C oracle. GPU: slabs of the CUDA path in one process on one
+GPU, exchanging through device buffers, bit-exact against one domain."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1301_4539_b200.slabs import HaloExchange, partition
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.ascontiguousarray(a).view(np.uint32), np.ascontiguousarray(b).view(np.uint32))
+
+
+def test_partition():
+    assert partition(10, 3) == [(0, 3), (3, 3), (6, 4)]
+    assert partition(8, 8) == [(r, 1) for r in range(8)]
+    with pytest.raises(ValueError):
+        partition(3, 4)
+
+
+CASE = dict(nx=13, ny=11, nzg=17, steps=9, medium=(7, 7), fseed=8)
+
+
+def reference_run(oracle, nx, ny, nzg, steps, medium, fseed, src=None):
+    f = oracle.fill_fields(nx, ny, nzg, fseed)
+    ca, cb, da, db = oracle.cell_coeffs(nx, ny, nzg, *medium)
+    co = oracle.Coeffs(nx, ny, nzg, ca=ca, cb=cb, da=da, db=db)
+    oracle.run(nx, ny, nzg, f, co, steps, sources=[oracle.Source(*src)] if src else None)
+    return f
+
+
+def assemble(oracle, nx, ny, nzg, slabs):
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in slabs:
+        for c in range(6):
+            (k0, k1), a = s.owned(c)
+            out[c][k0:k1] = a
+    return out
+
+
+class DirectExchange:
+    """In-process stand-in for HaloExchange (same pack/unpack protocol)."""
+
+    def __init__(self, slabs):
+        self.slabs = slabs
+
+    def exchange(self):
+        for lo, hi in zip(self.slabs[:-1], self.slabs[1:]):
+            up = np.empty(lo.halo_bytes(1, False), np.uint8)
+            down = np.empty(hi.halo_bytes(0, False), np.uint8)
+            lo.halo_pack(1, up.ctypes.data)
+            hi.halo_pack(0, down.ctypes.data)
+            hi.halo_unpack(0, up.ctypes.data)
+            lo.halo_unpack(1, down.ctypes.data)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 5])
+def test_slab_oracle_matches_single_domain(oracle, nranks):
+    from oracle.slab_oracle import OracleSlab
+    nx, ny, nzg, steps = CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"]
+    tab = oracle.gauss_table(steps)
+    src = (2, 6, 5, 8, tab)
+    f0 = oracle.fill_fields(nx, ny, nzg, CASE["fseed"])
+    slabs = [OracleSlab(nx, ny, nzg, z0, n, medium=CASE["medium"], sources=[src])
+             for z0, n in partition(nzg, nranks)]
+    for s in slabs:
+        s.load_global(f0)
+    ex = DirectExchange(slabs)
+    for _ in range(steps):
+        ex.exchange()
+        for s in slabs:
+            s.run(1)
+    got = assemble(oracle, nx, ny, nzg, slabs)
+    want = reference_run(oracle, nx, ny, nzg, steps, CASE["medium"], CASE["fseed"], src)
+    for c in range(6):
+        assert bits_equal(got[c], want[c]), c
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, result_path):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import pyoracle as O
+    from oracle.slab_oracle import OracleSlab
+    from paper_1301_4539_b200.slabs import HaloExchange, partition
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, ny, nzg, steps = CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"]
+    z0, n = partition(nzg, world)[rank]
+    tab = O.gauss_table(steps)
+    slab = OracleSlab(nx, ny, nzg, z0, n, medium=CASE["medium"], sources=[(2, 6, 5, 8, tab)])
+    slab.load_global(O.fill_fields(nx, ny, nzg, CASE["fseed"]))
+    hx = HaloExchange(slab, rank, world, "cpu")
+    for _ in range(steps):
+        hx.exchange()
+        slab.run(1)
+    parts = [None] * world
+    dist.all_gather_object(parts, [(slab.owned(c)[0], slab.owned(c)[1].copy()) for c in range(6)])
+    if rank == 0:
+        out = O.zeros_state(nx, ny, nzg)
+        for p in parts:
+            for c, ((k0, k1), a) in enumerate(p):
+                out[c][k0:k1] = a
+        np.savez(result_path, *out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_halo_exchange_bit_exact(oracle, tmp_path, world):
+    """HaloExchange over torch.distributed (gloo, world_size 2/3, 127.0.0.1)."""
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_gloo_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    got = np.load(path)
+    want = reference_run(oracle, CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"], CASE["medium"],
+                         CASE["fseed"], (2, 6, 5, 8, oracle.gauss_table(CASE["steps"])))
+    for c in range(6):
+        assert bits_equal(got[f"arr_{c}"], want[c]), c
+
+
+class _DeviceExchange:
+    """Single-GPU stand-in for HaloExchange between CUDA slabs (stream-ordered
+    device copies between launches; no kernel waits on another)."""
+
+    def __init__(self, sims):
+        self.sims = sims
+        self.bufs = []
+        for lo, hi in zip(sims[:-1], sims[1:]):
+            self.bufs.append((torch.empty(lo.halo_bytes(1, False), dtype=torch.uint8, device="cuda"),
+                              torch.empty(hi.halo_bytes(0, False), dtype=torch.uint8, device="cuda")))
+
+    def exchange(self):
+        for (lo, hi), (up, down) in zip(zip(self.sims[:-1], self.sims[1:]), self.bufs):
+            lo.halo_pack(1, up.data_ptr())
+            hi.halo_pack(0, down.data_ptr())
+            hi.halo_unpack(0, up.data_ptr())
+            lo.halo_unpack(1, down.data_ptr())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks,medium,fseed,src", [(2, (7, 7), 8, True), (3, (4, -1), None, True),
+                                                     (4, (-1, -1), 5, False)])
+def test_gpu_slabs_bit_exact(yb, oracle, nranks, medium, fseed, src):
+    nx, ny, nzg, steps = 136, 40, 29, 11
+    tab = oracle.gauss_table(steps)
+    srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)] if src else []
+    sims = []
+    for z0, n in partition(nzg, nranks):
+        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, zchunk=4)
+        s.generate_medium(*medium)
+        for q in srcs:
+            s.add_source(*q)
+        if fseed is not None:
+            s.fill(fseed)
+        sims.append(s)
+    ex = _DeviceExchange(sims)
+    for _ in range(steps):
+        ex.exchange()
+        for s in sims:
+            s.run(1)
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in sims:
+        d = s.download()
+        at_top = s.z_offset + s.nz == nzg
+        for c in range(6):
+            node_z = c in (0, 1, 5)
+            n = s.nz + (1 if node_z and at_top else 0)
+            out[c][s.z_offset:s.z_offset + n] = d[c][:n]
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(*medium)
+        for q in srcs:
+            one.add_source(*q)
+        if fseed is not None:
+            one.fill(fseed)
+        one.run(steps)
+        want = one.download()
+    for c in range(6):
+        assert bits_equal(out[c], want[c]), c
+    for s in sims:
+        s.close()
