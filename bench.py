@@ -193,25 +193,60 @@ def main():
 
     import torch
     import paper_1301_4539_b200 as Y
+    from paper_1301_4539_b200.slabs import HaloExchange, partition
 
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
     variant = Y.VARIANT_FUSED if args.variant == "fused" else Y.VARIANT_NAIVE
 
-    sim = Y.Simulation(nx, ny, nz, device=local, variant=variant, zchunk=args.zchunk)
-    sim.generate_medium(es, ss)
+    # z-slab decomposition (§8(e)): config 4 is strong scaling (fixed grid),
+    # every other config weak scaling (each GPU keeps the config's depth).
+    strong = args.config == "c4"
+    nz_global = nzg if (strong or world == 1) else nzg * world
+    z0, nz = partition(nz_global, world)[rank]
+    cells, cells_total = nx * ny * nz, nx * ny * nz_global
+    at_top = z0 + nz == nz_global
+    config.update({"grid": [nx, ny, nz_global], "per_gpu_grid": [nx, ny, nz],
+                   "parallelism": f"zslab{world}" if world > 1 else "single",
+                   "l2": "working set > 126 MB L2 (no flush needed)" if cells * 28 > 126e6 else
+                         "working set fits L2; L2 not flushed (informational)"})
+    slab = dict(z_offset=z0, nz_global=nz_global) if world > 1 else {}
+
+    def make_sim():
+        s_ = Y.Simulation(nx, ny, nz, device=local, variant=variant, zchunk=args.zchunk, **slab)
+        s_.set_stream(stream.cuda_stream)  # torch events then time exactly our work
+        return s_
+
     table = None
     if has_src:
-        from paper_1301_4539_b200 import S  # noqa: F401
         t = np.arange(cfg_steps + args.steps + args.warmup + 16, dtype=np.float64)
         table = np.exp(-((t - 40.0) / 12.0) ** 2).astype(np.float32)
-        sim.add_source(Y.EZ, nx // 2, ny // 2, nz // 2, table)
+    src = (Y.EZ, nx // 2, ny // 2, nz_global // 2)
+
+    sim = make_sim()
+    sim.generate_medium(es, ss)
+    if table is not None:
+        sim.add_source(*src, table)
     if fs is not None:
         sim.fill(fs)
-    sim.run(args.warmup)
+    if dist:
+        dist.barrier()  # the first NCCL op involves every rank (communicator init)
+    exch = HaloExchange(sim, rank, world, f"cuda:{local}") if world > 1 else None
+
+    def advance(s_, n):
+        if exch is None:
+            s_.run(n, sync=False)
+        else:
+            for _ in range(n):
+                exch.exchange()
+                s_.run(1, sync=False)
+
+    advance(sim, args.warmup)
+    sim.synchronize()
     info0 = sim.info()
 
     sampler = ClockSampler(local)
@@ -221,7 +256,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     sim.set_kernel_timing(True)
-    ms = sim.run_timed(args.steps)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    advance(sim, args.steps)
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
     info1 = sim.info()
     sim.set_kernel_timing(False)
     clocks = sampler.stop()
@@ -233,7 +273,7 @@ def main():
         dist.barrier()
 
     launches = info1["kernel_launches"] - info0["kernel_launches"]
-    value = cells * world * args.steps / (ms * 1e-3) / 1e9
+    value = cells_total * args.steps / (ms * 1e-3) / 1e9
     bpc = info1["bytes_per_cell_update"]
     kern_ms = info1["main_kernel_ms"] / max(1, info1["main_kernel_timed"])
     peak, peak_src = load_peak()
@@ -242,56 +282,67 @@ def main():
                 "frac": achieved / peak, "traffic": load_traffic(args.config, args.variant),
                 "kernel": "k_fused (one E+H sweep)" if variant == 0 else "naive step (4 kernels)",
                 "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,
-                "peak_source": peak_src,
+                "peak_source": peak_src, "per_gpu": world > 1,
                 "step_ms_share_of_kernel": kern_ms / (ms / args.steps)}
     config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
-                   "grid": [info1["grid_x"], info1["grid_y"], info1["grid_z"]],
-                   "n_cell_arrays": info1["n_cell_arrays"]})
+                   "ctas": info1["grid_x"], "n_cell_arrays": info1["n_cell_arrays"]})
+    if exch is not None:
+        config["halo_bytes_per_step_per_gpu"] = exch.bytes_per_exchange
 
-    # e2e through the public API with host buffers: run_simulation semantics
-    # (upload state + coefficients, advance the config's step count, download).
+    # e2e through the public API with pinned host buffers (run_simulation
+    # semantics): per-cell coefficients + fields uploaded, the config's full
+    # step count (with halo exchanges), fields downloaded.
     e2e = None
     if not args.no_e2e:
-        pin = lambda shape: torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
-        host_f = [pin(Y.comp_extents(nx, ny, nz, c)[::-1]) for c in range(6)]
-        host_out = [pin(Y.comp_extents(nx, ny, nz, c)[::-1]) for c in range(6)]
+        def pin(shape):
+            return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+        shapes = [Y.comp_extents(nx, ny, nz, c)[::-1] for c in range(6)]
+        host_f = [pin(sh) for sh in shapes]
+        host_out = [pin(sh) for sh in shapes]
         if fs is not None:
-            Y.host_fields(nx, ny, nz, fs, out=host_f)
+            Y.host_fields_slab(nx, ny, nz_global, z0, nz, fs, out=host_f)
         else:
-            for a in host_f:
-                a[...] = 0.0
-        # per-cell coefficient arrays the caller supplies from host memory
+            for a_ in host_f:
+                a_[...] = 0.0
         cell_arrays = {}
         if es >= 0:
             want = (Y.CB,) if ss < 0 else (Y.CA, Y.CB, Y.DA, Y.DB)
-            med = Y.host_medium(nx, ny, nz, es, ss,
-                                out=[pin((nz, ny, nx)) if q in want else None for q in range(4)])
+            nzc = nz if at_top else nz + 1
+            med = Y.host_medium_slab(nx, ny, nz_global, z0, nzc, es, ss,
+                                     [pin((nzc, ny, nx)) if q in want else None for q in range(4)])
             cell_arrays = {q: med[q] for q in want}
         e_steps = cfg_steps
-        with Y.Simulation(nx, ny, nz, device=local, variant=variant, zchunk=args.zchunk) as s2:
-            if table is not None:
-                s2.add_source(Y.EZ, nx // 2, ny // 2, nz // 2, table)
-            if dist:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for q, a in cell_arrays.items():
-                s2.set_cell_coeffs(q, a)
-            s2.upload(host_f)
+        s2 = make_sim()
+        if table is not None:
+            s2.add_source(*src, table)
+        ex2 = HaloExchange(s2, rank, world, f"cuda:{local}") if world > 1 else None
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for q, a_ in cell_arrays.items():
+            s2.set_cell_coeffs(q, a_)
+        s2.upload(host_f)
+        if ex2 is None:
             s2.run(e_steps)
-            out = s2.download(out=host_out)
-            t1 = time.perf_counter()
-        dt = t1 - t0
+        else:
+            for _ in range(e_steps):
+                ex2.exchange()
+                s2.run(1, sync=False)
+        s2.download(out=host_out)
+        dt = time.perf_counter() - t0
+        s2.close()
         if dist:
             tt = torch.tensor([dt], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
-        h2d = sum(a.nbytes for a in host_f) + sum(a.nbytes for a in cell_arrays.values())
-        d2h = sum(a.nbytes for a in out)
-        e2e = {"value": cells * world * e_steps / dt / 1e9, "unit": UNIT,
+        h2d = sum(a_.nbytes for a_ in host_f) + sum(a_.nbytes for a_ in cell_arrays.values())
+        d2h = sum(a_.nbytes for a_ in host_out)
+        e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
-               "steps": e_steps, "wall_s": dt,
-               "path": "Simulation: set_cell_coeffs + upload (dense host) -> run(config steps) -> download"}
+               "steps": e_steps, "wall_s": dt, "per_gpu_bytes": True,
+               "path": "Simulation: set_cell_coeffs + upload (pinned host) -> run(config steps) -> "
+                       "download (pinned host)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -300,9 +351,9 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks}
+                "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": config, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         print(json.dumps(line), flush=True)
     sim.close()
     if dist:

@@ -117,6 +117,14 @@ int yb_generate_medium(yb_sim* sim, int64_t eps_seed, int64_t sigma_seed);
 int yb_host_medium(int nx, int ny, int nz, int64_t eps_seed, int64_t sigma_seed, float* ca,
                    float* cb, float* da, float* db);
 int yb_host_field(int nx, int ny, int nz, uint64_t seed, int comp, float* dense);
+/* The same for the z-slab [z_offset, z_offset+nplanes) of a grid with
+ * nz_global planes: `nplanes` dense planes of the component (clipped to its
+ * global extent) / `nplanes` cell planes of the medium. */
+int yb_host_field_slab(int nx, int ny, int nz_global, int z_offset, int nplanes, uint64_t seed,
+                       int comp, float* dense);
+int yb_host_medium_slab(int nx, int ny, int nz_global, int z_offset, int nplanes,
+                        int64_t eps_seed, int64_t sigma_seed, float* ca, float* cb, float* da,
+                        float* db);
 
 /* FieldSet readout/writeback (fields.hpp:21-67). Dense reference layout. */
 int yb_upload_field(yb_sim* sim, int comp, const float* dense);

@@ -38,6 +38,7 @@ ABI_SYMBOLS = (
     "yb_apply_ampere_range", "yb_apply_faraday_range", "yb_apply_pec_boundary",
     "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
     "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
+    "yb_host_field_slab", "yb_host_medium_slab",
 )
 
 
@@ -116,6 +117,8 @@ def lib():
         L.yb_host_medium.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
                                      _f32p, _f32p, _f32p, _f32p]
         L.yb_host_field.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _f32p]
+        L.yb_host_field_slab.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_int, _f32p]
+        L.yb_host_medium_slab.argtypes = [C.c_int] * 5 + [C.c_int64, C.c_int64] + [_f32p] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
         L.yb_halo_unpack.argtypes = [vp, C.c_int, vp]
@@ -316,6 +319,26 @@ def host_fields(nx, ny, nz, seed, out=None):
     out = out or [np.empty(comp_extents(nx, ny, nz, c)[::-1], np.float32) for c in range(6)]
     for c in range(6):
         _check(lib().yb_host_field(nx, ny, nz, seed, c, _fp(out[c])))
+    return out
+
+
+def host_fields_slab(nx, ny, nz_global, z_offset, nz_local, seed, out=None):
+    """Seeded fields of one z-slab (dense local layout: node-z components carry
+    nz_local+1 planes, the same planes a slab Simulation uploads)."""
+    res = []
+    for c in range(6):
+        e = comp_extents(nx, ny, nz_local, c)
+        a = np.empty(e[::-1], np.float32) if out is None else out[c]
+        _check(lib().yb_host_field_slab(nx, ny, nz_global, z_offset, e[2], seed, c, _fp(a)))
+        res.append(a)
+    return res
+
+
+def host_medium_slab(nx, ny, nz_global, z_offset, nplanes, eps_seed, sigma_seed, out):
+    """Seeded medium for cell planes [z_offset, z_offset+nplanes) into out=(ca, cb, da, db)
+    (None entries skipped)."""
+    _check(lib().yb_host_medium_slab(nx, ny, nz_global, z_offset, nplanes, eps_seed, sigma_seed,
+                                     *[None if a is None else _fp(a) for a in out]))
     return out
 
 

@@ -625,6 +625,47 @@ int yb_host_field(int nx, int ny, int nz, uint64_t seed, int comp, float* dense)
   return YB_OK;
 }
 
+int yb_host_field_slab(int nx, int ny, int nz_global, int z_offset, int nplanes, uint64_t seed,
+                       int comp, float* dense) {
+  if (nx < 1 || ny < 1 || nz_global < 1 || !dense || z_offset < 0 || nplanes < 0)
+    return fail(YB_INVALID_ARGUMENT, "bad argument");
+  if (int rc = check_comp(comp)) return rc;
+  Geo g{};
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = nz_global;
+  int e[3];
+  comp_ext(g, comp, e);
+  const long long pl = (long long)e[0] * e[1];
+  for (int k = 0; k < nplanes; ++k) {
+    const int kg = z_offset + k;
+    for (long long q = 0; q < pl; ++q)
+      dense[k * pl + q] = kg < e[2] ? yb_field_value(seed, comp, (uint64_t)(kg * pl + q)) : 0.0f;
+  }
+  return YB_OK;
+}
+
+int yb_host_medium_slab(int nx, int ny, int nz_global, int z_offset, int nplanes,
+                        int64_t eps_seed, int64_t sigma_seed, float* ca, float* cb, float* da,
+                        float* db) {
+  if (nx < 1 || ny < 1 || nz_global < 1 || z_offset < 0 || nplanes < 0)
+    return fail(YB_INVALID_ARGUMENT, "bad argument");
+  const float S = courant();
+  const long long pl = (long long)nx * ny;
+  for (int k = 0; k < nplanes; ++k) {
+    const long long kg = std::min(z_offset + k, nz_global - 1);
+    for (long long q = 0; q < pl; ++q) {
+      const yb_cell_coeffs c = yb_cell_coeffs_at(eps_seed, sigma_seed, (uint64_t)(kg * pl + q), S);
+      const long long o = k * pl + q;
+      if (ca) ca[o] = c.ca;
+      if (cb) cb[o] = c.cb;
+      if (da) da[o] = c.da;
+      if (db) db[o] = c.db;
+    }
+  }
+  return YB_OK;
+}
+
 int yb_upload_field(yb_sim* s, int comp, const float* dense) {
   if (!s || !dense) return fail(YB_INVALID_ARGUMENT, "null argument");
   if (int rc = check_comp(comp)) return rc;
