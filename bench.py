@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--variant", default="fused", choices=["fused", "naive"])
+    ap.add_argument("--variant", default="fused", choices=["fused", "naive", "tb2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--zchunk", type=int, default=0, help="fused: z planes per work item (0 = auto)")
@@ -200,8 +200,13 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
-    variant = Y.VARIANT_FUSED if args.variant == "fused" else Y.VARIANT_NAIVE
+    # a real (non-default) stream: the library's work and torch's events /
+    # NCCL ops all run on it, so the events bracket exactly our work
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    variant = {"fused": Y.VARIANT_FUSED, "naive": Y.VARIANT_NAIVE, "tb2": Y.VARIANT_TB2}[args.variant]
+    if world > 1 and variant != Y.VARIANT_FUSED:
+        raise SystemExit("z-slab multi-GPU runs use the one-step fused variant")
 
     # z-slab decomposition (§8(e)): config 4 is strong scaling (fixed grid),
     # every other config weak scaling (each GPU keeps the config's depth).
@@ -277,13 +282,15 @@ def main():
     bpc = info1["bytes_per_cell_update"]
     kern_ms = info1["main_kernel_ms"] / max(1, info1["main_kernel_timed"])
     peak, peak_src = load_peak()
-    achieved = bpc * cells / (kern_ms * 1e-3) / 1e9
+    steps_per_launch = 2 if variant == Y.VARIANT_TB2 else 1
+    achieved = bpc * cells * steps_per_launch / (kern_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.config, args.variant),
-                "kernel": "k_fused (one E+H sweep)" if variant == 0 else "naive step (4 kernels)",
+                "kernel": {0: "k_fused (one E+H sweep per step)", 1: "naive step (4 kernels)",
+                           2: "k_tb2 (two steps per sweep)"}[variant],
                 "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,
                 "peak_source": peak_src, "per_gpu": world > 1,
-                "step_ms_share_of_kernel": kern_ms / (ms / args.steps)}
+                "step_ms_share_of_kernel": kern_ms / (ms / args.steps * steps_per_launch)}
     config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
                    "ctas": info1["grid_x"], "n_cell_arrays": info1["n_cell_arrays"]})
     if exch is not None:

@@ -107,6 +107,9 @@ struct yb_sim {
   dim3 grid{1, 1, 1};
   int zchunk = 0;
   int ntx = 1, nty = 1, nitems = 1;
+  yb::TMaps tm2[2];  // two-step sweep maps (taller boxes)
+  int stages2 = 0, zchunk2 = 0, nitems2 = 1;
+  dim3 grid2{1, 1, 1};
   unsigned long long* sched = nullptr;  // device work counter of the fused kernel
   unsigned long long sched_base = 0;
   int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
@@ -162,13 +165,13 @@ yb::Fields fields_of(const yb_sim* s, int b) {
   return F;
 }
 
-int encode_map(CUtensorMap* m, const Geo& g, float* base) {
+int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   // z coordinate = local plane + 1: the allocation starts at ghost plane -1
   const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ + 1};
   const cuuint64_t strides[2] = {(cuuint64_t)g.PX * 4, (cuuint64_t)g.plane * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)yb::kBY, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   // YB_L2PROMO=0..3 (tuning knob): none / 64B / 128B / 256B L2 promotion
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
@@ -231,19 +234,59 @@ int prepare_fused(yb_sim* s) {
   const char* one = std::getenv("YB_CTAS_PER_ITEM");
   const int ctas = (one && one[0] == '1') ? s->nitems : std::min(s->nitems, s->num_sms);
   s->grid = dim3(ctas, 1, 1);
+  if (s->variant == YB_VARIANT_TB2) {
+    for (int b = 0; b < 2; ++b) {
+      int q = 0;
+      for (int c = 0; c < 6; ++c)
+        if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->buf[b][c], yb::kTB2BY)) return rc;
+      for (int a = 0; a < 4; ++a)
+        if (s->cell[a])
+          if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->cell[a],
+                                  a < 2 ? yb::kTB2RowsCA : yb::kTB2RowsDA))
+            return rc;
+    }
+    int S2 = 3;
+    if (const char* e = std::getenv("YB_STAGES2")) S2 = std::max(2, std::min(4, std::atoi(e)));
+    while (S2 > 2 && yb::tb2_smem_bytes(mask, S2) > avail) --S2;
+    s->stages2 = S2;
+    int zc2 = s->zchunk_req;
+    if (zc2 <= 0) {  // a two-step item re-streams ~3 planes at its z boundaries
+      const long long T = (long long)tx * ty;
+      double best = 1e300;
+      for (int Z = 1; Z <= s->g.nz; ++Z) {
+        const int len = (s->g.nz + Z - 1) / Z;
+        const int Zr = (s->g.nz + len - 1) / len;
+        const long long rounds = (T * Zr + s->num_sms - 1) / s->num_sms;
+        const double cost = (double)rounds * (len + (Zr > 1 ? 3.0 : 0.0)) * (1.0 + len / 400.0);
+        if (cost < best - 1e-9) {
+          best = cost;
+          zc2 = len;
+        }
+      }
+    }
+    zc2 = std::min(std::max(zc2, 1), s->g.nz);
+    s->zchunk2 = zc2;
+    s->nitems2 = tx * ty * ((s->g.nz + zc2 - 1) / zc2);
+    s->grid2 = dim3(std::min(s->nitems2, s->num_sms), 1, 1);
+  }
   s->tm_valid = true;
   return YB_OK;
 }
 
-yb::SrcArgs sources_at(const yb_sim* s, int64_t step) {
+// Active sources at `step` (and `step+1` when two steps run in one launch).
+yb::SrcArgs sources_at(const yb_sim* s, int64_t step, bool two = false) {
   yb::SrcArgs a{};
   for (const Src& q : s->sources) {
-    if (step < 0 || step >= (int64_t)q.table.size()) continue;
+    const int64_t n = (int64_t)q.table.size();
+    const bool a0 = step >= 0 && step < n, a1 = two && step + 1 >= 0 && step + 1 < n;
+    if (!a0 && !a1) continue;
     a.comp[a.n] = q.comp;
     a.i[a.n] = q.i;
     a.j[a.n] = q.j;
     a.k[a.n] = q.k - s->g.zoff;  // local plane (may be outside the slab)
-    a.val[a.n] = q.table[step];
+    a.val[a.n] = a0 ? q.table[step] : 0.0f;
+    a.val2[a.n] = a1 ? q.table[step + 1] : 0.0f;
+    a.act[a.n] = (a0 ? 1 : 0) | (a1 ? 2 : 0);
     ++a.n;
   }
   return a;
@@ -295,6 +338,47 @@ int step_fused(yb_sim* s) {
   }
   YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, s->grid, smem, s->stream));
   s->sched_base += (unsigned long long)s->nitems + s->grid.x;  // every CTA's last fetch fails
+  if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
+  s->launches += 1;
+  s->cur = nxt;
+  if (s->timers_used >= 4096) return collect_timers(s);
+  return YB_OK;
+}
+
+// Two Standard steps in one launch (temporal depth 2).
+int step_tb2(yb_sim* s) {
+  const int nxt = s->cur ^ 1;
+  yb::FusedArgs a{};
+  a.g = s->g;
+  a.nstages = s->stages2;
+  a.zchunk = s->zchunk2;
+  a.ntx = s->ntx;
+  a.nty = s->nty;
+  a.nitems = s->nitems2;
+  a.sched = s->sched;
+  a.sched_base = s->sched_base;
+  a.store_policy = 1;
+  a.co = coef_args(s);
+  for (int c = 0; c < 6; ++c) {
+    a.in[c] = s->buf[s->cur][c];
+    a.out[c] = s->buf[nxt][c];
+  }
+  a.src = sources_at(s, s->step_index, true);
+  const int mask = cell_mask(s);
+  const size_t smem = yb::tb2_smem_bytes(mask, s->stages2);
+  TimerPair* tp = nullptr;
+  if (s->timing) {
+    if (s->timers_used == s->timers.size()) {
+      TimerPair p;
+      YB_CU(cudaEventCreate(&p.a));
+      YB_CU(cudaEventCreate(&p.b));
+      s->timers.push_back(p);
+    }
+    tp = &s->timers[s->timers_used++];
+    YB_CU(cudaEventRecord(tp->a, s->stream));
+  }
+  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], mask, s->grid2, smem, s->stream));
+  s->sched_base += (unsigned long long)s->nitems2 + s->grid2.x;
   if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
   s->launches += 1;
   s->cur = nxt;
@@ -381,7 +465,8 @@ int yb_create(const yb_desc* d, yb_sim** out) {
     return fail(YB_INVALID_ARGUMENT, "GridSpec: cell counts must be positive");
   if (d->ny > 65000 || d->nz > 65000 || d->nx > (1 << 24))
     return fail(YB_INVALID_ARGUMENT, "grid too large for this build");
-  if (d->variant != YB_VARIANT_FUSED && d->variant != YB_VARIANT_NAIVE)
+  if (d->variant != YB_VARIANT_FUSED && d->variant != YB_VARIANT_NAIVE &&
+      d->variant != YB_VARIANT_TB2)
     return fail(YB_INVALID_ARGUMENT, "unknown variant %d", d->variant);
   if (d->nz_global > 0 && (d->z_offset < 0 || d->z_offset + d->nz > d->nz_global))
     return fail(YB_INVALID_ARGUMENT, "slab [%d,%d) outside the global grid of %d planes",
@@ -389,7 +474,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (d->nz_global <= 0 && d->z_offset != 0)
     return fail(YB_INVALID_ARGUMENT, "z_offset needs nz_global");
   if (d->nz_global > 0 && d->nz_global != d->nz && d->variant != YB_VARIANT_FUSED)
-    return fail(YB_INVALID_ARGUMENT, "z-slab mode needs the fused variant");
+    return fail(YB_INVALID_ARGUMENT, "z-slab mode needs the fused (one-step) variant");
   YB_CU(cudaSetDevice(d->device));
   yb_sim* s = new yb_sim;
   s->device = d->device;
@@ -445,7 +530,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (int rc = upload_axis(s)) return bail(rc);
   static bool limits_set = false;
   if (!limits_set) {
-    if (yb::fused_set_smem_limits() != cudaSuccess)
+    if (yb::fused_set_smem_limits() != cudaSuccess || yb::tb2_set_smem_limits() != cudaSuccess)
       return bail(fail(YB_CUDA_ERROR, "cudaFuncSetAttribute failed"));
     limits_set = true;
   }
@@ -740,10 +825,17 @@ int yb_advance(yb_sim* s, int64_t nsteps) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
   YB_CU(cudaSetDevice(s->device));
-  if (s->variant == YB_VARIANT_FUSED)
+  if (s->variant != YB_VARIANT_NAIVE)
     if (int rc = prepare_fused(s)) return rc;
-  for (int64_t t = 0; t < nsteps; ++t) {
-    const int rc = s->variant == YB_VARIANT_FUSED ? step_fused(s) : step_naive(s);
+  int64_t t = 0;
+  if (s->variant == YB_VARIANT_TB2)
+    for (; t + 2 <= nsteps; t += 2) {
+      if (int rc = step_tb2(s)) return rc;
+      s->step_index += 2;
+      s->steps += 2;
+    }
+  for (; t < nsteps; ++t) {
+    const int rc = s->variant == YB_VARIANT_NAIVE ? step_naive(s) : step_fused(s);
     if (rc) return rc;
     ++s->step_index;
     ++s->steps;
@@ -761,7 +853,7 @@ int yb_synchronize(yb_sim* s) {
 int yb_advance_timed(yb_sim* s, int64_t nsteps, float* ms) {
   if (!s || !ms) return fail(YB_INVALID_ARGUMENT, "null argument");
   YB_CU(cudaSetDevice(s->device));
-  if (s->variant == YB_VARIANT_FUSED)
+  if (s->variant != YB_VARIANT_NAIVE)
     if (int rc = prepare_fused(s)) return rc;
   cudaEvent_t a, b;
   YB_CU(cudaEventCreate(&a));
@@ -914,7 +1006,7 @@ int yb_get_info(yb_sim* s, yb_info* info) {
   if (!s || !info) return fail(YB_INVALID_ARGUMENT, "null argument");
   YB_CU(cudaSetDevice(s->device));
   if (int rc = collect_timers(s)) return rc;
-  if (s->variant == YB_VARIANT_FUSED)
+  if (s->variant != YB_VARIANT_NAIVE)
     if (int rc = prepare_fused(s)) return rc;
   std::memset(info, 0, sizeof *info);
   info->step_index = s->step_index;
@@ -929,7 +1021,13 @@ int yb_get_info(yb_sim* s, yb_info* info) {
   info->grid_y = (int)s->grid.y;
   info->grid_z = (int)s->grid.z;
   info->zchunk = s->zchunk;
-  info->bytes_per_cell_update = 48.0 + 4.0 * info->n_cell_arrays;
+  info->bytes_per_cell_update = (48.0 + 4.0 * info->n_cell_arrays) /
+                                (s->variant == YB_VARIANT_TB2 ? 2.0 : 1.0);
+  if (s->variant == YB_VARIANT_TB2) {
+    info->stages = s->stages2;
+    info->grid_x = (int)s->grid2.x;
+    info->zchunk = s->zchunk2;
+  }
   info->device_bytes = s->dev_bytes;
   return YB_OK;
 }

@@ -33,7 +33,9 @@ __host__ __device__ __forceinline__ bool at_top(const Geo& g) { return g.zoff + 
 struct SrcArgs {
   int n;
   int comp[kMaxSources], i[kMaxSources], j[kMaxSources], k[kMaxSources];
-  float val[kMaxSources];
+  float val[kMaxSources];   // increment at step n (the launch's first step)
+  float val2[kMaxSources];  // increment at step n+1 (two-step sweeps)
+  int act[kMaxSources];     // bit 0: active at step n, bit 1: active at step n+1
 };
 
 // Coefficients as seen by a kernel: per-cell arrays (nullptr if not cell

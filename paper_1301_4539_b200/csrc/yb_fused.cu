@@ -28,87 +28,10 @@
 #include <cuda_runtime.h>
 
 #include "yb_launch.h"
+#include "yb_ptx.cuh"
 
 namespace yb {
 namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "YB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra YB_WAIT;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y,
-                                            int z, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
-__device__ __forceinline__ void sts4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-
-__device__ __forceinline__ float& el(float4& v, int q) {
-  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
-}
-__device__ __forceinline__ float elc(const float4& v, int q) {
-  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
-}
-
-// value at i-1 for each element of a lane's float4 (lane 0 reads `left`).
-__device__ __forceinline__ float4 shift_im(float4 v, int lane, float left) {
-  float w = __shfl_up_sync(0xffffffffu, v.w, 1);
-  if (lane == 0) w = left;
-  return make_float4(w, v.x, v.y, v.z);
-}
-// value at i+1 for each element (lane 31 reads `right`).
-__device__ __forceinline__ float4 shift_ip(float4 v, int lane, float right) {
-  float x = __shfl_down_sync(0xffffffffu, v.x, 1);
-  if (lane == 31) x = right;
-  return make_float4(v.y, v.z, v.w, x);
-}
-
-// 128-bit store with an L2 cache-policy hint (evict_first: the next-state
-// arrays are not read again in this launch, so they should not push the
-// halo rows neighbouring CTAs are about to read out of L2).
-__device__ __forceinline__ void stg4_hint(float* ptr, float4 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
-}
-
-__device__ __forceinline__ void store_row4(float* base, long long p, int i0, int nx, float4 v,
-                                           uint64_t pol) {
-  if (i0 + 3 < nx) {
-    stg4_hint(base + p, v, pol);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + q < nx) base[p + q] = elc(v, q);
-  }
-}
 
 template <bool CAC, bool CBC, bool DAC, bool DBC>
 __global__ void __launch_bounds__(kThreads, 1)

@@ -19,6 +19,37 @@ constexpr int kBY = kTY + 2;        // staged box: y0-1 .. y0+TY
 constexpr int kSlot = ((kBX * kBY * 4 + 127) / 128) * 32;  // floats per array slot (128-B aligned)
 constexpr int kMaxArrays = 10;      // 6 fields + up to 4 per-cell coefficient arrays
 
+// Two-step (temporal depth 2) sweep geometry (yb_tb2.cu): 8 output rows,
+// staged rows y0-2..y0+9, row warps for rows y0-1..y0+9, one edge-column
+// warp, one TMA producer warp, one face warp.
+constexpr int kTB2Rows = 8;
+constexpr int kTB2BY = kTB2Rows + 4;                  // staged box rows
+constexpr int kTB2RowWarps = kTB2Rows + 3;            // E1 rows
+constexpr int kTB2Warps = kTB2RowWarps + 3;           // + edge, producer, face
+constexpr int kTB2Threads = 32 * kTB2Warps;
+// Staged rows per array: fields y0-2..y0+9 (12), Ca/Cb y0-1..y0+9 (11),
+// Da/Db y0-1..y0+8 (10) — each array only as tall as its consumers need.
+constexpr int kTB2RowsCA = kTB2Rows + 3;
+constexpr int kTB2RowsDA = kTB2Rows + 2;
+constexpr int slot_floats(int rows) { return ((kBX * rows * 4 + 127) / 128) * 32; }
+constexpr int kTB2SlotF = slot_floats(kTB2BY);
+constexpr int kTB2SlotC = slot_floats(kTB2RowsCA);
+constexpr int kTB2SlotD = slot_floats(kTB2RowsDA);
+constexpr int kTB2E1 = 2 * 3 * kTB2RowWarps * kBX;    // E^{n+1} planes (double buffered)
+constexpr int kTB2H1 = 2 * 3 * (kTB2Rows + 2) * kBX;  // H^{n+3/2} planes (double buffered)
+constexpr int kTB2E2 = 2 * 3 * (kTB2Rows + 1) * kBX;  // E^{n+2} planes (double buffered)
+
+// floats of one stage for a coefficient set (mask bit q: array q per-cell)
+inline int tb2_stage_floats(int cell_mask) {
+  return 6 * kTB2SlotF + ((cell_mask & 1) + ((cell_mask >> 1) & 1)) * kTB2SlotC +
+         (((cell_mask >> 2) & 1) + ((cell_mask >> 3) & 1)) * kTB2SlotD;
+}
+
+inline size_t tb2_smem_bytes(int cell_mask, int stages) {
+  return (size_t)stages * tb2_stage_floats(cell_mask) * 4 + (size_t)(kTB2E1 + kTB2H1 + kTB2E2) * 4 +
+         (size_t)stages * 16 + 8 * 4;
+}
+
 struct TMaps {
   CUtensorMap m[kMaxArrays];  // read side: ex..hz of the current state, then cell coeffs
 };
@@ -47,6 +78,10 @@ inline size_t fused_smem_bytes(int narr, int stages) {
 cudaError_t launch_fused(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid,
                          size_t smem, cudaStream_t st);
 cudaError_t fused_set_smem_limits();
+// Two full steps per launch (maps with kTB2BY-row boxes).
+cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid, size_t smem,
+                       cudaStream_t st);
+cudaError_t tb2_set_smem_limits();
 
 cudaError_t launch_naive_ampere(const Geo& g, const Fields& F, const CoefArgs& co, const int* box,
                                 cudaStream_t st);

@@ -1,0 +1,619 @@
+// yb_tb2.cu — temporal blocking of depth 2: TWO full Standard steps per
+// sweep (four fused half-steps E1, H1, E2, H2), the GPU analogue of the
+// paper's two-step cache-reuse scheme — here the reuse is
+// in shared memory instead of a CPU cache, and it halves the HBM bytes per
+// cell-update: the state and the per-cell coefficients are read once and the
+// state written once per two steps.
+//
+// Work item = 8 output rows x 128 columns x a z-chunk. The producer warp
+// streams the box x0-4..x0+131, y0-2..y0+9 of each read array per plane
+// (TMA, mbarrier ring). Per plane p the CTA runs a four-level wavefront:
+//   L1  E^{n+1}(p)    rows y0-1..y0+9, cols x0-1..x0+129   -> smem (2 planes)
+//   L2  H^{n+3/2}(p-1) rows y0-1..y0+8, cols x0-1..x0+128  -> smem
+//   L3  E^{n+2}(p-1)  rows y0..y0+8,   cols x0..x0+128     -> smem (2 planes), rows y0..y0+7 -> HBM
+//   L4  H^{n+5/2}(p-2) rows y0..y0+7,   cols x0..x0+127     -> HBM
+// (update_e_dof / update_h_dof, kernels.hpp:27-63, PEC folded in, sources at
+// steps n and n+1 added after their E level, schedule.hpp:175-199).
+// Row warp w owns physical row y0-1+w at every level, so its own-row values
+// of earlier planes/levels stay in registers; the x0-1 / x0+128 / x0+129
+// columns are computed by a dedicated edge warp (lane = row). Two CTA
+// barriers per plane. Chunk boundaries re-stream two planes below and one
+// above (the wavefront's z-halo). Arithmetic: yee_upd, bit-identical to two
+// single steps.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "yb_launch.h"
+#include "yb_ptx.cuh"
+
+namespace yb {
+namespace {
+
+constexpr int RW = kTB2RowWarps;     // 11 row warps: rows y0-1 .. y0+9
+constexpr int EDGE = RW;             // warp 11
+constexpr int PROD = RW + 1;         // warp 12
+constexpr int FACE = RW + 2;         // warp 13
+constexpr int BX = kBX;              // 136 smem columns: x = x0-4+c
+constexpr int CL = 3, CR = 4 + kTX;  // edge columns x0-1, x0+128 (and CR+1)
+
+constexpr int kConsumers = 32 * (RW + 1);  // row warps + edge warp
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+// true if any source sits on (global-local) plane kl and row j at step bit sb
+__device__ __forceinline__ bool src_row(const SrcArgs& s, int sb, int j, int kl) {
+  bool hit = false;
+  for (int q = 0; q < s.n; ++q) hit |= (s.act[q] & sb) && s.j[q] == j && s.k[q] == kl;
+  return hit;
+}
+
+struct F4x3 {
+  float4 x, y, z;
+};
+
+// E update of one float4 group (4 consecutive i) — the same expression as
+// the single-step kernel (reference operand order, PEC as a mask).
+template <bool CAC, bool CBC>
+__device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int i0, int j, int kg,
+                                          float cdy, float cdz, float4 cdx, float4 ca, float4 cb,
+                                          float4 ex, float4 ey, float4 ez, float4 hx, float4 hy,
+                                          float4 hz, float4 hx_jm, float4 hz_jm, float4 hy_im,
+                                          float4 hz_im, float4 hx_km, float4 hy_km) {
+  const bool kin = kg >= 1 && kg < g.nzg;
+  const bool jin = j >= 1 && j < g.ny, jlt = j >= 0 && j < g.ny;
+  F4x3 o;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + q;
+    const bool iin = i >= 1 && i < g.nx, ilt = i >= 0 && i < g.nx;
+    const float A = CAC ? elc(ca, q) : co.ca_s;
+    const float B = elc(cb, q);
+    el(o.x, q) = (ilt && jin && kin) ? yee_upd(A, elc(ex, q), CBC ? B : cdy, elc(hz, q), elc(hz_jm, q),
+                                               CBC ? B : cdz, elc(hy, q), elc(hy_km, q))
+                                     : 0.f;
+    el(o.y, q) = (iin && jlt && kin) ? yee_upd(A, elc(ey, q), CBC ? B : cdz, elc(hx, q), elc(hx_km, q),
+                                               CBC ? B : elc(cdx, q), elc(hz, q), elc(hz_im, q))
+                                     : 0.f;
+    el(o.z, q) = (iin && jin && kg >= 0 && kg < g.nzg)
+                     ? yee_upd(A, elc(ez, q), CBC ? B : elc(cdx, q), elc(hy, q), elc(hy_im, q),
+                               CBC ? B : cdy, elc(hx, q), elc(hx_jm, q))
+                     : 0.f;
+  }
+  return o;
+}
+
+// Scalar E update at (i, j, kg).
+template <bool CAC, bool CBC>
+__device__ __forceinline__ void e_update1(const CoefArgs& co, const Geo& g, int i, int j, int kg,
+                                          float cdy, float cdz, float cdx, float ca, float cb,
+                                          float ex, float ey, float ez, float hx, float hy, float hz,
+                                          float hx_jm, float hz_jm, float hy_im, float hz_im,
+                                          float hx_km, float hy_km, float& ox, float& oy, float& oz) {
+  const bool kin = kg >= 1 && kg < g.nzg;
+  const bool jin = j >= 1 && j < g.ny, jlt = j >= 0 && j < g.ny;
+  const bool iin = i >= 1 && i < g.nx, ilt = i >= 0 && i < g.nx;
+  const float A = CAC ? ca : co.ca_s;
+  ox = (ilt && jin && kin) ? yee_upd(A, ex, CBC ? cb : cdy, hz, hz_jm, CBC ? cb : cdz, hy, hy_km) : 0.f;
+  oy = (iin && jlt && kin) ? yee_upd(A, ey, CBC ? cb : cdz, hx, hx_km, CBC ? cb : cdx, hz, hz_im) : 0.f;
+  oz = (iin && jin && kg >= 0 && kg < g.nzg) ? yee_upd(A, ez, CBC ? cb : cdx, hy, hy_im, CBC ? cb : cdy, hx, hx_jm)
+                                             : 0.f;
+}
+
+// Source increments for one E level at global plane kg (step bit `sb`).
+__device__ __forceinline__ float src_add(const SrcArgs& s, int sb, int comp, int i, int j, int kl) {
+  float v = 0.f;
+  bool hit = false;
+  for (int q = 0; q < s.n; ++q)
+    if ((s.act[q] & sb) && s.comp[q] == comp && s.i[q] == i && s.j[q] == j && s.k[q] == kl) {
+      v = sb == 1 ? s.val[q] : s.val2[q];
+      hit = true;
+    }
+  return hit ? v : -0.0f;  // -0 is the additive identity (x + -0 == x for every x)
+}
+
+// Per-item geometry shared by the consumer paths.
+struct Item {
+  int x0, y0, kz0, kz1, pstart, pin_end, pend;
+};
+
+// Stage layout: fields (12 rows from y0-2), then Ca, Cb (11 rows from y0-1),
+// then Da, Db (10 rows from y0-1), each present only in per-cell mode.
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+struct StageLayout {
+  static constexpr int floats =
+      6 * kTB2SlotF + (CAC + CBC) * kTB2SlotC + (DAC + DBC) * kTB2SlotD;
+  static constexpr int off_ca = 6 * kTB2SlotF;
+  static constexpr int off_cb = off_ca + CAC * kTB2SlotC;
+  static constexpr int off_da = off_cb + CBC * kTB2SlotC;
+  static constexpr int off_db = off_da + DAC * kTB2SlotD;
+};
+
+struct Bufs {
+  float *stages, *e1b, *h1b, *e2b;
+  uint64_t *full, *empty;
+  __device__ float* E1(int b, int comp, int r, int col) const {
+    return e1b + ((size_t)(b * 3 + comp) * RW + r) * BX + col;
+  }
+  __device__ float* H1(int b, int comp, int r, int col) const {
+    return h1b + ((size_t)(b * 3 + comp) * (RW - 1) + r) * BX + col;
+  }
+  __device__ float* E2(int b, int comp, int r, int col) const {
+    return e2b + ((size_t)(b * 3 + comp) * (RW - 2) + r) * BX + col;
+  }
+};
+
+struct Cursor {
+  int cs;
+  bool peeked;
+  __device__ int wait(const Bufs& B, int S) {
+    const int s = cs % S;
+    if (!peeked) mbar_wait(smem_u32(&B.full[s]), (uint32_t)((cs / S) & 1));
+    peeked = false;
+    ++cs;
+    return s;
+  }
+};
+
+// ============================================================== row warps
+// Warp er owns row j = y0-1+er at every level. Carried across planes in
+// registers: H0(p-1), Ca/Cb(p-1), Da/Db(p-1), Da/Db(p-2) of its own row;
+// E1(p-1) and H1(p-2) of its own row are re-read from shared memory.
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+__device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
+                                         int er, int l, uint64_t st_pol) {
+  using L = StageLayout<CAC, CBC, DAC, DBC>;
+  const Geo& g = a.g;
+  const CoefArgs& co = a.co;
+  const int S = a.nstages;
+  const int j = it.y0 - 1 + er;
+  const int rs = er + 1;  // field stage row
+  const int c = 4 + 4 * l;
+  const int i0 = it.x0 + 4 * l;
+  const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
+  const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  F4x3 h0p = {z4, z4, z4};
+  float4 cap = z4, cbp = z4, dap = z4, dbp = z4, dap2 = z4, dbp2 = z4;
+
+  if (it.kz0 >= 2) {  // prologue: hx, hy of plane kz0-2
+    const int s = cur.wait(B, S);
+    const float* F = B.stages + (size_t)s * L::floats;
+    h0p.x = lds4(F + 3 * kTB2SlotF + rs * BX + c);
+    h0p.y = lds4(F + 4 * kTB2SlotF + rs * BX + c);
+    consumer_sync();
+    if (er == 0 && l == 0) mbar_arrive(smem_u32(&B.empty[s]));
+  }
+
+  for (int p = it.pstart; p <= it.pend; ++p) {
+    // ------------------------------------------------------- L1: E1(p)
+    const bool l1 = p <= it.pin_end;
+    F4x3 e1c = {z4, z4, z4}, h0n = {z4, z4, z4};
+    float4 can = z4, cbn = z4, dan = z4, dbn = z4;
+    int s1 = -1;
+    if (l1) {
+      s1 = cur.wait(B, S);
+      const float* F = B.stages + (size_t)s1 * L::floats;
+      const float cdz_e = co.cdz_e[p];
+      h0n.x = lds4(F + 3 * kTB2SlotF + rs * BX + c);
+      h0n.y = lds4(F + 4 * kTB2SlotF + rs * BX + c);
+      h0n.z = lds4(F + 5 * kTB2SlotF + rs * BX + c);
+      const float4 hy_im = shift_im(h0n.y, l, F[4 * kTB2SlotF + rs * BX + c - 1]);
+      const float4 hz_im = shift_im(h0n.z, l, F[5 * kTB2SlotF + rs * BX + c - 1]);
+      if (CAC) can = lds4(F + L::off_ca + er * BX + c);
+      if (CBC) cbn = lds4(F + L::off_cb + er * BX + c);
+      if (DAC && er <= RW - 2) dan = lds4(F + L::off_da + er * BX + c);
+      if (DBC && er <= RW - 2) dbn = lds4(F + L::off_db + er * BX + c);
+      e1c = e_update4<CAC, CBC>(co, g, i0, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn,
+                                lds4(F + 0 * kTB2SlotF + rs * BX + c), lds4(F + 1 * kTB2SlotF + rs * BX + c),
+                                lds4(F + 2 * kTB2SlotF + rs * BX + c), h0n.x, h0n.y, h0n.z,
+                                lds4(F + 3 * kTB2SlotF + (rs - 1) * BX + c),
+                                lds4(F + 5 * kTB2SlotF + (rs - 1) * BX + c), hy_im, hz_im, h0p.x, h0p.y);
+      if (src_row(a.src, 1, j, p)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          el(e1c.x, q) = __fadd_rn(el(e1c.x, q), src_add(a.src, 1, 0, i0 + q, j, p));
+          el(e1c.y, q) = __fadd_rn(el(e1c.y, q), src_add(a.src, 1, 1, i0 + q, j, p));
+          el(e1c.z, q) = __fadd_rn(el(e1c.z, q), src_add(a.src, 1, 2, i0 + q, j, p));
+        }
+      }
+      sts4(B.E1(p & 1, 0, er, c), e1c.x);
+      sts4(B.E1(p & 1, 1, er, c), e1c.y);
+      sts4(B.E1(p & 1, 2, er, c), e1c.z);
+    }
+    consumer_sync();  // (A) E1(p) complete, stage free
+    if (l1 && er == 0 && l == 0) mbar_arrive(smem_u32(&B.empty[s1]));
+
+    // ----------------------------------------------------- L2: H1(p-1)
+    const int kh = p - 1;
+    if (kh >= it.pstart && kh <= min(it.kz1, g.nz - 1) && er <= RW - 2) {
+      const int pb = kh & 1;
+      const float cdz_h = co.cdz_h[kh];
+      const float4 ex_h = lds4(B.E1(pb, 0, er, c)), ex_jp = lds4(B.E1(pb, 0, er + 1, c));
+      const float4 ey_h = lds4(B.E1(pb, 1, er, c));
+      const float4 ez_h = lds4(B.E1(pb, 2, er, c)), ez_jp = lds4(B.E1(pb, 2, er + 1, c));
+      const float4 ey_ip = shift_ip(ey_h, l, *B.E1(pb, 1, er, CR));
+      const float4 ez_ip = shift_ip(ez_h, l, *B.E1(pb, 2, er, CR));
+      F4x3 h1c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float A = DAC ? elc(dap, q) : co.da_s;
+        const float Bq = elc(dbp, q);
+        el(h1c.x, q) = yee_upd(A, elc(h0p.x, q), DBC ? Bq : cdz_h, elc(e1c.y, q), elc(ey_h, q),
+                               DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
+        el(h1c.y, q) = yee_upd(A, elc(h0p.y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
+                               DBC ? Bq : cdz_h, elc(e1c.x, q), elc(ex_h, q));
+        el(h1c.z, q) = yee_upd(A, elc(h0p.z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
+                               DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
+      }
+      sts4(B.H1(pb, 0, er, c), h1c.x);
+      sts4(B.H1(pb, 1, er, c), h1c.y);
+      sts4(B.H1(pb, 2, er, c), h1c.z);
+    }
+    consumer_sync();  // (B) H1(p-1) complete
+
+    // ----------------------------------------------------- L3: E2(p-1)
+    F4x3 e2c = {z4, z4, z4};
+    if (kh >= it.kz0 && kh <= min(it.kz1, g.nz - 1) && er >= 1 && er <= RW - 2) {
+      const int hb = kh & 1;
+      const float cdz_e = co.cdz_e[kh];
+      const float4 hx = lds4(B.H1(hb, 0, er, c)), hy = lds4(B.H1(hb, 1, er, c));
+      const float4 hz = lds4(B.H1(hb, 2, er, c));
+      const float4 hy_im = shift_im(hy, l, *B.H1(hb, 1, er, CL));
+      const float4 hz_im = shift_im(hz, l, *B.H1(hb, 2, er, CL));
+      e2c = e_update4<CAC, CBC>(co, g, i0, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
+                                lds4(B.E1(hb, 0, er, c)), lds4(B.E1(hb, 1, er, c)), lds4(B.E1(hb, 2, er, c)),
+                                hx, hy, hz, lds4(B.H1(hb, 0, er - 1, c)), lds4(B.H1(hb, 2, er - 1, c)), hy_im,
+                                hz_im, lds4(B.H1(hb ^ 1, 0, er, c)), lds4(B.H1(hb ^ 1, 1, er, c)));
+      if (src_row(a.src, 2, j, kh)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          el(e2c.x, q) = __fadd_rn(el(e2c.x, q), src_add(a.src, 2, 0, i0 + q, j, kh));
+          el(e2c.y, q) = __fadd_rn(el(e2c.y, q), src_add(a.src, 2, 1, i0 + q, j, kh));
+          el(e2c.z, q) = __fadd_rn(el(e2c.z, q), src_add(a.src, 2, 2, i0 + q, j, kh));
+        }
+      }
+      sts4(B.E2(hb, 0, er - 1, c), e2c.x);
+      sts4(B.E2(hb, 1, er - 1, c), e2c.y);
+      sts4(B.E2(hb, 2, er - 1, c), e2c.z);
+      if (er <= kTB2Rows && j < g.ny && kh < it.kz1) {  // E^{n+2} of the owned rows -> HBM
+        const long long gp = gidx(g, i0, j, kh);
+        store_row4(a.out[0], gp, i0, g.nx, e2c.x, st_pol);
+        store_row4(a.out[1], gp, i0, g.nx, e2c.y, st_pol);
+        store_row4(a.out[2], gp, i0, g.nx, e2c.z, st_pol);
+      }
+    }
+
+    // ----------------------------------------------------- L4: H2(p-2)
+    const int k4 = p - 2;
+    if (k4 >= it.kz0 && k4 <= it.kz1 - 1 && er >= 1 && er <= kTB2Rows) {
+      const int pb = k4 & 1;
+      const float cdz_h = co.cdz_h[k4];
+      const float4 ex_h = lds4(B.E2(pb, 0, er - 1, c)), ex_jp = lds4(B.E2(pb, 0, er, c));
+      const float4 ey_h = lds4(B.E2(pb, 1, er - 1, c));
+      const float4 ez_h = lds4(B.E2(pb, 2, er - 1, c)), ez_jp = lds4(B.E2(pb, 2, er, c));
+      const float4 ey_ip = shift_ip(ey_h, l, *B.E2(pb, 1, er - 1, CR));
+      const float4 ez_ip = shift_ip(ez_h, l, *B.E2(pb, 2, er - 1, CR));
+      const float4 h1x = lds4(B.H1(pb, 0, er, c)), h1y = lds4(B.H1(pb, 1, er, c));
+      const float4 h1z = lds4(B.H1(pb, 2, er, c));
+      F4x3 h2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float A = DAC ? elc(dap2, q) : co.da_s;
+        const float Bq = elc(dbp2, q);
+        el(h2.x, q) = yee_upd(A, elc(h1x, q), DBC ? Bq : cdz_h, elc(e2c.y, q), elc(ey_h, q),
+                              DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
+        el(h2.y, q) = yee_upd(A, elc(h1y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
+                              DBC ? Bq : cdz_h, elc(e2c.x, q), elc(ex_h, q));
+        el(h2.z, q) = yee_upd(A, elc(h1z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
+                              DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
+      }
+      if (j < g.ny) {
+        const long long gp = gidx(g, i0, j, k4);
+        store_row4(a.out[3], gp, i0, g.nx, h2.x, st_pol);
+        store_row4(a.out[4], gp, i0, g.nx, h2.y, st_pol);
+        store_row4(a.out[5], gp, i0, g.nx, h2.z, st_pol);
+      }
+    }
+    // ---------------------------------------------------------- rotate
+    dap2 = dap;
+    dbp2 = dbp;
+    if (l1) {
+      h0p = h0n;
+      cap = can;
+      cbp = cbn;
+      dap = dan;
+      dbp = dbn;
+    }
+  }
+}
+
+// ============================================================= edge warp
+// Lane r owns row j = y0-1+r (r < RW) at the edge columns x0-1 (CL),
+// x0+128 (CR) and x0+129 (CR+1): E1 at all three, H1 at CL and CR, E2 at CR.
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+__device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
+                                         int l) {
+  using L = StageLayout<CAC, CBC, DAC, DBC>;
+  const Geo& g = a.g;
+  const CoefArgs& co = a.co;
+  const int S = a.nstages;
+  const bool act = l < RW;
+  const int er = act ? l : 0;
+  const int j = it.y0 - 1 + er;
+  const int rs = er + 1;
+  const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
+  const int ie[3] = {it.x0 - 1, it.x0 + kTX, it.x0 + kTX + 1};
+  const int ce[3] = {CL, CR, CR + 1};
+  float h0[3][3] = {};   // H0(p-1) [col][comp]
+  float dap[2] = {}, dbp[2] = {};  // Da/Db(p-1) at CL, CR
+  float cap = 0.f, cbp = 0.f;      // Ca/Cb(p-1) at CR
+
+  if (it.kz0 >= 2) {
+    const int s = cur.wait(B, S);
+    const float* F = B.stages + (size_t)s * L::floats;
+    if (act) {
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        h0[e][0] = F[3 * kTB2SlotF + rs * BX + ce[e]];
+        h0[e][1] = F[4 * kTB2SlotF + rs * BX + ce[e]];
+      }
+    }
+    consumer_sync();
+  }
+
+  for (int p = it.pstart; p <= it.pend; ++p) {
+    const bool l1 = p <= it.pin_end;
+    float e1[3][3] = {}, h0n[3][3] = {};
+    float dan[2] = {}, dbn[2] = {}, can = 0.f, cbn = 0.f;
+    if (l1) {
+      const int s1 = cur.wait(B, S);
+      const float* F = B.stages + (size_t)s1 * L::floats;
+      const float cdz_e = co.cdz_e[p];
+      if (act) {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          const int col = ce[e], i = ie[e];
+          const float* Fr = F + rs * BX + col;
+          h0n[e][0] = Fr[3 * kTB2SlotF];
+          h0n[e][1] = Fr[4 * kTB2SlotF];
+          h0n[e][2] = Fr[5 * kTB2SlotF];
+          const float ca = CAC ? F[L::off_ca + er * BX + col] : 0.f;
+          const float cb = CBC ? F[L::off_cb + er * BX + col] : 0.f;
+          e_update1<CAC, CBC>(co, g, i, j, p + g.zoff, cdy_e, cdz_e, co.cdx_e[max(i, 0)], ca, cb,
+                              Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], h0n[e][0], h0n[e][1], h0n[e][2],
+                              Fr[3 * kTB2SlotF - BX], Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1],
+                              Fr[5 * kTB2SlotF - 1], h0[e][0], h0[e][1], e1[e][0], e1[e][1], e1[e][2]);
+          if (src_row(a.src, 1, j, p)) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) e1[e][q] = __fadd_rn(e1[e][q], src_add(a.src, 1, q, i, j, p));
+          }
+#pragma unroll
+          for (int q = 0; q < 3; ++q) *B.E1(p & 1, q, er, col) = e1[e][q];
+          if (e < 2 && er <= RW - 2) {
+            if (DAC) dan[e] = F[L::off_da + er * BX + col];
+            if (DBC) dbn[e] = F[L::off_db + er * BX + col];
+          }
+          if (e == 1) {
+            can = ca;
+            cbn = cb;
+          }
+        }
+      }
+    }
+    consumer_sync();  // (A)
+
+    const int kh = p - 1;
+    if (act && kh >= it.pstart && kh <= min(it.kz1, g.nz - 1) && er <= RW - 2) {
+      const int pb = kh & 1;
+      const float cdz_h = co.cdz_h[kh];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {  // CL, CR
+        const int col = ce[e], i = ie[e];
+        const float A = DAC ? dap[e] : co.da_s;
+        const float Bq = dbp[e];
+        const float cdx = co.cdx_h[max(i, 0)];
+        const float ex_h = *B.E1(pb, 0, er, col), ey_h = *B.E1(pb, 1, er, col), ez_h = *B.E1(pb, 2, er, col);
+        *B.H1(pb, 0, er, col) = yee_upd(A, h0[e][0], DBC ? Bq : cdz_h, e1[e][1], ey_h, DBC ? Bq : cdy_h,
+                                        *B.E1(pb, 2, er + 1, col), ez_h);
+        *B.H1(pb, 1, er, col) = yee_upd(A, h0[e][1], DBC ? Bq : cdx, *B.E1(pb, 2, er, col + 1), ez_h,
+                                        DBC ? Bq : cdz_h, e1[e][0], ex_h);
+        *B.H1(pb, 2, er, col) = yee_upd(A, h0[e][2], DBC ? Bq : cdy_h, *B.E1(pb, 0, er + 1, col), ex_h,
+                                        DBC ? Bq : cdx, *B.E1(pb, 1, er, col + 1), ey_h);
+      }
+    }
+    consumer_sync();  // (B)
+
+    if (act && kh >= it.kz0 && kh <= min(it.kz1, g.nz - 1) && er >= 1 && er <= RW - 2) {
+      const int hb = kh & 1, i = ie[1];
+      const float cdz_e = co.cdz_e[kh];
+      float ox, oy, oz;
+      e_update1<CAC, CBC>(co, g, i, j, kh + g.zoff, cdy_e, cdz_e, co.cdx_e[i], cap, cbp,
+                          *B.E1(hb, 0, er, CR), *B.E1(hb, 1, er, CR), *B.E1(hb, 2, er, CR),
+                          *B.H1(hb, 0, er, CR), *B.H1(hb, 1, er, CR), *B.H1(hb, 2, er, CR),
+                          *B.H1(hb, 0, er - 1, CR), *B.H1(hb, 2, er - 1, CR), *B.H1(hb, 1, er, CR - 1),
+                          *B.H1(hb, 2, er, CR - 1), *B.H1(hb ^ 1, 0, er, CR), *B.H1(hb ^ 1, 1, er, CR), ox,
+                          oy, oz);
+      if (src_row(a.src, 2, j, kh)) {
+        ox = __fadd_rn(ox, src_add(a.src, 2, 0, i, j, kh));
+        oy = __fadd_rn(oy, src_add(a.src, 2, 1, i, j, kh));
+        oz = __fadd_rn(oz, src_add(a.src, 2, 2, i, j, kh));
+      }
+      *B.E2(hb, 0, er - 1, CR) = ox;
+      *B.E2(hb, 1, er - 1, CR) = oy;
+      *B.E2(hb, 2, er - 1, CR) = oz;
+    }
+    if (l1) {
+#pragma unroll
+      for (int e = 0; e < 3; ++e)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) h0[e][q] = h0n[e][q];
+      dap[0] = dan[0];
+      dap[1] = dan[1];
+      dbp[0] = dbn[0];
+      dbp[1] = dbn[1];
+      cap = can;
+      cbp = cbn;
+    }
+  }
+}
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+__global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm) {
+  using L = StageLayout<CAC, CBC, DAC, DBC>;
+  constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
+  constexpr uint32_t kBytesF = kBX * kTB2BY * 4, kBytesC = kBX * kTB2RowsCA * 4,
+                     kBytesD = kBX * kTB2RowsDA * 4;
+  constexpr uint32_t kStageBytes = 6 * kBytesF + (CAC + CBC) * kBytesC + (DAC + DBC) * kBytesD;
+  constexpr int kQ = 8;
+  extern __shared__ __align__(128) float smem[];
+
+  const Geo& g = a.g;
+  const CoefArgs& co = a.co;
+  const int S = a.nstages;
+  Bufs B;
+  B.stages = smem;
+  B.e1b = smem + (size_t)S * L::floats;
+  B.h1b = B.e1b + kTB2E1;
+  B.e2b = B.h1b + kTB2H1;
+  B.full = reinterpret_cast<uint64_t*>(B.e2b + kTB2E2);
+  B.empty = B.full + S;
+  int* item_q = reinterpret_cast<int*>(B.empty + S);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int T = a.ntx * a.nty;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&B.full[s]), 1);
+      mbar_init(smem_u32(&B.empty[s]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (w == FACE) {  // upper-face DoFs, two steps: h <- Da*(Da*h + 0) + 0
+    const long long nf = face_points(g);
+    for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {
+      face_point(g, a.in, a.out, co, t);
+      face_point(g, a.out, a.out, co, t);
+    }
+    return;
+  }
+
+  if (w == PROD) {  // TMA producer (one lane)
+    if (l != 0) return;
+    int p_item = -1, p_e = 0, p_nE = 0, p_seq = 0;
+    for (int q = 0;; ++q) {
+      const int s = q % S;
+      if (q >= S) mbar_wait(smem_u32(&B.empty[s]), (uint32_t)(((q / S) - 1) & 1));
+      const uint32_t bar = smem_u32(&B.full[s]);
+      if (p_item < 0) {
+        const unsigned long long v = atomicAdd(a.sched, 1ull) - a.sched_base;
+        const int it = v < (unsigned long long)a.nitems ? (int)v : -1;
+        item_q[p_seq % kQ] = it;
+        ++p_seq;
+        if (it < 0) {
+          mbar_arrive(bar);
+          return;
+        }
+        p_item = it;
+        p_e = 0;
+        const int kz0 = (it / T) * a.zchunk;
+        const int kz1 = min(kz0 + a.zchunk, g.nz);
+        p_nE = (kz0 >= 2 ? 1 : 0) + min(kz1 + 1, g.nz - 1) - max(kz0 - 1, 0) + 1;
+      }
+      const int chunk = p_item / T, tile = p_item - chunk * T;
+      const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTB2Rows;
+      const int kz0 = chunk * a.zchunk;
+      const int pro = kz0 >= 2 ? 1 : 0;
+      float* dst = B.stages + (size_t)s * L::floats;
+      if (pro && p_e == 0) {  // hx, hy of plane kz0-2 (tensor z = plane + 1)
+        mbar_expect_tx(bar, 2 * kBytesF);
+        tma_load_3d(smem_u32(dst + 3 * kTB2SlotF), &tm.m[3], x0 - 4, y0 - 2, kz0 - 1, bar);
+        tma_load_3d(smem_u32(dst + 4 * kTB2SlotF), &tm.m[4], x0 - 4, y0 - 2, kz0 - 1, bar);
+      } else {
+        const int z = max(kz0 - 1, 0) + p_e - pro + 1;
+        mbar_expect_tx(bar, kStageBytes);
+#pragma unroll
+        for (int q2 = 0; q2 < 6; ++q2)
+          tma_load_3d(smem_u32(dst + q2 * kTB2SlotF), &tm.m[q2], x0 - 4, y0 - 2, z, bar);
+        int m = 6;
+        if (CAC) tma_load_3d(smem_u32(dst + L::off_ca), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (CBC) tma_load_3d(smem_u32(dst + L::off_cb), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (DAC) tma_load_3d(smem_u32(dst + L::off_da), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (DBC) tma_load_3d(smem_u32(dst + L::off_db), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
+        (void)NARR;
+      }
+      if (++p_e == p_nE) p_item = -1;
+    }
+  }
+
+  uint64_t st_pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(st_pol));
+  Cursor cur{0, false};
+  int c_seq = 0;
+  for (;;) {
+    mbar_wait(smem_u32(&B.full[cur.cs % S]), (uint32_t)((cur.cs / S) & 1));
+    cur.peeked = true;
+    const int item = item_q[c_seq % kQ];
+    ++c_seq;
+    if (item < 0) break;
+    Item it;
+    const int chunk = item / T, tile = item - chunk * T;
+    it.x0 = (tile % a.ntx) * kTX;
+    it.y0 = (tile / a.ntx) * kTB2Rows;
+    it.kz0 = chunk * a.zchunk;
+    it.kz1 = min(it.kz0 + a.zchunk, g.nz);
+    it.pstart = max(it.kz0 - 1, 0);
+    it.pin_end = min(it.kz1 + 1, g.nz - 1);
+    it.pend = it.kz1 + 1;
+    if (w == EDGE)
+      tb2_edge<CAC, CBC, DAC, DBC>(a, it, B, cur, l);
+    else
+      tb2_rows<CAC, CBC, DAC, DBC>(a, it, B, cur, w, l, st_pol);
+  }
+}
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+cudaError_t launch_t(const FusedArgs& a, const TMaps& tm, dim3 grid, size_t smem, cudaStream_t st) {
+  k_tb2<CAC, CBC, DAC, DBC><<<grid, kTB2Threads, smem, st>>>(a, tm);
+  return cudaGetLastError();
+}
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+cudaError_t set_limit_t() {
+  return cudaFuncSetAttribute(k_tb2<CAC, CBC, DAC, DBC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024);
+}
+
+using LaunchFn = cudaError_t (*)(const FusedArgs&, const TMaps&, dim3, size_t, cudaStream_t);
+using LimitFn = cudaError_t (*)();
+
+#define YB_T(m) launch_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
+#define YB_L(m) set_limit_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
+const LaunchFn kLaunch[16] = {YB_T(0),  YB_T(1),  YB_T(2),  YB_T(3), YB_T(4),  YB_T(5),
+                              YB_T(6),  YB_T(7),  YB_T(8),  YB_T(9), YB_T(10), YB_T(11),
+                              YB_T(12), YB_T(13), YB_T(14), YB_T(15)};
+const LimitFn kLimit[16] = {YB_L(0),  YB_L(1),  YB_L(2),  YB_L(3), YB_L(4),  YB_L(5),
+                            YB_L(6),  YB_L(7),  YB_L(8),  YB_L(9), YB_L(10), YB_L(11),
+                            YB_L(12), YB_L(13), YB_L(14), YB_L(15)};
+#undef YB_T
+#undef YB_L
+
+}  // namespace
+
+cudaError_t tb2_set_smem_limits() {
+  for (int m = 0; m < 16; ++m) {
+    const cudaError_t e = kLimit[m]();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid, size_t smem,
+                       cudaStream_t st) {
+  return kLaunch[cell_mask & 15](a, tm, grid, smem, st);
+}
+
+}  // namespace yb

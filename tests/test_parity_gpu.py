@@ -32,7 +32,7 @@ def assert_bits(a, b, what=""):
                                  f"{y[tuple(v[0] for v in bad)]}"
 
 
-VARIANTS = [0, 1]  # fused, naive
+VARIANTS = [0, 1, 2]  # fused, naive, two-step temporal blocking
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -176,15 +176,16 @@ def test_configs_vs_oracle(yb, oracle, name, variant):
     assert_bits(got, want, name)
 
 
+@pytest.mark.parametrize("variant", [0, 2])
 @pytest.mark.parametrize("shape,zchunk", [((40, 24, 30), 1), ((40, 24, 30), 3), ((40, 24, 30), 7),
                                           ((40, 24, 30), 64), ((200, 64, 40), 2), ((130, 40, 33), 1),
                                           ((256, 96, 21), 4)])
-def test_zchunks_bit_identical(yb, oracle, shape, zchunk):
+def test_zchunks_bit_identical(yb, oracle, shape, zchunk, variant):
     """Persistent CTAs stride over (tile, z-chunk) items; with many items per
     CTA the TMA ring runs across item boundaries (prologue/epilogue planes)."""
     (nx, ny, nz), steps = shape, 9
     f = oracle.fill_fields(nx, ny, nz, 41)
-    with yb.Simulation(nx, ny, nz, zchunk=zchunk) as sim:
+    with yb.Simulation(nx, ny, nz, zchunk=zchunk, variant=variant) as sim:
         sim.generate_medium(42, 43)
         sim.upload(f)
         sim.run(steps)
@@ -273,13 +274,13 @@ def test_full_size_fused_equals_naive(yb, cfg):
     else:
         nx, ny, nz, es, ss, fs, steps = 1024, 1024, 256, 5, 5, 6, 100
     digs = []
-    for variant in VARIANTS:
+    for variant in VARIANTS:  # fused, naive, two-step
         with yb.Simulation(nx, ny, nz, variant=variant) as sim:
             sim.generate_medium(es, ss)
             sim.fill(fs)
             sim.run(steps)
             digs.append(sim.digest())
-    assert digs[0] == digs[1]
+    assert digs[0] == digs[1] == digs[2]
 
 
 def test_cpp_shim_known_answers(yb, tmp_path):
