@@ -38,6 +38,7 @@ constexpr int kTB2SlotD = slot_floats(kTB2RowsDA);
 constexpr int kTB2E1 = 2 * 3 * kTB2RowWarps * kBX;    // E^{n+1} planes (double buffered)
 constexpr int kTB2H1 = 2 * 3 * (kTB2Rows + 2) * kBX;  // H^{n+3/2} planes (double buffered)
 constexpr int kTB2E2 = 2 * 3 * (kTB2Rows + 1) * kBX;  // E^{n+2} planes (double buffered)
+constexpr int kTB2Edge = 2 * 3 * kTB2RowWarps * 3 + 2 * 2 * (kTB2Rows + 2) * 2 + 2 * 2 * kTB2RowWarps;
 
 // floats of one stage for a coefficient set (mask bit q: array q per-cell)
 inline int tb2_stage_floats(int cell_mask) {
@@ -46,7 +47,7 @@ inline int tb2_stage_floats(int cell_mask) {
 }
 
 inline size_t tb2_smem_bytes(int cell_mask, int stages) {
-  return (size_t)stages * tb2_stage_floats(cell_mask) * 4 + (size_t)(kTB2E1 + kTB2H1 + kTB2E2) * 4 +
+  return (size_t)stages * tb2_stage_floats(cell_mask) * 4 + (size_t)(kTB2E1 + kTB2H1 + kTB2E2 + kTB2Edge) * 4 +
          (size_t)stages * 16 + 8 * 4;
 }
 

@@ -54,32 +54,39 @@ struct F4x3 {
 };
 
 // E update of one float4 group (4 consecutive i) — the same expression as
-// the single-step kernel (reference operand order, PEC as a mask).
+// the single-step kernel (reference operand order). PEC / non-DoF positions
+// are forced to +0 afterwards; the mask pass only runs where some element can
+// be masked (boundary tiles, rows, planes), decided warp-uniformly.
 template <bool CAC, bool CBC>
-__device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int i0, int j, int kg,
-                                          float cdy, float cdz, float4 cdx, float4 ca, float4 cb,
-                                          float4 ex, float4 ey, float4 ez, float4 hx, float4 hy,
-                                          float4 hz, float4 hx_jm, float4 hz_jm, float4 hy_im,
-                                          float4 hz_im, float4 hx_km, float4 hy_km) {
-  const bool kin = kg >= 1 && kg < g.nzg;
-  const bool jin = j >= 1 && j < g.ny, jlt = j >= 0 && j < g.ny;
+__device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int i0, bool xint, int j,
+                                          int kg, float cdy, float cdz, float4 cdx, float4 ca,
+                                          float4 cb, float4 ex, float4 ey, float4 ez, float4 hx,
+                                          float4 hy, float4 hz, float4 hx_jm, float4 hz_jm,
+                                          float4 hy_im, float4 hz_im, float4 hx_km, float4 hy_km) {
   F4x3 o;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int i = i0 + q;
-    const bool iin = i >= 1 && i < g.nx, ilt = i >= 0 && i < g.nx;
     const float A = CAC ? elc(ca, q) : co.ca_s;
     const float B = elc(cb, q);
-    el(o.x, q) = (ilt && jin && kin) ? yee_upd(A, elc(ex, q), CBC ? B : cdy, elc(hz, q), elc(hz_jm, q),
-                                               CBC ? B : cdz, elc(hy, q), elc(hy_km, q))
-                                     : 0.f;
-    el(o.y, q) = (iin && jlt && kin) ? yee_upd(A, elc(ey, q), CBC ? B : cdz, elc(hx, q), elc(hx_km, q),
-                                               CBC ? B : elc(cdx, q), elc(hz, q), elc(hz_im, q))
-                                     : 0.f;
-    el(o.z, q) = (iin && jin && kg >= 0 && kg < g.nzg)
-                     ? yee_upd(A, elc(ez, q), CBC ? B : elc(cdx, q), elc(hy, q), elc(hy_im, q),
-                               CBC ? B : cdy, elc(hx, q), elc(hx_jm, q))
-                     : 0.f;
+    el(o.x, q) = yee_upd(A, elc(ex, q), CBC ? B : cdy, elc(hz, q), elc(hz_jm, q), CBC ? B : cdz,
+                         elc(hy, q), elc(hy_km, q));
+    el(o.y, q) = yee_upd(A, elc(ey, q), CBC ? B : cdz, elc(hx, q), elc(hx_km, q),
+                         CBC ? B : elc(cdx, q), elc(hz, q), elc(hz_im, q));
+    el(o.z, q) = yee_upd(A, elc(ez, q), CBC ? B : elc(cdx, q), elc(hy, q), elc(hy_im, q),
+                         CBC ? B : cdy, elc(hx, q), elc(hx_jm, q));
+  }
+  const bool kin = kg >= 1 && kg < g.nzg;
+  const bool jin = j >= 1 && j < g.ny;
+  if (!(xint && jin && kin)) {
+    const bool jlt = j >= 0 && j < g.ny, kz = kg >= 0 && kg < g.nzg;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q;
+      const bool iin = i >= 1 && i < g.nx, ilt = i >= 0 && i < g.nx;
+      if (!(ilt && jin && kin)) el(o.x, q) = 0.f;
+      if (!(iin && jlt && kin)) el(o.y, q) = 0.f;
+      if (!(iin && jin && kz)) el(o.z, q) = 0.f;
+    }
   }
   return o;
 }
@@ -142,6 +149,15 @@ struct Bufs {
   __device__ float* E2(int b, int comp, int r, int col) const {
     return e2b + ((size_t)(b * 3 + comp) * (RW - 2) + r) * BX + col;
   }
+  // edge-column state: H0 at CL/CR/CR+1, Da/Db at CL/CR, Ca/Cb at CR
+  float* edge;
+  __device__ float* H0e(int b, int comp, int r, int e) const { return edge + ((b * 3 + comp) * RW + r) * 3 + e; }
+  __device__ float* De(int b, int q, int r, int e) const {
+    return edge + 2 * 3 * RW * 3 + ((b * 2 + q) * (RW - 1) + r) * 2 + e;
+  }
+  __device__ float* Ce(int b, int q, int r) const {
+    return edge + 2 * 3 * RW * 3 + 2 * 2 * (RW - 1) * 2 + (b * 2 + q) * RW + r;
+  }
 };
 
 struct Cursor {
@@ -174,6 +190,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
   const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
   const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool xint = it.x0 >= 1 && it.x0 + kTX <= g.nx;  // no lane touches i=0 or i>=nx
   F4x3 h0p = {z4, z4, z4};
   float4 cap = z4, cbp = z4, dap = z4, dbp = z4, dap2 = z4, dbp2 = z4;
 
@@ -205,7 +222,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       if (CBC) cbn = lds4(F + L::off_cb + er * BX + c);
       if (DAC && er <= RW - 2) dan = lds4(F + L::off_da + er * BX + c);
       if (DBC && er <= RW - 2) dbn = lds4(F + L::off_db + er * BX + c);
-      e1c = e_update4<CAC, CBC>(co, g, i0, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn,
+      e1c = e_update4<CAC, CBC>(co, g, i0, xint, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn,
                                 lds4(F + 0 * kTB2SlotF + rs * BX + c), lds4(F + 1 * kTB2SlotF + rs * BX + c),
                                 lds4(F + 2 * kTB2SlotF + rs * BX + c), h0n.x, h0n.y, h0n.z,
                                 lds4(F + 3 * kTB2SlotF + (rs - 1) * BX + c),
@@ -262,7 +279,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       const float4 hz = lds4(B.H1(hb, 2, er, c));
       const float4 hy_im = shift_im(hy, l, *B.H1(hb, 1, er, CL));
       const float4 hz_im = shift_im(hz, l, *B.H1(hb, 2, er, CL));
-      e2c = e_update4<CAC, CBC>(co, g, i0, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
+      e2c = e_update4<CAC, CBC>(co, g, i0, xint, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
                                 lds4(B.E1(hb, 0, er, c)), lds4(B.E1(hb, 1, er, c)), lds4(B.E1(hb, 2, er, c)),
                                 hx, hy, hz, lds4(B.H1(hb, 0, er - 1, c)), lds4(B.H1(hb, 2, er - 1, c)), hy_im,
                                 hz_im, lds4(B.H1(hb ^ 1, 0, er, c)), lds4(B.H1(hb ^ 1, 1, er, c)));
@@ -330,8 +347,11 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
 }
 
 // ============================================================= edge warp
-// Lane r owns row j = y0-1+r (r < RW) at the edge columns x0-1 (CL),
-// x0+128 (CR) and x0+129 (CR+1): E1 at all three, H1 at CL and CR, E2 at CR.
+// The columns the row warps' lanes cannot cover: x0-1 (CL), x0+128 (CR),
+// x0+129 (CR+1). Work is spread over the lanes as (row, column) tasks per
+// level — L1: 11 + 11 + 10 = 32 tasks, L2: 20, L3: 9 — and all state that
+// crosses planes (H0, Da/Db, Ca/Cb of these columns) lives in shared memory
+// (Bufs::h0e/de/cee), so any lane can pick up any task.
 template <bool CAC, bool CBC, bool DAC, bool DBC>
 __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
                                          int l) {
@@ -339,123 +359,104 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
   const Geo& g = a.g;
   const CoefArgs& co = a.co;
   const int S = a.nstages;
-  const bool act = l < RW;
-  const int er = act ? l : 0;
-  const int j = it.y0 - 1 + er;
-  const int rs = er + 1;
-  const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
-  const int ie[3] = {it.x0 - 1, it.x0 + kTX, it.x0 + kTX + 1};
-  const int ce[3] = {CL, CR, CR + 1};
-  float h0[3][3] = {};   // H0(p-1) [col][comp]
-  float dap[2] = {}, dbp[2] = {};  // Da/Db(p-1) at CL, CR
-  float cap = 0.f, cbp = 0.f;      // Ca/Cb(p-1) at CR
+  // L1 task of this lane: column index e (0: CL, 1: CR, 2: CR+1) and row r
+  const int e1i = l < RW ? 0 : (l < 2 * RW ? 1 : 2);
+  const int e1r = l - e1i * RW;
+  auto ce = [](int e) { return e == 0 ? CL : (e == 1 ? CR : CR + 1); };
+  auto ie = [&](int e) { return e == 0 ? it.x0 - 1 : it.x0 + kTX + (e - 1); };
+  // L2 task: (column CL|CR, row 0..9) for lanes 0..19
+  const int e2i = l < RW - 1 ? 0 : 1, e2r = l - e2i * (RW - 1);
+  const bool l2_lane = l < 2 * (RW - 1);
+  // L3 task: column CR, rows 1..9 for lanes 0..8
+  const int e3r = l + 1;
+  const bool l3_lane = l < RW - 2;
 
-  if (it.kz0 >= 2) {
+  if (it.kz0 >= 2) {  // prologue: H0 hx, hy of plane kz0-2 at the edge columns
     const int s = cur.wait(B, S);
     const float* F = B.stages + (size_t)s * L::floats;
-    if (act) {
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        h0[e][0] = F[3 * kTB2SlotF + rs * BX + ce[e]];
-        h0[e][1] = F[4 * kTB2SlotF + rs * BX + ce[e]];
-      }
-    }
+    const int pb = (it.kz0 - 2) & 1;
+    *B.H0e(pb, 0, e1r, e1i) = F[3 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
+    *B.H0e(pb, 1, e1r, e1i) = F[4 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
     consumer_sync();
   }
 
   for (int p = it.pstart; p <= it.pend; ++p) {
     const bool l1 = p <= it.pin_end;
-    float e1[3][3] = {}, h0n[3][3] = {};
-    float dan[2] = {}, dbn[2] = {}, can = 0.f, cbn = 0.f;
     if (l1) {
       const int s1 = cur.wait(B, S);
       const float* F = B.stages + (size_t)s1 * L::floats;
-      const float cdz_e = co.cdz_e[p];
-      if (act) {
-#pragma unroll
-        for (int e = 0; e < 3; ++e) {
-          const int col = ce[e], i = ie[e];
-          const float* Fr = F + rs * BX + col;
-          h0n[e][0] = Fr[3 * kTB2SlotF];
-          h0n[e][1] = Fr[4 * kTB2SlotF];
-          h0n[e][2] = Fr[5 * kTB2SlotF];
-          const float ca = CAC ? F[L::off_ca + er * BX + col] : 0.f;
-          const float cb = CBC ? F[L::off_cb + er * BX + col] : 0.f;
-          e_update1<CAC, CBC>(co, g, i, j, p + g.zoff, cdy_e, cdz_e, co.cdx_e[max(i, 0)], ca, cb,
-                              Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], h0n[e][0], h0n[e][1], h0n[e][2],
-                              Fr[3 * kTB2SlotF - BX], Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1],
-                              Fr[5 * kTB2SlotF - 1], h0[e][0], h0[e][1], e1[e][0], e1[e][1], e1[e][2]);
-          if (src_row(a.src, 1, j, p)) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) e1[e][q] = __fadd_rn(e1[e][q], src_add(a.src, 1, q, i, j, p));
-          }
-#pragma unroll
-          for (int q = 0; q < 3; ++q) *B.E1(p & 1, q, er, col) = e1[e][q];
-          if (e < 2 && er <= RW - 2) {
-            if (DAC) dan[e] = F[L::off_da + er * BX + col];
-            if (DBC) dbn[e] = F[L::off_db + er * BX + col];
-          }
-          if (e == 1) {
-            can = ca;
-            cbn = cb;
-          }
-        }
+      const int r = e1r, col = ce(e1i), i = ie(e1i), j = it.y0 - 1 + r, rs = r + 1;
+      const float* Fr = F + rs * BX + col;
+      const float hx = Fr[3 * kTB2SlotF], hy = Fr[4 * kTB2SlotF], hz = Fr[5 * kTB2SlotF];
+      const float ca = CAC ? F[L::off_ca + r * BX + col] : 0.f;
+      const float cb = CBC ? F[L::off_cb + r * BX + col] : 0.f;
+      float ox, oy, oz;
+      e_update1<CAC, CBC>(co, g, i, j, p + g.zoff, co.cdy_e[max(j, 0)], co.cdz_e[p], co.cdx_e[max(i, 0)], ca,
+                          cb, Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], hx, hy, hz, Fr[3 * kTB2SlotF - BX],
+                          Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1], Fr[5 * kTB2SlotF - 1],
+                          *B.H0e((p - 1) & 1, 0, r, e1i), *B.H0e((p - 1) & 1, 1, r, e1i), ox, oy, oz);
+      if (src_row(a.src, 1, j, p)) {
+        ox = __fadd_rn(ox, src_add(a.src, 1, 0, i, j, p));
+        oy = __fadd_rn(oy, src_add(a.src, 1, 1, i, j, p));
+        oz = __fadd_rn(oz, src_add(a.src, 1, 2, i, j, p));
+      }
+      *B.E1(p & 1, 0, r, col) = ox;
+      *B.E1(p & 1, 1, r, col) = oy;
+      *B.E1(p & 1, 2, r, col) = oz;
+      *B.H0e(p & 1, 0, r, e1i) = hx;
+      *B.H0e(p & 1, 1, r, e1i) = hy;
+      *B.H0e(p & 1, 2, r, e1i) = hz;
+      if (e1i < 2 && r <= RW - 2) {
+        if (DAC) *B.De(p & 1, 0, r, e1i) = F[L::off_da + r * BX + col];
+        if (DBC) *B.De(p & 1, 1, r, e1i) = F[L::off_db + r * BX + col];
+      }
+      if (e1i == 1) {
+        *B.Ce(p & 1, 0, r) = ca;
+        *B.Ce(p & 1, 1, r) = cb;
       }
     }
     consumer_sync();  // (A)
 
-    const int kh = p - 1;
-    if (act && kh >= it.pstart && kh <= min(it.kz1, g.nz - 1) && er <= RW - 2) {
-      const int pb = kh & 1;
-      const float cdz_h = co.cdz_h[kh];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {  // CL, CR
-        const int col = ce[e], i = ie[e];
-        const float A = DAC ? dap[e] : co.da_s;
-        const float Bq = dbp[e];
-        const float cdx = co.cdx_h[max(i, 0)];
-        const float ex_h = *B.E1(pb, 0, er, col), ey_h = *B.E1(pb, 1, er, col), ez_h = *B.E1(pb, 2, er, col);
-        *B.H1(pb, 0, er, col) = yee_upd(A, h0[e][0], DBC ? Bq : cdz_h, e1[e][1], ey_h, DBC ? Bq : cdy_h,
-                                        *B.E1(pb, 2, er + 1, col), ez_h);
-        *B.H1(pb, 1, er, col) = yee_upd(A, h0[e][1], DBC ? Bq : cdx, *B.E1(pb, 2, er, col + 1), ez_h,
-                                        DBC ? Bq : cdz_h, e1[e][0], ex_h);
-        *B.H1(pb, 2, er, col) = yee_upd(A, h0[e][2], DBC ? Bq : cdy_h, *B.E1(pb, 0, er + 1, col), ex_h,
-                                        DBC ? Bq : cdx, *B.E1(pb, 1, er, col + 1), ey_h);
-      }
+    const int kh = p - 1, hb = kh & 1;
+    if (l2_lane && kh >= it.pstart && kh <= min(it.kz1, g.nz - 1)) {
+      const int r = e2r, col = ce(e2i), i = ie(e2i), j = it.y0 - 1 + r;
+      const float A = DAC ? *B.De(hb, 0, r, e2i) : co.da_s;
+      const float Bq = DBC ? *B.De(hb, 1, r, e2i) : 0.f;
+      const float cdz_h = co.cdz_h[kh], cdy_h = co.cdy_h[max(j, 0)], cdx = co.cdx_h[max(i, 0)];
+      const float ex_h = *B.E1(hb, 0, r, col), ey_h = *B.E1(hb, 1, r, col), ez_h = *B.E1(hb, 2, r, col);
+      // E1(p) at this column (z+1 neighbour); in the top drain plane p = nz
+      // it is the PEC zero, not the stale buffer content
+      const float exk = l1 ? *B.E1(p & 1, 0, r, col) : 0.f;
+      const float eyk = l1 ? *B.E1(p & 1, 1, r, col) : 0.f;
+      *B.H1(hb, 0, r, col) = yee_upd(A, *B.H0e(hb, 0, r, e2i), DBC ? Bq : cdz_h, eyk, ey_h,
+                                     DBC ? Bq : cdy_h, *B.E1(hb, 2, r + 1, col), ez_h);
+      *B.H1(hb, 1, r, col) = yee_upd(A, *B.H0e(hb, 1, r, e2i), DBC ? Bq : cdx, *B.E1(hb, 2, r, col + 1), ez_h,
+                                     DBC ? Bq : cdz_h, exk, ex_h);
+      *B.H1(hb, 2, r, col) = yee_upd(A, *B.H0e(hb, 2, r, e2i), DBC ? Bq : cdy_h, *B.E1(hb, 0, r + 1, col), ex_h,
+                                     DBC ? Bq : cdx, *B.E1(hb, 1, r, col + 1), ey_h);
     }
     consumer_sync();  // (B)
 
-    if (act && kh >= it.kz0 && kh <= min(it.kz1, g.nz - 1) && er >= 1 && er <= RW - 2) {
-      const int hb = kh & 1, i = ie[1];
-      const float cdz_e = co.cdz_e[kh];
+    if (l3_lane && kh >= it.kz0 && kh <= min(it.kz1, g.nz - 1)) {
+      const int r = e3r, i = ie(1), j = it.y0 - 1 + r;
       float ox, oy, oz;
-      e_update1<CAC, CBC>(co, g, i, j, kh + g.zoff, cdy_e, cdz_e, co.cdx_e[i], cap, cbp,
-                          *B.E1(hb, 0, er, CR), *B.E1(hb, 1, er, CR), *B.E1(hb, 2, er, CR),
-                          *B.H1(hb, 0, er, CR), *B.H1(hb, 1, er, CR), *B.H1(hb, 2, er, CR),
-                          *B.H1(hb, 0, er - 1, CR), *B.H1(hb, 2, er - 1, CR), *B.H1(hb, 1, er, CR - 1),
-                          *B.H1(hb, 2, er, CR - 1), *B.H1(hb ^ 1, 0, er, CR), *B.H1(hb ^ 1, 1, er, CR), ox,
-                          oy, oz);
+      e_update1<CAC, CBC>(co, g, i, j, kh + g.zoff, co.cdy_e[max(j, 0)], co.cdz_e[kh], co.cdx_e[i],
+                          *B.Ce(hb, 0, r), *B.Ce(hb, 1, r), *B.E1(hb, 0, r, CR), *B.E1(hb, 1, r, CR),
+                          *B.E1(hb, 2, r, CR), *B.H1(hb, 0, r, CR), *B.H1(hb, 1, r, CR), *B.H1(hb, 2, r, CR),
+                          *B.H1(hb, 0, r - 1, CR), *B.H1(hb, 2, r - 1, CR), *B.H1(hb, 1, r, CR - 1),
+                          *B.H1(hb, 2, r, CR - 1), *B.H1(hb ^ 1, 0, r, CR), *B.H1(hb ^ 1, 1, r, CR), ox, oy,
+                          oz);
       if (src_row(a.src, 2, j, kh)) {
         ox = __fadd_rn(ox, src_add(a.src, 2, 0, i, j, kh));
         oy = __fadd_rn(oy, src_add(a.src, 2, 1, i, j, kh));
         oz = __fadd_rn(oz, src_add(a.src, 2, 2, i, j, kh));
       }
-      *B.E2(hb, 0, er - 1, CR) = ox;
-      *B.E2(hb, 1, er - 1, CR) = oy;
-      *B.E2(hb, 2, er - 1, CR) = oz;
+      *B.E2(hb, 0, r - 1, CR) = ox;
+      *B.E2(hb, 1, r - 1, CR) = oy;
+      *B.E2(hb, 2, r - 1, CR) = oz;
     }
-    if (l1) {
-#pragma unroll
-      for (int e = 0; e < 3; ++e)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) h0[e][q] = h0n[e][q];
-      dap[0] = dan[0];
-      dap[1] = dan[1];
-      dbp[0] = dbn[0];
-      dbp[1] = dbn[1];
-      cap = can;
-      cbp = cbn;
-    }
+    // lanes read other lanes' E1/Ce slots in L3 that the next L1 rewrites
+    __syncwarp();
   }
 }
 
@@ -477,7 +478,8 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   B.e1b = smem + (size_t)S * L::floats;
   B.h1b = B.e1b + kTB2E1;
   B.e2b = B.h1b + kTB2H1;
-  B.full = reinterpret_cast<uint64_t*>(B.e2b + kTB2E2);
+  B.edge = B.e2b + kTB2E2;
+  B.full = reinterpret_cast<uint64_t*>(B.edge + kTB2Edge);
   B.empty = B.full + S;
   int* item_q = reinterpret_cast<int*>(B.empty + S);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
