@@ -257,7 +257,7 @@ int prepare_fused(yb_sim* s) {
         const int len = (s->g.nz + Z - 1) / Z;
         const int Zr = (s->g.nz + len - 1) / len;
         const long long rounds = (T * Zr + s->num_sms - 1) / s->num_sms;
-        const double cost = (double)rounds * (len + (Zr > 1 ? 3.0 : 0.0)) * (1.0 + len / 400.0);
+        const double cost = (double)rounds * (len + (Zr > 1 ? 3.0 : 0.0)) * (1.0 + len / 4000.0);
         if (cost < best - 1e-9) {
           best = cost;
           zc2 = len;

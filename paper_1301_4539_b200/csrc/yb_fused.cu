@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool jin = j >= 1 && j < g.ny, jlt = j < g.ny;
     const bool jnin = jn < g.ny;  // jn >= 1 always
     const bool ih_in = ih >= 1 && ih < g.nx;
+    const bool xint = x0 >= 1 && x0 + kTX <= g.nx;  // no lane touches i=0 or i>=nx
 
     // carried state: H(k-1) (own row, hy of row j+1, hx of the halo column),
     // Da/Db(k-1), E(k-1) own row / +y row (ex, ez) / +x column (ey, ez)
@@ -244,33 +245,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (DBC) db4 = lds4(SM(S_DB, r, c));
       float4 exw, eyw, ezw, exn, ezn;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q;
-        const bool iin = i >= 1 && i < g.nx, ilt = i < g.nx;
+      for (int q = 0; q < 4; ++q) {  // unmasked updates; PEC / non-DoF zeroed below
         const float A = CAC ? elc(ca4, q) : co.ca_s;
         const float B = elc(cb4, q);
         const float An = CAC ? elc(ca4n, q) : co.ca_s;
         const float Bn = elc(cb4n, q);
-        el(exw, q) = (ilt && jin && kin)
-                         ? yee_upd(A, elc(ex, q), CBC ? B : cdy_e, elc(hz, q), elc(hz_jm, q),
-                                   CBC ? B : cdz_e, elc(hy, q), elc(phy, q))
-                         : 0.f;
-        el(eyw, q) = (iin && jlt && kin)
-                         ? yee_upd(A, elc(ey, q), CBC ? B : cdz_e, elc(hx, q), elc(phx, q),
-                                   CBC ? B : elc(cdx_e, q), elc(hz, q), elc(hz_im, q))
-                         : 0.f;
-        el(ezw, q) = (iin && jin)
-                         ? yee_upd(A, elc(ez, q), CBC ? B : elc(cdx_e, q), elc(hy, q),
-                                   elc(hy_im, q), CBC ? B : cdy_e, elc(hx, q), elc(hx_jm, q))
-                         : 0.f;
-        el(exn, q) = (ilt && jnin && kin)
-                         ? yee_upd(An, elc(ex_n, q), CBC ? Bn : cdy_en, elc(hz_n, q), elc(hz, q),
-                                   CBC ? Bn : cdz_e, elc(hy_n, q), elc(phy_n, q))
-                         : 0.f;
-        el(ezn, q) = (iin && jnin)
-                         ? yee_upd(An, elc(ez_n, q), CBC ? Bn : elc(cdx_e, q), elc(hy_n, q),
-                                   elc(hy_n_im, q), CBC ? Bn : cdy_en, elc(hx_n, q), elc(hx, q))
-                         : 0.f;
+        el(exw, q) = yee_upd(A, elc(ex, q), CBC ? B : cdy_e, elc(hz, q), elc(hz_jm, q), CBC ? B : cdz_e,
+                             elc(hy, q), elc(phy, q));
+        el(eyw, q) = yee_upd(A, elc(ey, q), CBC ? B : cdz_e, elc(hx, q), elc(phx, q),
+                             CBC ? B : elc(cdx_e, q), elc(hz, q), elc(hz_im, q));
+        el(ezw, q) = yee_upd(A, elc(ez, q), CBC ? B : elc(cdx_e, q), elc(hy, q), elc(hy_im, q),
+                             CBC ? B : cdy_e, elc(hx, q), elc(hx_jm, q));
+        el(exn, q) = yee_upd(An, elc(ex_n, q), CBC ? Bn : cdy_en, elc(hz_n, q), elc(hz, q),
+                             CBC ? Bn : cdz_e, elc(hy_n, q), elc(phy_n, q));
+        el(ezn, q) = yee_upd(An, elc(ez_n, q), CBC ? Bn : elc(cdx_e, q), elc(hy_n, q), elc(hy_n_im, q),
+                             CBC ? Bn : cdy_en, elc(hx_n, q), elc(hx, q));
+      }
+      if (!(xint && jin && jnin && kin)) {  // warp-uniform: only boundary tiles/rows/planes
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = i0 + q;
+          const bool iin = i >= 1 && i < g.nx, ilt = i < g.nx;
+          if (!(ilt && jin && kin)) el(exw, q) = 0.f;
+          if (!(iin && jlt && kin)) el(eyw, q) = 0.f;
+          if (!(iin && jin)) el(ezw, q) = 0.f;
+          if (!(ilt && jnin && kin)) el(exn, q) = 0.f;
+          if (!(iin && jnin)) el(ezn, q) = 0.f;
+        }
       }
       // +x halo column i = x0+TX, row j: ey, ez (lane 31)
       float eyc = 0.f, ezc = 0.f, hx_c = 0.f;
