@@ -163,7 +163,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--variant", default="fused", choices=["fused", "naive", "tb2"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "fused", "naive", "tb2"],
+                    help="auto: tb2 (two steps per sweep) on 1 GPU, fused with z-slabs on N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--zchunk", type=int, default=0, help="fused: z planes per work item (0 = auto)")
@@ -204,6 +205,8 @@ def main():
     # NCCL ops all run on it, so the events bracket exactly our work
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    if args.variant == "auto":
+        args.variant = "tb2" if world == 1 else "fused"
     variant = {"fused": Y.VARIANT_FUSED, "naive": Y.VARIANT_NAIVE, "tb2": Y.VARIANT_TB2}[args.variant]
     if world > 1 and variant != Y.VARIANT_FUSED:
         raise SystemExit("z-slab multi-GPU runs use the one-step fused variant")
@@ -290,6 +293,9 @@ def main():
                            2: "k_tb2 (two steps per sweep)"}[variant],
                 "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,
                 "peak_source": peak_src, "per_gpu": world > 1,
+                "one_sweep_bytes_per_cell_update": 48.0 + 4.0 * info1["n_cell_arrays"],
+                "effective_frac_vs_one_sweep": (48.0 + 4.0 * info1["n_cell_arrays"]) * cells
+                                               * args.steps / (ms * 1e-3) / 1e9 / peak,
                 "step_ms_share_of_kernel": kern_ms / (ms / args.steps * steps_per_launch)}
     config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
                    "ctas": info1["grid_x"], "n_cell_arrays": info1["n_cell_arrays"]})
