@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool jin = j >= 1 && j < g.ny, jlt = j < g.ny;
     const bool jnin = jn < g.ny;  // jn >= 1 always
     const bool ih_in = ih >= 1 && ih < g.nx;
-    const bool xint = x0 >= 1 && x0 + kTX <= g.nx;  // no lane touches i=0 or i>=nx
+    const bool xint = i0 >= 1 && i0 + 4 <= g.nx;  // this lane touches neither i=0 nor i>=nx
 
     // carried state: H(k-1) (own row, hy of row j+1, hx of the halo column),
     // Da/Db(k-1), E(k-1) own row / +y row (ex, ez) / +x column (ey, ez)
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         el(ezn, q) = yee_upd(An, elc(ez_n, q), CBC ? Bn : elc(cdx_e, q), elc(hy_n, q), elc(hy_n_im, q),
                              CBC ? Bn : cdy_en, elc(hx_n, q), elc(hx, q));
       }
-      if (!(xint && jin && jnin && kin)) {  // warp-uniform: only boundary tiles/rows/planes
+      if (!(xint && jin && jnin && kin)) {  // only lanes on a boundary column/row/plane
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int i = i0 + q;

@@ -190,7 +190,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
   const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
   const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const bool xint = it.x0 >= 1 && it.x0 + kTX <= g.nx;  // no lane touches i=0 or i>=nx
+  const bool xint = i0 >= 1 && i0 + 4 <= g.nx;  // this lane touches neither i=0 nor i>=nx
   F4x3 h0p = {z4, z4, z4};
   float4 cap = z4, cbp = z4, dap = z4, dbp = z4, dap2 = z4, dbp2 = z4;
 
