@@ -164,7 +164,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "fused", "naive", "tb2"],
-                    help="auto: tb2 (two steps per sweep) on 1 GPU, fused with z-slabs on N>1")
+                    help="auto: tb2 (two steps per sweep; z-slabs exchange every two steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--zchunk", type=int, default=0, help="fused: z planes per work item (0 = auto)")
@@ -194,7 +194,7 @@ def main():
 
     import torch
     import paper_1301_4539_b200 as Y
-    from paper_1301_4539_b200.slabs import HaloExchange, partition
+    from paper_1301_4539_b200.slabs import HaloExchange, partition, run_steps
 
     dist = None
     if world > 1:
@@ -206,10 +206,10 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     if args.variant == "auto":
-        args.variant = "tb2" if world == 1 else "fused"
+        args.variant = "tb2"
     variant = {"fused": Y.VARIANT_FUSED, "naive": Y.VARIANT_NAIVE, "tb2": Y.VARIANT_TB2}[args.variant]
-    if world > 1 and variant != Y.VARIANT_FUSED:
-        raise SystemExit("z-slab multi-GPU runs use the one-step fused variant")
+    if world > 1 and variant == Y.VARIANT_NAIVE:
+        raise SystemExit("z-slab multi-GPU runs need a sweep variant (fused or tb2)")
 
     # z-slab decomposition (§8(e)): config 4 is strong scaling (fixed grid),
     # every other config weak scaling (each GPU keeps the config's depth).
@@ -245,13 +245,13 @@ def main():
         dist.barrier()  # the first NCCL op involves every rank (communicator init)
     exch = HaloExchange(sim, rank, world, f"cuda:{local}") if world > 1 else None
 
+    depth = sim.info()["halo_depth"]  # steps per ghost-plane exchange
+
     def advance(s_, n):
         if exch is None:
             s_.run(n, sync=False)
         else:
-            for _ in range(n):
-                exch.exchange()
-                s_.run(1, sync=False)
+            run_steps(s_, exch, n, depth)
 
     advance(sim, args.warmup)
     sim.synchronize()
@@ -320,8 +320,9 @@ def main():
         cell_arrays = {}
         if es >= 0:
             want = (Y.CB,) if ss < 0 else (Y.CA, Y.CB, Y.DA, Y.DB)
-            nzc = nz if at_top else nz + 1
-            med = Y.host_medium_slab(nx, ny, nz_global, z0, nzc, es, ss,
+            # single domain: nz cell planes; z-slab: planes z0-2 .. z0+nz+1 (yb_set_cell_coeffs)
+            zc0, nzc = (z0 - 2, nz + 4) if world > 1 else (0, nz)
+            med = Y.host_medium_slab(nx, ny, nz_global, zc0, nzc, es, ss,
                                      [pin((nzc, ny, nx)) if q in want else None for q in range(4)])
             cell_arrays = {q: med[q] for q in want}
         e_steps = cfg_steps
@@ -339,9 +340,7 @@ def main():
         if ex2 is None:
             s2.run(e_steps)
         else:
-            for _ in range(e_steps):
-                ex2.exchange()
-                s2.run(1, sync=False)
+            run_steps(s2, ex2, e_steps, depth)
         s2.download(out=host_out)
         dt = time.perf_counter() - t0
         s2.close()

@@ -80,6 +80,7 @@ typedef struct {
   int zchunk;
   double bytes_per_cell_update; /* algorithmic HBM bytes per cell-update, one sweep */
   size_t device_bytes;     /* device memory held by the handle */
+  int halo_depth;          /* z-slab mode: ghost planes refreshed per exchange = steps per exchange */
 } yb_info;
 
 /* Last error message of the calling thread ("" if none). */
@@ -120,7 +121,8 @@ int yb_host_medium(int nx, int ny, int nz, int64_t eps_seed, int64_t sigma_seed,
 int yb_host_field(int nx, int ny, int nz, uint64_t seed, int comp, float* dense);
 /* The same for the z-slab [z_offset, z_offset+nplanes) of a grid with
  * nz_global planes: `nplanes` dense planes of the component (clipped to its
- * global extent) / `nplanes` cell planes of the medium. */
+ * global extent) / `nplanes` cell planes of the medium (z_offset may be
+ * negative; planes outside the grid get clamped copies). */
 int yb_host_field_slab(int nx, int ny, int nz_global, int z_offset, int nplanes, uint64_t seed,
                        int comp, float* dense);
 int yb_host_medium_slab(int nx, int ny, int nz_global, int z_offset, int nplanes,
@@ -163,20 +165,21 @@ int yb_apply_pec_boundary(yb_sim* sim);
 /* field_digest (fields.hpp:151-166): FNV-1a-64 over the dense Ex..Hz bytes. */
 int yb_field_digest(yb_sim* sim, uint64_t* out);
 
-/* z-slab decomposition (desc.nz_global > desc.nz; FUSED variant). The slab
- * owns global cell planes [z_offset, z_offset+nz). Before each step the
- * current state's ghost planes must be refreshed from the neighbours:
- *   side 0 (bottom, rank below): send = my plane 0 of ex,ey,hx,hy,hz
- *                                (5 planes); receive -> my ghost plane -1 (hx,hy)
- *   side 1 (top, rank above):    send = my plane nz-1 of hx,hy (2 planes);
- *                                receive -> my ghost plane nz (ex,ey,hx,hy,hz)
+/* z-slab decomposition (desc.nz_global > desc.nz; FUSED or TB2 variant). The
+ * slab owns global cell planes [z_offset, z_offset+nz). Ghost planes are
+ * refreshed from the neighbours every yb_info.halo_depth = d steps (d = 1
+ * FUSED, 2 TB2): exchange, then yb_advance(sim, d).
+ *   side 0 (bottom, rank below): send my planes 0..d-1 (all six components);
+ *                                receive -> my ghosts -d (hx,hy), -d+1..-1 (all)
+ *   side 1 (top, rank above):    send my planes nz-d (hx,hy), nz-d+1..nz-1 (all);
+ *                                receive -> my ghosts nz..nz+d-1 (all)
  * Buffers are device memory of yb_halo_bytes(sim, side, 0|1) bytes
  * (0: what this side sends, 1: what it receives); plane = PX*PY floats. A
  * slab's dense field arrays are the local part of the global Array3 (node-z
  * components carry nz+1 planes; the top one belongs to the rank above unless
- * this is the global top). Per-cell coefficient uploads carry nz planes plus,
- * below the global top, the first plane of the slab above. Axis coefficient
- * cdz is the GLOBAL array (length nz_global). */
+ * this is the global top). Per-cell coefficient uploads in slab mode carry
+ * nz+4 cell planes: global planes z_offset-2 .. z_offset+nz+1 (planes outside
+ * the grid are ignored). Axis coefficient cdz is the GLOBAL array. */
 int yb_halo_bytes(yb_sim* sim, int side, int receive, size_t* bytes);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);

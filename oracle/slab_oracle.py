@@ -1,14 +1,18 @@
 """CPU ORACLE for the z-slab decomposition (test infrastructure only).
 
-A numpy restatement of one Standard step (kernels.hpp:27-63 operand order,
+A numpy restatement of the Standard step (kernels.hpp:27-63 operand order,
 PEC staggering.hpp:70-86, sources source.hpp:61-68, order schedule.hpp:171-210)
-on ONE z-slab with ghost planes, exposing the same halo interface as the CUDA
-Simulation (halo_bytes / halo_pack / halo_unpack / run). It lets the gloo
-tests run the real HaloExchange protocol across processes and compare the
-assembled result with the single-domain C oracle bit for bit.
+on ONE z-slab with `depth` ghost planes on each side, exposing the same halo
+protocol as the CUDA Simulation (halo_bytes / halo_pack / halo_unpack / run;
+include/yeeb200.h): after an exchange it may advance up to `depth` steps, each
+step updating a plane range that shrinks by one ghost plane per step (the
+ghost-zone scheme the two-step kernel uses). The gloo tests run the real
+HaloExchange across processes and compare the assembled result with the
+single-domain C oracle bit for bit.
 
-Local arrays: every component on the node box with one ghost plane below and
-one pad cell around x/y: shape (nz+2, ny+3, nx+3), index [k+1, j+1, i+1].
+Local arrays: every component on the node box with `depth` ghost planes below
+and above and one pad cell around x/y: shape (nz + 2*depth + 1, ny+3, nx+3),
+index [k + depth, j+1, i+1].
 """
 from __future__ import annotations
 
@@ -18,122 +22,129 @@ import numpy as np
 
 from oracle import pyoracle as O
 
-HALO_DOWN = (0, 1, 3, 4, 5)  # ex, ey, hx, hy, hz of plane 0 -> slab below's ghost plane nz
-HALO_UP = (3, 4)             # hx, hy of plane nz-1 -> slab above's ghost plane -1
-
 
 class OracleSlab:
-    def __init__(self, nx, ny, nz_global, z_offset, nz, medium=None, sources=()):
-        self.nx, self.ny, self.nzg, self.zoff, self.nz = nx, ny, nz_global, z_offset, nz
+    def __init__(self, nx, ny, nz_global, z_offset, nz, medium=None, sources=(), depth=1):
+        self.nx, self.ny, self.nzg, self.zoff, self.nz, self.d = nx, ny, nz_global, z_offset, nz, depth
         self.at_bot, self.at_top = z_offset == 0, z_offset + nz == nz_global
-        self.f = [np.zeros((nz + 2, ny + 3, nx + 3), np.float32) for _ in range(6)]
+        P = nz + 2 * depth + 1
+        self.f = [np.zeros((P, ny + 3, nx + 3), np.float32) for _ in range(6)]
         S = O.courant()
-        cells = None
-        if medium is not None:
-            cells = O.cell_coeffs(nx, ny, nz_global, *medium)
-        # per-position coefficients on the local node box (cell clamped, global z)
-        k = np.clip(np.arange(-1, nz + 1) + z_offset, 0, nz_global - 1)
+        k = np.clip(np.arange(-depth, nz + depth + 1) + z_offset, 0, nz_global - 1)
         j = np.clip(np.arange(-1, ny + 2), 0, ny - 1)
         i = np.clip(np.arange(-1, nx + 2), 0, nx - 1)
-        if cells is None:
+        if medium is None:
             self.ca = self.da = np.float32(1.0)
-            self.cb = self.db = None
+            self.cb = self.db = np.float32(S)
         else:
+            cells = O.cell_coeffs(nx, ny, nz_global, *medium)
             pick = np.ix_(k, j, i)
             self.ca, self.cb, self.da, self.db = (a[pick] for a in cells)
-        self.S = S
         self.sources = list(sources)  # (comp, i, j, k_global, table)
         self.step_index = 0
+        self.since_exchange = 0
 
     # -------- state in/out (global dense arrays, planes of this slab)
     def load_global(self, fields):
+        d = self.d
         for c in range(6):
             e0, e1, e2 = O.comp_extents(self.nx, self.ny, self.nzg, c)
             k0, k1 = self.zoff, min(self.zoff + self.nz + 1, e2)
-            self.f[c][1 + (k0 - self.zoff):1 + (k1 - self.zoff), 1:1 + e1, 1:1 + e0] = fields[c][k0:k1]
+            self.f[c][d + k0 - self.zoff:d + k1 - self.zoff, 1:1 + e1, 1:1 + e0] = fields[c][k0:k1]
 
     def owned(self, c):
         """(global k range, local array) this slab owns for component c."""
         e0, e1, e2 = O.comp_extents(self.nx, self.ny, self.nzg, c)
-        node_z = c in (0, 1, 5)
-        n = self.nz + (1 if node_z and self.at_top else 0)
-        return (self.zoff, self.zoff + n), self.f[c][1:1 + n, 1:1 + e1, 1:1 + e0]
+        n = self.nz + (1 if c in (0, 1, 5) and self.at_top else 0)
+        return (self.zoff, self.zoff + n), self.f[c][self.d:self.d + n, 1:1 + e1, 1:1 + e0]
 
-    # -------- halo interface (same semantics as yb_halo_*)
-    def _plane_bytes(self):
-        return (self.ny + 3) * (self.nx + 3) * 4
+    # -------- halo protocol (same plane lists as yb_halo_*, own buffer layout)
+    def _planes(self, side, pack):
+        d, nz = self.d, self.nz
+        if (side == 0) == pack:  # down-data: planes 0..d-1 (sender) / nz..nz+d-1 (receiver)
+            base = 0 if pack else nz
+            return [(c, base + q) for q in range(d) for c in range(6)]
+        base = nz - d if pack else -d  # up-data: plane base hx, hy; base+1..base+d-1 all
+        return [(3, base), (4, base)] + [(c, base + q) for q in range(1, d) for c in range(6)]
 
     def halo_bytes(self, side, receive):
-        n = len(HALO_DOWN) if (side == 0) != bool(receive) else len(HALO_UP)
-        return n * self._plane_bytes()
+        return len(self._planes(side, not receive)) * (self.ny + 3) * (self.nx + 3) * 4
 
     def halo_pack(self, side, ptr):
-        planes = [self.f[c][1] for c in HALO_DOWN] if side == 0 else \
-                 [self.f[c][self.nz] for c in HALO_UP]
-        buf = np.ascontiguousarray(np.stack(planes))
+        buf = np.ascontiguousarray(np.stack([self.f[c][self.d + k] for c, k in self._planes(side, True)]))
         C.memmove(ptr, buf.ctypes.data, buf.nbytes)
 
     def halo_unpack(self, side, ptr):
-        comps, plane = (HALO_UP, 0) if side == 0 else (HALO_DOWN, self.nz + 1)
-        n = len(comps)
-        buf = np.empty((n, self.ny + 3, self.nx + 3), np.float32)
+        pl = self._planes(side, False)
+        buf = np.empty((len(pl), self.ny + 3, self.nx + 3), np.float32)
         C.memmove(buf.ctypes.data, ptr, buf.nbytes)
-        for q, c in enumerate(comps):
-            self.f[c][plane] = buf[q]
+        for q, (c, k) in enumerate(pl):
+            self.f[c][self.d + k] = buf[q]
+        self.since_exchange = 0
 
-    # -------- one Standard step on the slab
+    # -------- steps
     def run(self, nsteps, sync=True):
         for _ in range(nsteps):
-            self._step()
+            self.since_exchange += 1
+            alone = self.at_bot and self.at_top
+            assert alone or self.since_exchange <= self.d, "ghost planes exhausted: exchange first"
+            g = max(self.d - self.since_exchange, 0)  # ghost planes still valid after this step
+            lo = 0 if self.at_bot else -g
+            self._step(lo, self.nz + (0 if self.at_top else g))
 
-    def _step(self):
-        nx, ny, nz, S = self.nx, self.ny, self.nz, self.S
+    def _step(self, lo, hi):
+        """E on local planes [lo, hi], H on [lo, hi-1] (+ hz on plane nz at the global top)."""
+        nx, ny, d = self.nx, self.ny, self.d
         ex, ey, ez, hx, hy, hz = self.f
-        K = np.arange(0, nz + 1)[:, None, None] + self.zoff  # global plane of local 0..nz
-        J = np.arange(0, ny + 1)[None, :, None]
-        I = np.arange(0, nx + 1)[None, None, :]
 
-        def v(a, dk=0, dj=0, di=0, k_hi=nz + 1):  # local k in [0, k_hi), j in [0,ny], i in [0,nx]
-            return a[1 + dk:1 + k_hi + dk, 1 + dj:ny + 2 + dj, 1 + di:nx + 2 + di]
+        def v(a, k0, k1, dk=0, dj=0, di=0):  # local planes k0..k1-1, j 0..ny, i 0..nx
+            return a[d + k0 + dk:d + k1 + dk, 1 + dj:ny + 2 + dj, 1 + di:nx + 2 + di]
 
-        def coef(a, k_hi=nz + 1):
-            return a if np.isscalar(a) or a.ndim == 0 else a[1:1 + k_hi, 1:ny + 2, 1:nx + 2]
+        def cf(a, k0, k1):
+            return a if np.ndim(a) == 0 else a[d + k0:d + k1, 1:ny + 2, 1:nx + 2]
 
-        ca = coef(self.ca)
-        cb1 = coef(self.cb) if self.cb is not None else np.float32(S)
+        def grid(k0, k1):
+            K = np.arange(k0, k1)[:, None, None] + self.zoff
+            J = np.arange(0, ny + 1)[None, :, None]
+            I = np.arange(0, nx + 1)[None, None, :]
+            return K, J, I
+
+        k0, k1 = lo, hi + 1
+        K, J, I = grid(k0, k1)
         kin = (K >= 1) & (K < self.nzg)
-        # Ampere + PEC on planes 0..nz (plane nz below the global top = the recompute)
-        e_new = [None] * 3
-        m = (I < nx) & (J >= 1) & (J < ny) & kin
-        e_new[0] = np.where(m, ca * v(ex) + (cb1 * (v(hz) - v(hz, dj=-1)) - cb1 * (v(hy) - v(hy, dk=-1))), 0)
-        m = (I >= 1) & (I < nx) & (J < ny) & kin
-        e_new[1] = np.where(m, ca * v(ey) + (cb1 * (v(hx) - v(hx, dk=-1)) - cb1 * (v(hz) - v(hz, di=-1))), 0)
-        m = (I >= 1) & (I < nx) & (J >= 1) & (J < ny) & (K < self.nzg)
-        e_new[2] = np.where(m, ca * v(ez) + (cb1 * (v(hy) - v(hy, di=-1)) - cb1 * (v(hx) - v(hx, dj=-1))), 0)
+        ca, cb = cf(self.ca, k0, k1), cf(self.cb, k0, k1)
+        new = [
+            np.where((I < nx) & (J >= 1) & (J < ny) & kin,
+                     ca * v(ex, k0, k1) + (cb * (v(hz, k0, k1) - v(hz, k0, k1, dj=-1))
+                                           - cb * (v(hy, k0, k1) - v(hy, k0, k1, dk=-1))), 0),
+            np.where((I >= 1) & (I < nx) & (J < ny) & kin,
+                     ca * v(ey, k0, k1) + (cb * (v(hx, k0, k1) - v(hx, k0, k1, dk=-1))
+                                           - cb * (v(hz, k0, k1) - v(hz, k0, k1, di=-1))), 0),
+            np.where((I >= 1) & (I < nx) & (J >= 1) & (J < ny) & (K >= 0) & (K < self.nzg),
+                     ca * v(ez, k0, k1) + (cb * (v(hy, k0, k1) - v(hy, k0, k1, di=-1))
+                                           - cb * (v(hx, k0, k1) - v(hx, k0, k1, dj=-1))), 0),
+        ]
         for c in range(3):
-            e_new[c] = e_new[c].astype(np.float32)
-            v(self.f[c])[...] = e_new[c]
+            v(self.f[c], k0, k1)[...] = new[c].astype(np.float32)
         for (sc, si, sj, sk, tab) in self.sources:
             kl = sk - self.zoff
-            if 0 <= kl <= nz and self.step_index < len(tab):
-                self.f[sc][1 + kl, 1 + sj, 1 + si] += np.float32(tab[self.step_index])
-        # Faraday on planes 0..nz-1 (hz also on plane nz at the global top)
-        da = coef(self.da, nz)
-        db1 = coef(self.db, nz) if self.db is not None else np.float32(S)
-        Kh = K[:nz]
-        m = (J < ny) & (Kh < self.nzg)
-        hx_n = np.where(m, da * v(hx, k_hi=nz) + (db1 * (v(ey, dk=1, k_hi=nz) - v(ey, k_hi=nz))
-                                                   - db1 * (v(ez, dj=1, k_hi=nz) - v(ez, k_hi=nz))), 0)
-        m = (I < nx) & (Kh < self.nzg)
-        hy_n = np.where(m, da * v(hy, k_hi=nz) + (db1 * (v(ez, di=1, k_hi=nz) - v(ez, k_hi=nz))
-                                                   - db1 * (v(ex, dk=1, k_hi=nz) - v(ex, k_hi=nz))), 0)
-        nzh = nz + 1 if self.at_top else nz
-        da2 = coef(self.da, nzh)
-        db2 = coef(self.db, nzh) if self.db is not None else np.float32(S)
-        m = (I < nx) & (J < ny)
-        hz_n = np.where(m, da2 * v(hz, k_hi=nzh) + (db2 * (v(ex, dj=1, k_hi=nzh) - v(ex, k_hi=nzh))
-                                                     - db2 * (v(ey, di=1, k_hi=nzh) - v(ey, k_hi=nzh))), 0)
-        v(hx, k_hi=nz)[...] = hx_n.astype(np.float32)
-        v(hy, k_hi=nz)[...] = hy_n.astype(np.float32)
-        v(hz, k_hi=nzh)[...] = hz_n.astype(np.float32)
+            if k0 <= kl < k1 and self.step_index < len(tab):
+                self.f[sc][d + kl, 1 + sj, 1 + si] += np.float32(tab[self.step_index])
+        # Faraday: hx, hy on [lo, hi-1]; hz on [lo, hi-1] (+ plane nz at the global top)
+        K, J, I = grid(k0, hi)
+        da, db = cf(self.da, k0, hi), cf(self.db, k0, hi)
+        kzl = K < self.nzg
+        hxn = np.where((J < ny) & kzl, da * v(hx, k0, hi) + (db * (v(ey, k0, hi, dk=1) - v(ey, k0, hi))
+                                                             - db * (v(ez, k0, hi, dj=1) - v(ez, k0, hi))), 0)
+        hyn = np.where((I < nx) & kzl, da * v(hy, k0, hi) + (db * (v(ez, k0, hi, di=1) - v(ez, k0, hi))
+                                                             - db * (v(ex, k0, hi, dk=1) - v(ex, k0, hi))), 0)
+        hz_hi = hi + 1 if self.at_top else hi
+        K2, J2, I2 = grid(k0, hz_hi)
+        da2, db2 = cf(self.da, k0, hz_hi), cf(self.db, k0, hz_hi)
+        hzn = np.where((I2 < nx) & (J2 < ny), da2 * v(hz, k0, hz_hi)
+                       + (db2 * (v(ex, k0, hz_hi, dj=1) - v(ex, k0, hz_hi))
+                          - db2 * (v(ey, k0, hz_hi, di=1) - v(ey, k0, hz_hi))), 0)
+        v(hx, k0, hi)[...] = hxn.astype(np.float32)
+        v(hy, k0, hi)[...] = hyn.astype(np.float32)
+        v(hz, k0, hz_hi)[...] = hzn.astype(np.float32)
         self.step_index += 1

@@ -65,7 +65,8 @@ class Info(C.Structure):
                 ("main_kernel_ms", C.c_double), ("main_kernel_timed", C.c_int64),
                 ("n_cell_arrays", C.c_int), ("variant", C.c_int), ("stages", C.c_int),
                 ("grid_x", C.c_int), ("grid_y", C.c_int), ("grid_z", C.c_int), ("zchunk", C.c_int),
-                ("bytes_per_cell_update", C.c_double), ("device_bytes", C.c_size_t)]
+                ("bytes_per_cell_update", C.c_double), ("device_bytes", C.c_size_t),
+                ("halo_depth", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -203,8 +204,8 @@ class Simulation:
             _check(lib().yb_set_cell_coeffs(self._h, which, None, uniform))
         else:
             cells = _f32c(cells)
-            at_top = self.z_offset + self.nz == self.nz_global
-            assert cells.size == self.nx * self.ny * (self.nz + (0 if at_top else 1))
+            slab = self.nz_global != self.nz  # z-slab: nz + 4 cell planes from z_offset - 2
+            assert cells.size == self.nx * self.ny * (self.nz + (4 if slab else 0))
             _check(lib().yb_set_cell_coeffs(self._h, which, _fp(cells), uniform))
 
     def generate_medium(self, eps_seed=-1, sigma_seed=-1):

@@ -131,14 +131,15 @@ __global__ void k_fill_fields(Geo g, Fields F, uint64_t seed) {
   }
 }
 
-// Pinned medium over the node box with clamped cell index.
+// Pinned medium over the node box and the ghost planes (local planes
+// -kGhost..nz+1) with the clamped GLOBAL cell index.
 __global__ void k_medium(Geo g, float* ca, float* cb, float* da, float* db, long long eps_seed,
                          long long sigma_seed, float S) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
-  const int k = blockIdx.z;
+  const int k = (int)blockIdx.z - kGhost;
   if (i > g.nx) return;
-  const int ci = min(i, g.nx - 1), cj = min(j, g.ny - 1), ck = min(k + g.zoff, g.nzg - 1);
+  const int ci = min(i, g.nx - 1), cj = min(j, g.ny - 1), ck = max(0, min(k + g.zoff, g.nzg - 1));
   const uint64_t cell = ((uint64_t)ck * g.ny + cj) * g.nx + ci;
   const yb_cell_coeffs q = yb_cell_coeffs_at(eps_seed, sigma_seed, cell, S);
   const long long p = gidx(g, i, j, k);
@@ -148,15 +149,15 @@ __global__ void k_medium(Geo g, float* ca, float* cb, float* da, float* db, long
   if (db) db[p] = q.db;
 }
 
-// After a dense upload into [0,nx)x[0,ny)x[0,kmax]: fill the clamped
-// duplicates at i=nx, j=ny and planes k > kmax.
-__global__ void k_clamp_fill(Geo g, float* a, int kmax) {
+// After a dense upload of cell planes kmin..kmax into [0,nx)x[0,ny): fill the
+// clamped duplicates at i=nx, j=ny and on the other planes of -kGhost..nz+1.
+__global__ void k_clamp_fill(Geo g, float* a, int kmin, int kmax) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
-  const int k = blockIdx.z;
+  const int k = (int)blockIdx.z - kGhost;
   if (i > g.nx) return;
-  if (i < g.nx && j < g.ny && k <= kmax) return;
-  a[gidx(g, i, j, k)] = a[gidx(g, min(i, g.nx - 1), min(j, g.ny - 1), min(k, kmax))];
+  if (i < g.nx && j < g.ny && k >= kmin && k <= kmax) return;
+  a[gidx(g, i, j, k)] = a[gidx(g, min(i, g.nx - 1), min(j, g.ny - 1), max(kmin, min(k, kmax)))];
 }
 
 // Dense (reference Array3 layout, extents e0 x e1 x e2) <-> padded node box.
@@ -189,6 +190,10 @@ __global__ void k_all_equal(const float* __restrict__ a, long long n, int* flag)
 }
 
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + 1 + bx - 1) / bx, g.ny + 1, g.nz + 1); }
+// node box plus the ghost planes: local planes -kGhost..nz+1
+dim3 ghost_grid(const Geo& g, int bx) {
+  return dim3((g.nx + 1 + bx - 1) / bx, g.ny + 1, g.nz + 2 + kGhost);
+}
 
 }  // namespace
 
@@ -233,7 +238,7 @@ cudaError_t launch_fill_fields(const Geo& g, const Fields& F, uint64_t seed, cud
 
 cudaError_t launch_medium(const Geo& g, float* ca, float* cb, float* da, float* db,
                           long long eps_seed, long long sigma_seed, float S, cudaStream_t st) {
-  k_medium<<<node_grid(g, 128), 128, 0, st>>>(g, ca, cb, da, db, eps_seed, sigma_seed, S);
+  k_medium<<<ghost_grid(g, 128), 128, 0, st>>>(g, ca, cb, da, db, eps_seed, sigma_seed, S);
   return cudaGetLastError();
 }
 
@@ -256,8 +261,8 @@ cudaError_t launch_all_equal(const float* a, long long n, int* flag, int num_sms
   return cudaGetLastError();
 }
 
-cudaError_t launch_clamp_fill(const Geo& g, float* a, int kmax, cudaStream_t st) {
-  k_clamp_fill<<<node_grid(g, 128), 128, 0, st>>>(g, a, kmax);
+cudaError_t launch_clamp_fill(const Geo& g, float* a, int kmin, int kmax, cudaStream_t st) {
+  k_clamp_fill<<<ghost_grid(g, 128), 128, 0, st>>>(g, a, kmin, kmax);
   return cudaGetLastError();
 }
 

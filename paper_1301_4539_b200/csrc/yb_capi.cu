@@ -132,11 +132,18 @@ int upload_axis(yb_sim* s) {
     const float uv = side == 0 ? s->cb_u : s->db_u;
     for (int a = 0; a < 3; ++a) {
       std::vector<float> h(s->axis_len[a], 0.0f);
-      // x, y: full arrays; z: local planes 0..nz of the global array (plane
-      // nz is the ghost plane's value below the global top)
-      const int off = a == 2 ? s->g.zoff : 0;
-      const int n = (int)s->axis_ref[a].size() - off;
-      for (int q = 0; q < n && q < s->axis_len[a]; ++q) h[q] = uni ? uv : s->axis_ref[a][off + q];
+      // x, y: full arrays; z: the global array's values for local planes
+      // -kGhost..nz+1 (element q + kGhost holds local plane q; ghost planes
+      // outside the global grid stay 0 and are never read)
+      if (a < 2) {
+        for (size_t q = 0; q < s->axis_ref[a].size(); ++q) h[q] = uni ? uv : s->axis_ref[a][q];
+      } else {
+        const int nzg = (int)s->axis_ref[2].size();
+        for (int q = -yb::kGhost; q <= s->g.nz + 1; ++q) {
+          const int kg = s->g.zoff + q;
+          if (kg >= 0 && kg < nzg) h[q + yb::kGhost] = uni ? uv : s->axis_ref[2][kg];
+        }
+      }
       YB_CU(cudaMemcpyAsync(s->axis_dev[side * 3 + a], h.data(), h.size() * sizeof(float),
                             cudaMemcpyHostToDevice, s->stream));
     }
@@ -152,10 +159,10 @@ yb::CoefArgs coef_args(const yb_sim* s) {
   c.da_s = s->da_s;
   c.cdx_e = s->axis_dev[0];
   c.cdy_e = s->axis_dev[1];
-  c.cdz_e = s->axis_dev[2];
+  c.cdz_e = s->axis_dev[2] + yb::kGhost;  // indexable at local planes -kGhost..nz+1
   c.cdx_h = s->axis_dev[3];
   c.cdy_h = s->axis_dev[4];
-  c.cdz_h = s->axis_dev[5];
+  c.cdz_h = s->axis_dev[5] + yb::kGhost;
   return c;
 }
 
@@ -168,15 +175,15 @@ yb::Fields fields_of(const yb_sim* s, int b) {
 int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-  // z coordinate = local plane + 1: the allocation starts at ghost plane -1
-  const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ + 1};
+  // z coordinate = local plane + kGhost: the allocation starts at ghost plane -kGhost
+  const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ + yb::kGhost + 1};
   const cuuint64_t strides[2] = {(cuuint64_t)g.PX * 4, (cuuint64_t)g.plane * 4};
   const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   // YB_L2PROMO=0..3 (tuning knob): none / 64B / 128B / 256B L2 promotion
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (const char* e = std::getenv("YB_L2PROMO")) promo = (CUtensorMapL2promotion)std::atoi(e);
-  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base - g.plane, dims, strides, box, estr,
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base - yb::kGhost * g.plane, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -439,7 +446,7 @@ int copy_dense(yb_sim* s, int comp, float* dev, const float* hsrc, float* hdst) 
     YB_CU(yb::launch_gather_dense(s->g, e, dev, stage, s->stream));
     YB_CU(cudaMemcpyAsync(hdst, stage, n * 4, cudaMemcpyDeviceToHost, s->stream));
   }
-  YB_CU(cudaMemsetAsync(stage - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
+  YB_CU(cudaMemsetAsync(stage - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
@@ -473,8 +480,10 @@ int yb_create(const yb_desc* d, yb_sim** out) {
                 d->z_offset, d->z_offset + d->nz, d->nz_global);
   if (d->nz_global <= 0 && d->z_offset != 0)
     return fail(YB_INVALID_ARGUMENT, "z_offset needs nz_global");
-  if (d->nz_global > 0 && d->nz_global != d->nz && d->variant != YB_VARIANT_FUSED)
-    return fail(YB_INVALID_ARGUMENT, "z-slab mode needs the fused (one-step) variant");
+  if (d->nz_global > 0 && d->nz_global != d->nz && d->variant == YB_VARIANT_NAIVE)
+    return fail(YB_INVALID_ARGUMENT, "z-slab mode needs a sweep variant (FUSED or TB2)");
+  if (d->nz_global > 0 && d->nz_global != d->nz && d->nz < 2)
+    return fail(YB_INVALID_ARGUMENT, "z-slabs need at least 2 planes each");
   YB_CU(cudaSetDevice(d->device));
   yb_sim* s = new yb_sim;
   s->device = d->device;
@@ -491,7 +500,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   g.PY = d->ny + 1;
   g.PZ = d->nz + 1;
   g.plane = (long long)g.PX * g.PY;
-  g.total = g.plane * (g.PZ + 3);  // ghost plane -1, planes 0..nz, 2 guard planes
+  g.total = g.plane * (g.PZ + yb::kGhost + 2);  // planes -2..nz+1 + 1 guard plane
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, d->device);
   if (dev_sms > 0) s->num_sms = dev_sms;
@@ -508,14 +517,14 @@ int yb_create(const yb_desc* d, yb_sim** out) {
       float* p = nullptr;
       if (cudaMalloc(&p, bytes) != cudaSuccess)
         return bail(fail(YB_CUDA_ERROR, "cudaMalloc of %zu bytes failed", bytes));
-      s->buf[b][c] = p + g.plane;
+      s->buf[b][c] = p + yb::kGhost * g.plane;
       s->dev_bytes += bytes;
       if (cudaMemsetAsync(p, 0, bytes, s->stream) != cudaSuccess)
         return bail(fail(YB_CUDA_ERROR, "memset failed"));
     }
   const int ns[3] = {g.nx, g.ny, g.nz};
   for (int a = 0; a < 3; ++a) {
-    s->axis_len[a] = ((ns[a] + yb::kTX) / yb::kTX + 1) * yb::kTX + 64;
+    s->axis_len[a] = ((ns[a] + yb::kTX) / yb::kTX + 1) * yb::kTX + 64 + yb::kGhost;
     s->axis_ref[a].assign(a == 2 ? g.nzg : ns[a], 0.0f);  // z: the global array
   }
   for (int q = 0; q < 6; ++q) {
@@ -546,9 +555,9 @@ int yb_destroy(yb_sim* s) {
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (int b = 0; b < 2; ++b)
     for (int c = 0; c < 6; ++c)
-      if (s->buf[b][c]) cudaFree(s->buf[b][c] - s->g.plane);
+      if (s->buf[b][c]) cudaFree(s->buf[b][c] - yb::kGhost * s->g.plane);
   for (int q = 0; q < 4; ++q)
-    if (s->cell[q]) cudaFree(s->cell[q] - s->g.plane);
+    if (s->cell[q]) cudaFree(s->cell[q] - yb::kGhost * s->g.plane);
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
   for (auto& t : s->timers) {
@@ -573,12 +582,16 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
   YB_CU(cudaSetDevice(s->device));
-  // slab mode below the global top: + the first cell plane of the slab above
-  const int nzc = yb::at_top(s->g) ? s->g.nz : s->g.nz + 1;
+  // single domain: nz cell planes. z-slab mode: nz + 2*kGhost planes, the
+  // global cell planes z_offset-kGhost .. z_offset+nz+kGhost-1 (entries of
+  // planes outside the global grid are ignored)
+  const bool slab = s->g.nzg != s->g.nz;
+  const int nzc = slab ? s->g.nz + 2 * yb::kGhost : s->g.nz;
   const long long n = (long long)s->g.nx * s->g.ny * nzc;
   bool all_equal = false;
   float v = uniform;
-  float* stage = s->buf[s->cur ^ 1][0];  // staging (see copy_dense)
+  // staging: the spare state buffer from its allocation start (see copy_dense)
+  float* stage = s->buf[s->cur ^ 1][0] - yb::kGhost * s->g.plane;
   if (cells) {
     // linear upload, then a device check of uniformity (bit patterns)
     YB_CU(cudaMemcpyAsync(stage, cells, (size_t)n * 4, cudaMemcpyHostToDevice, s->stream));
@@ -594,9 +607,9 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
   }
   s->tm_valid = false;
   if (!cells || all_equal) {
-    if (cells) YB_CU(cudaMemsetAsync(stage - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
+    if (cells) YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
     if (s->cell[which]) {
-      YB_CU(cudaFree(s->cell[which] - s->g.plane));
+      YB_CU(cudaFree(s->cell[which] - yb::kGhost * s->g.plane));
       s->cell[which] = nullptr;
       s->dev_bytes -= (size_t)s->g.total * 4;
     }
@@ -619,13 +632,15 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
     float* p = nullptr;
     YB_CU(cudaMalloc(&p, (size_t)s->g.total * 4));
     YB_CU(cudaMemsetAsync(p, 0, (size_t)s->g.total * 4, s->stream));
-    s->cell[which] = p + s->g.plane;
+    s->cell[which] = p + yb::kGhost * s->g.plane;
     s->dev_bytes += (size_t)s->g.total * 4;
   }
   const int ce[3] = {s->g.nx, s->g.ny, nzc};
-  YB_CU(yb::launch_scatter_dense(s->g, ce, stage, s->cell[which], s->stream));
-  YB_CU(yb::launch_clamp_fill(s->g, s->cell[which], nzc - 1, s->stream));
-  YB_CU(cudaMemsetAsync(stage - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
+  float* dst = slab ? s->cell[which] - yb::kGhost * s->g.plane : s->cell[which];
+  YB_CU(yb::launch_scatter_dense(s->g, ce, stage, dst, s->stream));
+  YB_CU(yb::launch_clamp_fill(s->g, s->cell[which], slab ? -yb::kGhost : 0,
+                              slab ? s->g.nz + 1 : nzc - 1, s->stream));
+  YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
@@ -640,14 +655,14 @@ int yb_generate_medium(yb_sim* s, int64_t eps_seed, int64_t sigma_seed) {
       float* p = nullptr;
       YB_CU(cudaMalloc(&p, (size_t)s->g.total * 4));
       YB_CU(cudaMemsetAsync(p, 0, (size_t)s->g.total * 4, s->stream));
-      s->cell[q] = p + s->g.plane;
+      s->cell[q] = p + yb::kGhost * s->g.plane;
       s->dev_bytes += (size_t)s->g.total * 4;
     }
     return YB_OK;
   };
   auto drop = [&](int q) -> int {
     if (s->cell[q]) {
-      YB_CU(cudaFree(s->cell[q] - s->g.plane));
+      YB_CU(cudaFree(s->cell[q] - yb::kGhost * s->g.plane));
       s->cell[q] = nullptr;
       s->dev_bytes -= (size_t)s->g.total * 4;
     }
@@ -733,12 +748,11 @@ int yb_host_field_slab(int nx, int ny, int nz_global, int z_offset, int nplanes,
 int yb_host_medium_slab(int nx, int ny, int nz_global, int z_offset, int nplanes,
                         int64_t eps_seed, int64_t sigma_seed, float* ca, float* cb, float* da,
                         float* db) {
-  if (nx < 1 || ny < 1 || nz_global < 1 || z_offset < 0 || nplanes < 0)
-    return fail(YB_INVALID_ARGUMENT, "bad argument");
+  if (nx < 1 || ny < 1 || nz_global < 1 || nplanes < 0) return fail(YB_INVALID_ARGUMENT, "bad argument");
   const float S = courant();
   const long long pl = (long long)nx * ny;
-  for (int k = 0; k < nplanes; ++k) {
-    const long long kg = std::min(z_offset + k, nz_global - 1);
+  for (int k = 0; k < nplanes; ++k) {  // cell planes outside the grid: clamped copies
+    const long long kg = std::max(0, std::min(z_offset + k, nz_global - 1));
     for (long long q = 0; q < pl; ++q) {
       const yb_cell_coeffs c = yb_cell_coeffs_at(eps_seed, sigma_seed, (uint64_t)(kg * pl + q), S);
       const long long o = k * pl + q;
@@ -769,7 +783,7 @@ int yb_zero_fields(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   YB_CU(cudaSetDevice(s->device));
   for (int c = 0; c < 6; ++c)
-    YB_CU(cudaMemsetAsync(s->buf[s->cur][c] - s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
+    YB_CU(cudaMemsetAsync(s->buf[s->cur][c] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   s->step_index = 0;
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
@@ -936,53 +950,62 @@ int yb_field_digest(yb_sim* s, uint64_t* out) {
   return YB_OK;
 }
 
-// z-slab halo planes (see include/yeeb200.h). Planes are contiguous
-// (PX*PY floats), so packing is one device-to-device copy per array.
-static const int kHaloDownComps[5] = {YB_EX, YB_EY, YB_HX, YB_HY, YB_HZ};
-static const int kHaloUpComps[2] = {YB_HX, YB_HY};
+// z-slab halo planes (see include/yeeb200.h). Depth d = 1 (one-step
+// sweeps) or 2 (two-step sweeps). Down-send: my planes 0..d-1, all six
+// components (-> the slab below's ghost planes nz..nz+d-1). Up-send: my planes
+// nz-d+1..nz-1 all six, plane nz-d hx, hy (-> the slab above's ghost planes
+// -d+1..-1 and -d). Planes are contiguous (PX*PY floats): one device copy each.
+static int halo_depth(const yb_sim* s) { return s->variant == YB_VARIANT_TB2 ? 2 : 1; }
+static int halo_planes(const yb_sim* s, bool down) {
+  const int d = halo_depth(s);
+  return down ? 6 * d : 6 * (d - 1) + 2;
+}
 
 int yb_halo_bytes(yb_sim* s, int side, int receive, size_t* bytes) {
   if (!s || !bytes || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
-  // side 0 sends 5 planes down and receives 2; side 1 sends 2 up and receives 5
-  const int planes = (side == 0) != (receive != 0) ? 5 : 2;
-  *bytes = (size_t)planes * s->g.plane * sizeof(float);
+  // side 0 sends down / receives up-data; side 1 sends up / receives down-data
+  const bool down = (side == 0) != (receive != 0);
+  *bytes = (size_t)halo_planes(s, down) * s->g.plane * sizeof(float);
+  return YB_OK;
+}
+
+static int halo_copy(yb_sim* s, int side, char* ext, bool pack) {
+  YB_CU(cudaSetDevice(s->device));
+  const size_t pb = (size_t)s->g.plane * sizeof(float);
+  const int d = halo_depth(s), nz = s->g.nz;
+  // (component, local plane) list in buffer order
+  int comp[12], plane[12], n = 0;
+  const bool down_data = (side == 0) == pack;  // planes 0.. of the slab above
+  if (down_data) {
+    const int base = pack ? 0 : nz;  // my planes 0..d-1, or my ghosts nz..nz+d-1
+    for (int q = 0; q < d; ++q)
+      for (int c = 0; c < 6; ++c) comp[n] = c, plane[n++] = base + q;
+  } else {
+    const int base = pack ? nz - d : -d;  // my planes nz-d..nz-1, or my ghosts -d..-1
+    comp[n] = YB_HX, plane[n++] = base;
+    comp[n] = YB_HY, plane[n++] = base;
+    for (int q = 1; q < d; ++q)
+      for (int c = 0; c < 6; ++c) comp[n] = c, plane[n++] = base + q;
+  }
+  for (int q = 0; q < n; ++q) {
+    float* dev = s->buf[s->cur][comp[q]] + (long long)plane[q] * s->g.plane;
+    if (pack)
+      YB_CU(cudaMemcpyAsync(ext + q * pb, dev, pb, cudaMemcpyDeviceToDevice, s->stream));
+    else
+      YB_CU(cudaMemcpyAsync(dev, ext + q * pb, pb, cudaMemcpyDeviceToDevice, s->stream));
+  }
+  YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
 
 int yb_halo_pack(yb_sim* s, int side, void* dst) {
   if (!s || !dst || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
-  YB_CU(cudaSetDevice(s->device));
-  const size_t pb = (size_t)s->g.plane * sizeof(float);
-  char* out = static_cast<char*>(dst);
-  if (side == 0) {  // my plane 0 -> the rank below's top ghost
-    for (int q = 0; q < 5; ++q)
-      YB_CU(cudaMemcpyAsync(out + q * pb, s->buf[s->cur][kHaloDownComps[q]], pb,
-                            cudaMemcpyDeviceToDevice, s->stream));
-  } else {  // my plane nz-1 (hx, hy) -> the rank above's bottom ghost
-    for (int q = 0; q < 2; ++q)
-      YB_CU(cudaMemcpyAsync(out + q * pb, s->buf[s->cur][kHaloUpComps[q]] + (s->g.nz - 1) * s->g.plane,
-                            pb, cudaMemcpyDeviceToDevice, s->stream));
-  }
-  YB_CU(cudaStreamSynchronize(s->stream));
-  return YB_OK;
+  return halo_copy(s, side, static_cast<char*>(dst), true);
 }
 
 int yb_halo_unpack(yb_sim* s, int side, const void* src) {
   if (!s || !src || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
-  YB_CU(cudaSetDevice(s->device));
-  const size_t pb = (size_t)s->g.plane * sizeof(float);
-  const char* in = static_cast<const char*>(src);
-  if (side == 0) {  // the rank below's plane nz-1 (hx, hy) -> my ghost plane -1
-    for (int q = 0; q < 2; ++q)
-      YB_CU(cudaMemcpyAsync(s->buf[s->cur][kHaloUpComps[q]] - s->g.plane, in + q * pb, pb,
-                            cudaMemcpyDeviceToDevice, s->stream));
-  } else {  // the rank above's plane 0 -> my ghost plane nz
-    for (int q = 0; q < 5; ++q)
-      YB_CU(cudaMemcpyAsync(s->buf[s->cur][kHaloDownComps[q]] + s->g.nz * s->g.plane, in + q * pb, pb,
-                            cudaMemcpyDeviceToDevice, s->stream));
-  }
-  YB_CU(cudaStreamSynchronize(s->stream));
-  return YB_OK;
+  return halo_copy(s, side, const_cast<char*>(static_cast<const char*>(src)), false);
 }
 
 int yb_set_stream(yb_sim* s, void* stream) {
@@ -1029,6 +1052,7 @@ int yb_get_info(yb_sim* s, yb_info* info) {
     info->zchunk = s->zchunk2;
   }
   info->device_bytes = s->dev_bytes;
+  info->halo_depth = halo_depth(s);
   return YB_OK;
 }
 

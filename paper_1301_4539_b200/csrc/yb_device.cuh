@@ -17,13 +17,15 @@ namespace yb {
 constexpr int kMaxSources = 8;
 
 // nz is the local slab depth; zoff/nzg place the slab in the global grid
-// (single GPU: zoff = 0, nzg = nz). Arrays carry one ghost plane below
-// local plane 0 (base pointer = allocation + one plane).
+// (single GPU: zoff = 0, nzg = nz). Arrays carry kGhost ghost planes below
+// local plane 0 (base pointer = allocation + kGhost planes) and ghost planes
+// nz (inside the node box) and nz+1 above; the two-step sweep needs both.
+constexpr int kGhost = 2;
 struct Geo {
   int nx, ny, nz;
   int PX, PY, PZ;
   long long plane;  // PX*PY
-  long long total;  // floats per allocation: ghost + PZ planes + 2 guard planes
+  long long total;  // floats per allocation: planes -2..nz+1 + 1 guard plane
   int zoff, nzg;    // global index of local plane 0, global cell count along z
 };
 

@@ -104,17 +104,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kz0 = chunk * a.zchunk;
       const int pro = (kz0 > 0 || !at_bottom(g)) ? 1 : 0;
       float* dst = stages + (size_t)s * NARR * kSlot;
-      // tensor z coordinate = local plane + 1 (ghost plane -1 is z = 0)
+      // tensor z coordinate = local plane + kGhost (ghost plane -kGhost is z = 0)
       if (pro && p_e == 0) {
         mbar_expect_tx(bar, 2 * kBoxBytes);
-        tma_load_3d(smem_u32(dst + 3 * kSlot), &tm.m[3], x0 - 4, y0 - 1, kz0, bar);
-        tma_load_3d(smem_u32(dst + 4 * kSlot), &tm.m[4], x0 - 4, y0 - 1, kz0, bar);
+        tma_load_3d(smem_u32(dst + 3 * kSlot), &tm.m[3], x0 - 4, y0 - 1, kz0 - 1 + kGhost, bar);
+        tma_load_3d(smem_u32(dst + 4 * kSlot), &tm.m[4], x0 - 4, y0 - 1, kz0 - 1 + kGhost, bar);
       } else {
         const int k = kz0 + p_e - pro;
         mbar_expect_tx(bar, NARR * kBoxBytes);
 #pragma unroll
         for (int qq = 0; qq < NARR; ++qq)
-          tma_load_3d(smem_u32(dst + qq * kSlot), &tm.m[qq], x0 - 4, y0 - 1, k + 1, bar);
+          tma_load_3d(smem_u32(dst + qq * kSlot), &tm.m[qq], x0 - 4, y0 - 1, k + kGhost, bar);
       }
       if (++p_e == p_nE) p_item = -1;
     }

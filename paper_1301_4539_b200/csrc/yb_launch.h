@@ -95,7 +95,7 @@ cudaError_t launch_faces(const Geo& g, const Fields& in, const Fields& out, cons
 cudaError_t launch_fill_fields(const Geo& g, const Fields& F, uint64_t seed, cudaStream_t st);
 cudaError_t launch_medium(const Geo& g, float* ca, float* cb, float* da, float* db,
                           long long eps_seed, long long sigma_seed, float S, cudaStream_t st);
-cudaError_t launch_clamp_fill(const Geo& g, float* a, int kmax, cudaStream_t st);
+cudaError_t launch_clamp_fill(const Geo& g, float* a, int kmin, int kmax, cudaStream_t st);
 cudaError_t launch_scatter_dense(const Geo& g, const int* e, const float* dense, float* padded,
                                  cudaStream_t st);
 cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded, float* dense,

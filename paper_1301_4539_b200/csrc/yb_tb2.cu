@@ -121,9 +121,30 @@ __device__ __forceinline__ float src_add(const SrcArgs& s, int sb, int comp, int
 }
 
 // Per-item geometry shared by the consumer paths.
+// pstart..pend: wavefront planes p; pin_end: last plane with input data;
+// up: last plane of the H1/E2 levels; pro: a prologue plane (pstart-1, hx/hy).
+// Below the global bottom / above the global top there are no planes; inside
+// a z-slab the ghost planes -2..-1 and nz..nz+1 stand in for the neighbours.
 struct Item {
-  int x0, y0, kz0, kz1, pstart, pin_end, pend;
+  int x0, y0, kz0, kz1, pstart, pin_end, pend, up;
+  bool pro;
 };
+
+__device__ __forceinline__ Item make_item(const Geo& g, int item, int T, int ntx, int zchunk) {
+  Item it;
+  const int chunk = item / T, tile = item - chunk * T;
+  it.x0 = (tile % ntx) * kTX;
+  it.y0 = (tile / ntx) * kTB2Rows;
+  it.kz0 = chunk * zchunk;
+  it.kz1 = min(it.kz0 + zchunk, g.nz);
+  const bool bot = at_bottom(g), top = at_top(g);
+  it.pstart = bot ? max(it.kz0 - 1, 0) : it.kz0 - 1;
+  it.pro = bot ? it.kz0 >= 2 : true;
+  it.pin_end = min(it.kz1 + 1, top ? g.nz - 1 : g.nz + 1);
+  it.pend = it.kz1 + 1;
+  it.up = min(it.kz1, top ? g.nz - 1 : g.nz);
+  return it;
+}
 
 // Stage layout: fields (12 rows from y0-2), then Ca, Cb (11 rows from y0-1),
 // then Da, Db (10 rows from y0-1), each present only in per-cell mode.
@@ -194,7 +215,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
   F4x3 h0p = {z4, z4, z4};
   float4 cap = z4, cbp = z4, dap = z4, dbp = z4, dap2 = z4, dbp2 = z4;
 
-  if (it.kz0 >= 2) {  // prologue: hx, hy of plane kz0-2
+  if (it.pro) {  // prologue: hx, hy of plane pstart-1
     const int s = cur.wait(B, S);
     const float* F = B.stages + (size_t)s * L::floats;
     h0p.x = lds4(F + 3 * kTB2SlotF + rs * BX + c);
@@ -244,7 +265,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
 
     // ----------------------------------------------------- L2: H1(p-1)
     const int kh = p - 1;
-    if (kh >= it.pstart && kh <= min(it.kz1, g.nz - 1) && er <= RW - 2) {
+    if (kh >= it.pstart && kh <= it.up && er <= RW - 2) {
       const int pb = kh & 1;
       const float cdz_h = co.cdz_h[kh];
       const float4 ex_h = lds4(B.E1(pb, 0, er, c)), ex_jp = lds4(B.E1(pb, 0, er + 1, c));
@@ -272,7 +293,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
 
     // ----------------------------------------------------- L3: E2(p-1)
     F4x3 e2c = {z4, z4, z4};
-    if (kh >= it.kz0 && kh <= min(it.kz1, g.nz - 1) && er >= 1 && er <= RW - 2) {
+    if (kh >= it.kz0 && kh <= it.up && er >= 1 && er <= RW - 2) {
       const int hb = kh & 1;
       const float cdz_e = co.cdz_e[kh];
       const float4 hx = lds4(B.H1(hb, 0, er, c)), hy = lds4(B.H1(hb, 1, er, c));
@@ -371,10 +392,10 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
   const int e3r = l + 1;
   const bool l3_lane = l < RW - 2;
 
-  if (it.kz0 >= 2) {  // prologue: H0 hx, hy of plane kz0-2 at the edge columns
+  if (it.pro) {  // prologue: H0 hx, hy of plane pstart-1 at the edge columns
     const int s = cur.wait(B, S);
     const float* F = B.stages + (size_t)s * L::floats;
-    const int pb = (it.kz0 - 2) & 1;
+    const int pb = (it.pstart - 1) & 1;
     *B.H0e(pb, 0, e1r, e1i) = F[3 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
     *B.H0e(pb, 1, e1r, e1i) = F[4 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
     consumer_sync();
@@ -418,7 +439,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
     consumer_sync();  // (A)
 
     const int kh = p - 1, hb = kh & 1;
-    if (l2_lane && kh >= it.pstart && kh <= min(it.kz1, g.nz - 1)) {
+    if (l2_lane && kh >= it.pstart && kh <= it.up) {
       const int r = e2r, col = ce(e2i), i = ie(e2i), j = it.y0 - 1 + r;
       const float A = DAC ? *B.De(hb, 0, r, e2i) : co.da_s;
       const float Bq = DBC ? *B.De(hb, 1, r, e2i) : 0.f;
@@ -437,7 +458,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
     }
     consumer_sync();  // (B)
 
-    if (l3_lane && kh >= it.kz0 && kh <= min(it.kz1, g.nz - 1)) {
+    if (l3_lane && kh >= it.kz0 && kh <= it.up) {
       const int r = e3r, i = ie(1), j = it.y0 - 1 + r;
       float ox, oy, oz;
       e_update1<CAC, CBC>(co, g, i, j, kh + g.zoff, co.cdy_e[max(j, 0)], co.cdz_e[kh], co.cdx_e[i],
@@ -521,21 +542,20 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         }
         p_item = it;
         p_e = 0;
-        const int kz0 = (it / T) * a.zchunk;
-        const int kz1 = min(kz0 + a.zchunk, g.nz);
-        p_nE = (kz0 >= 2 ? 1 : 0) + min(kz1 + 1, g.nz - 1) - max(kz0 - 1, 0) + 1;
+        const Item pi = make_item(g, it, T, a.ntx, a.zchunk);
+        p_nE = (pi.pro ? 1 : 0) + pi.pin_end - pi.pstart + 1;
       }
-      const int chunk = p_item / T, tile = p_item - chunk * T;
-      const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTB2Rows;
-      const int kz0 = chunk * a.zchunk;
-      const int pro = kz0 >= 2 ? 1 : 0;
+      const Item pi = make_item(g, p_item, T, a.ntx, a.zchunk);
+      const int x0 = pi.x0, y0 = pi.y0;
+      const int pro = pi.pro ? 1 : 0;
       float* dst = B.stages + (size_t)s * L::floats;
-      if (pro && p_e == 0) {  // hx, hy of plane kz0-2 (tensor z = plane + 1)
+      // tensor z coordinate = local plane + kGhost
+      if (pro && p_e == 0) {  // hx, hy of plane pstart-1
         mbar_expect_tx(bar, 2 * kBytesF);
-        tma_load_3d(smem_u32(dst + 3 * kTB2SlotF), &tm.m[3], x0 - 4, y0 - 2, kz0 - 1, bar);
-        tma_load_3d(smem_u32(dst + 4 * kTB2SlotF), &tm.m[4], x0 - 4, y0 - 2, kz0 - 1, bar);
+        tma_load_3d(smem_u32(dst + 3 * kTB2SlotF), &tm.m[3], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
+        tma_load_3d(smem_u32(dst + 4 * kTB2SlotF), &tm.m[4], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
       } else {
-        const int z = max(kz0 - 1, 0) + p_e - pro + 1;
+        const int z = pi.pstart + p_e - pro + kGhost;
         mbar_expect_tx(bar, kStageBytes);
 #pragma unroll
         for (int q2 = 0; q2 < 6; ++q2)
@@ -561,15 +581,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
     const int item = item_q[c_seq % kQ];
     ++c_seq;
     if (item < 0) break;
-    Item it;
-    const int chunk = item / T, tile = item - chunk * T;
-    it.x0 = (tile % a.ntx) * kTX;
-    it.y0 = (tile / a.ntx) * kTB2Rows;
-    it.kz0 = chunk * a.zchunk;
-    it.kz1 = min(it.kz0 + a.zchunk, g.nz);
-    it.pstart = max(it.kz0 - 1, 0);
-    it.pin_end = min(it.kz1 + 1, g.nz - 1);
-    it.pend = it.kz1 + 1;
+    const Item it = make_item(g, item, T, a.ntx, a.zchunk);
     if (w == EDGE)
       tb2_edge<CAC, CBC, DAC, DBC>(a, it, B, cur, l);
     else

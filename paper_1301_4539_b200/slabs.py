@@ -63,11 +63,15 @@ class HaloExchange:
             self.sim.halo_unpack(side, recv.data_ptr())
 
 
-def run_steps(sim, exchanger: HaloExchange, nsteps: int):
-    """Advance nsteps, refreshing ghost planes before every step."""
-    for _ in range(nsteps):
+def run_steps(sim, exchanger: HaloExchange, nsteps: int, depth: int = 1):
+    """Advance nsteps, refreshing the ghost planes every `depth` steps (the
+    sim's halo depth: 1 for one-step sweeps, 2 for two-step sweeps)."""
+    done = 0
+    while done < nsteps:
+        n = min(depth, nsteps - done)
         exchanger.exchange()
-        sim.run(1, sync=False)
+        sim.run(n, sync=False)
+        done += n
 
 
 def owned_planes(comp: int, nz_local: int, at_top: bool) -> int:

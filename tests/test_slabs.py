@@ -62,22 +62,31 @@ class DirectExchange:
             lo.halo_unpack(1, down.ctypes.data)
 
 
+def advance(exchange, slabs, steps, depth):
+    done = 0
+    while done < steps:
+        n = min(depth, steps - done)
+        exchange()
+        for s in slabs:
+            s.run(n)
+        done += n
+
+
+@pytest.mark.parametrize("depth", [1, 2])
 @pytest.mark.parametrize("nranks", [1, 2, 3, 5])
-def test_slab_oracle_matches_single_domain(oracle, nranks):
+def test_slab_oracle_matches_single_domain(oracle, nranks, depth):
+    """Ghost-zone slabs: halo depth 1 (exchange every step) and 2 (every two
+    steps, the two-step kernel's protocol)."""
     from oracle.slab_oracle import OracleSlab
     nx, ny, nzg, steps = CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"]
     tab = oracle.gauss_table(steps)
     src = (2, 6, 5, 8, tab)
     f0 = oracle.fill_fields(nx, ny, nzg, CASE["fseed"])
-    slabs = [OracleSlab(nx, ny, nzg, z0, n, medium=CASE["medium"], sources=[src])
+    slabs = [OracleSlab(nx, ny, nzg, z0, n, medium=CASE["medium"], sources=[src], depth=depth)
              for z0, n in partition(nzg, nranks)]
     for s in slabs:
         s.load_global(f0)
-    ex = DirectExchange(slabs)
-    for _ in range(steps):
-        ex.exchange()
-        for s in slabs:
-            s.run(1)
+    advance(DirectExchange(slabs).exchange, slabs, steps, depth)
     got = assemble(oracle, nx, ny, nzg, slabs)
     want = reference_run(oracle, nx, ny, nzg, steps, CASE["medium"], CASE["fseed"], src)
     for c in range(6):
@@ -90,7 +99,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _gloo_worker(rank, world, port, result_path):
+def _gloo_worker(rank, world, port, result_path, depth):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle import pyoracle as O
@@ -102,12 +111,12 @@ def _gloo_worker(rank, world, port, result_path):
     nx, ny, nzg, steps = CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"]
     z0, n = partition(nzg, world)[rank]
     tab = O.gauss_table(steps)
-    slab = OracleSlab(nx, ny, nzg, z0, n, medium=CASE["medium"], sources=[(2, 6, 5, 8, tab)])
+    slab = OracleSlab(nx, ny, nzg, z0, n, medium=CASE["medium"], sources=[(2, 6, 5, 8, tab)],
+                      depth=depth)
     slab.load_global(O.fill_fields(nx, ny, nzg, CASE["fseed"]))
     hx = HaloExchange(slab, rank, world, "cpu")
-    for _ in range(steps):
-        hx.exchange()
-        slab.run(1)
+    from paper_1301_4539_b200.slabs import run_steps
+    run_steps(slab, hx, steps, depth)
     parts = [None] * world
     dist.all_gather_object(parts, [(slab.owned(c)[0], slab.owned(c)[1].copy()) for c in range(6)])
     if rank == 0:
@@ -119,11 +128,12 @@ def _gloo_worker(rank, world, port, result_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_halo_exchange_bit_exact(oracle, tmp_path, world):
-    """HaloExchange over torch.distributed (gloo, world_size 2/3, 127.0.0.1)."""
+@pytest.mark.parametrize("world,depth", [(2, 1), (3, 1), (2, 2), (3, 2)])
+def test_gloo_halo_exchange_bit_exact(oracle, tmp_path, world, depth):
+    """HaloExchange over torch.distributed (gloo, world_size 2/3, 127.0.0.1),
+    halo depth 1 and 2."""
     path = str(tmp_path / "res.npz")
-    mp.spawn(_gloo_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    mp.spawn(_gloo_worker, args=(world, _free_port(), path, depth), nprocs=world, join=True)
     got = np.load(path)
     want = reference_run(oracle, CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"], CASE["medium"],
                          CASE["fseed"], (2, 6, 5, 8, oracle.gauss_table(CASE["steps"])))
@@ -151,26 +161,43 @@ class _DeviceExchange:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nranks,medium,fseed,src", [(2, (7, 7), 8, True), (3, (4, -1), None, True),
-                                                     (4, (-1, -1), 5, False)])
-def test_gpu_slabs_bit_exact(yb, oracle, nranks, medium, fseed, src):
+@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("nranks,medium,fseed,src,upload", [(2, (7, 7), 8, True, False),
+                                                            (3, (4, -1), None, True, False),
+                                                            (4, (-1, -1), 5, False, False),
+                                                            (3, (7, 7), 8, True, True)])
+def test_gpu_slabs_bit_exact(yb, oracle, nranks, medium, fseed, src, variant, upload):
+    """CUDA slabs (one-step fused, halo depth 1; two-step tb2, depth 2) in one
+    process on one GPU, bit-exact against a single domain. upload: per-cell
+    coefficients come from host arrays (slab layout: nz+4 cell planes)."""
     nx, ny, nzg, steps = 136, 40, 29, 11
     tab = oracle.gauss_table(steps)
     srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)] if src else []
     sims = []
     for z0, n in partition(nzg, nranks):
-        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, zchunk=4)
-        s.generate_medium(*medium)
+        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, zchunk=4, variant=variant)
+        if upload:
+            arrs = yb.host_medium_slab(nx, ny, nzg, z0 - 2, n + 4, *medium,
+                                       [np.empty((n + 4, ny, nx), np.float32) for _ in range(4)])
+            for q in range(4):
+                s.set_cell_coeffs(q, arrs[q])
+        else:
+            s.generate_medium(*medium)
         for q in srcs:
             s.add_source(*q)
         if fseed is not None:
             s.fill(fseed)
         sims.append(s)
     ex = _DeviceExchange(sims)
-    for _ in range(steps):
+    depth = sims[0].info()["halo_depth"]
+    assert depth == (2 if variant == 2 else 1)
+    done = 0
+    while done < steps:
+        n = min(depth, steps - done)
         ex.exchange()
         for s in sims:
-            s.run(1)
+            s.run(n)
+        done += n
     out = oracle.zeros_state(nx, ny, nzg)
     for s in sims:
         d = s.download()
