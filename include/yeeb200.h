@@ -146,6 +146,30 @@ int yb_get_step_index(yb_sim* sim, int64_t* step_index);
 int yb_add_source(yb_sim* sim, int comp, int i, int j, int k, const float* table, int64_t n);
 int yb_clear_sources(yb_sim* sim);
 
+/* Point probes (ProbeSpec + sample_probes, probe.hpp:14-51): after every
+ * completed step t with t % stride == 0 the probe's value is recorded on the
+ * device (no full-field readback). Positions index the component's own
+ * extents (ProbeSpec::validate). Two-step sweeps are split into single steps
+ * where a probe fires in between (the reference suspends pairing likewise,
+ * runner.hpp:279-285). Single-domain handles only. At most YB_MAX_PROBES. */
+#define YB_MAX_PROBES 64
+int yb_set_probes(yb_sim* sim, int n, const int* comp, const int* i, const int* j, const int* k,
+                  const int* stride);
+/* Moves up to `capacity` recorded samples (oldest first) to the host:
+ * step (completed steps), probe index, value; *count = number returned. */
+int yb_read_probes(yb_sim* sim, int64_t* steps, int* probe, float* values, int64_t capacity,
+                   int64_t* count);
+
+/* Leapfrog energy invariant (total_energy + HSnapshot, fields.hpp:68-146).
+ * yb_snapshot_h copies the current H (the reference's HSnapshot); after
+ * advancing, yb_total_energy returns sum_E V*E^2 + sum_H V*Hprev*Hnow with
+ * V the dual/primal cell volumes from the spacings dx[nx], dy[ny],
+ * dz[nz_global] (NULL = unit spacing), accumulated in double (deterministic;
+ * summation order differs from the reference's serial loop). On a z-slab the
+ * sum covers the planes the slab owns (sum over ranks for the total). */
+int yb_snapshot_h(yb_sim* sim);
+int yb_total_energy(yb_sim* sim, const double* dx, const double* dy, const double* dz, double* energy);
+
 /* Simulation::run(n) time loop (runner.hpp:243-266) with the Standard step
  * (schedule.hpp:171-210): advances step_index by n. Asynchronous on the
  * handle's stream. */

@@ -367,6 +367,18 @@ class Simulation {
     d.variant = opts_.variant;
     detail::check(yb_create(&d, &h_));
     detail::check(yb_set_axis_coeffs(h_, coeffs_.cdx.data(), coeffs_.cdy.data(), coeffs_.cdz.data()));
+    if (!opts_.probes.empty()) {  // sampled on the device (sample_probes, probe.hpp:36-51)
+      std::vector<int> c, i, j, k, st;
+      for (const ProbeSpec& p : opts_.probes) {
+        c.push_back(comp_index(p.component));
+        i.push_back(p.i);
+        j.push_back(p.j);
+        k.push_back(p.k);
+        st.push_back(p.stride);
+      }
+      detail::check(yb_set_probes(h_, static_cast<int>(c.size()), c.data(), i.data(), j.data(), k.data(),
+                                  st.data()));
+    }
   }
   ~Simulation() {
     if (h_) yb_destroy(h_);
@@ -407,7 +419,7 @@ class Simulation {
     std::vector<ProbeRecord> records;
     long long t = step_;
     const long long t_end = t + n_steps;
-    const bool per_step = !opts_.probes.empty() || static_cast<bool>(opts_.after_step);
+    const bool per_step = static_cast<bool>(opts_.after_step);
     while (t < t_end) {
       long long n = t_end - t;
       if (per_step) n = 1;
@@ -415,18 +427,36 @@ class Simulation {
       detail::check(yb_advance(h_, n));
       t += n;
       step_ = t;
-      if (!opts_.probes.empty()) sample(records, t);
       if (opts_.after_step) {
         have_mirror_ = false;
         sync_mirror();
         opts_.after_step(mirror_, t);
       }
     }
+    if (!opts_.probes.empty()) drain_probes(records);
     detail::check(yb_synchronize(h_));
     have_mirror_ = false;
     stats_.total_seconds += now() - t0;
     stats_.steps += n_steps;
     return records;
+  }
+
+  /// HSnapshot of the device-resident H (fields.hpp:71-82); pair with
+  /// total_energy() after advancing (the reference's measure_energy_drift
+  /// pattern, bench.hpp:273-303).
+  void snapshot_h() {
+    push_if_dirty();
+    detail::check(yb_snapshot_h(h_));
+  }
+  /// Leapfrog invariant on the device (total_energy, fields.hpp:116-146).
+  double total_energy() {
+    push_if_dirty();
+    std::vector<double> d[3];
+    for (int a = 0; a < 3; ++a)
+      for (Real v : grid_.spacing(a)) d[a].push_back(static_cast<double>(v));
+    double e = 0.0;
+    detail::check(yb_total_energy(h_, d[0].data(), d[1].data(), d[2].data(), &e));
+    return e;
   }
 
   /// The reference range ops on the device-resident state (kernels.hpp:129-155).
@@ -477,16 +507,20 @@ class Simulation {
       detail::check(yb_add_source(h_, comp_index(s.component), s.i, s.j, s.k, tab.data(), last + 1));
     }
   }
-  void sample(std::vector<ProbeRecord>& records, long long step) {
+  // Appends the device-recorded samples (step order, then probe order).
+  void drain_probes(std::vector<ProbeRecord>& records) {
     const double dt = static_cast<double>(grid_.dt);
-    for (std::size_t p = 0; p < opts_.probes.size(); ++p) {
-      const ProbeSpec& ps = opts_.probes[p];
-      if (!ps.fires_at(step)) continue;
-      if (!have_mirror_) sync_mirror();
-      const double v = static_cast<double>(mirror_.field(ps.component)(ps.i, ps.j, ps.k));
-      records.push_back({step, static_cast<double>(step) * dt, static_cast<int>(p), v});
+    constexpr long long kChunk = 1 << 16;
+    std::vector<int64_t> steps(kChunk);
+    std::vector<int> probe(kChunk);
+    std::vector<float> vals(kChunk);
+    for (;;) {
+      int64_t n = 0;
+      detail::check(yb_read_probes(h_, steps.data(), probe.data(), vals.data(), kChunk, &n));
+      for (int64_t q = 0; q < n; ++q)
+        records.push_back({steps[q], static_cast<double>(steps[q]) * dt, probe[q], static_cast<double>(vals[q])});
+      if (n < kChunk) break;
     }
-    have_mirror_ = false;
   }
 
   GridSpec<Real> grid_;

@@ -119,6 +119,8 @@ def ref():
         R.yr_source_table.restype = C.c_int64
         R.yr_digest.argtypes = [C.c_int] * 3 + [_f32p * 6]
         R.yr_digest.restype = C.c_uint64
+        R.yr_total_energy.argtypes = [C.c_int] * 3 + [_f32p] * 3 + [_f32p * 6, _f32p * 3]
+        R.yr_total_energy.restype = C.c_double
         _ref = R
     return _ref
 
@@ -305,3 +307,33 @@ def max_rel_err(a, b):
         d = float(np.max(np.abs(x.astype(np.float64) - y.astype(np.float64)))) if y.size else 0.0
         out.append(d / m if m > 0 else d)
     return out
+
+
+def total_energy(nx, ny, nz, fields, prev_h, dx=None, dy=None, dz=None):
+    """Leapfrog invariant (fields.hpp:116-146, dual_spacing :86-93, dof_volume
+    :96-105) in float64: sum_E V*E^2 + sum_H V*Hprev*Hnow. numpy summation
+    order (the reference's is a serial loop): compare with a relative tolerance."""
+    def weights(d, n):
+        d = np.ones(n) if d is None else np.asarray(d, np.float64)
+        node = np.empty(n + 1)
+        node[0], node[n] = 0.5 * d[0], 0.5 * d[n - 1]
+        node[1:n] = 0.5 * (d[:-1] + d[1:])
+        return node, d
+    W = [weights(dx, nx), weights(dy, ny), weights(dz, nz)]
+    total = 0.0
+    for c in range(6):
+        axis = c % 3
+        node = [(a != axis) if c < 3 else (a == axis) for a in range(3)]
+        wx, wy, wz = (W[a][0 if node[a] else 1] for a in range(3))
+        v = wz[:, None, None] * wy[None, :, None] * wx[None, None, :]
+        now = fields[c].astype(np.float64)
+        other = now if c < 3 else prev_h[c - 3].astype(np.float64)
+        total += float(np.sum(v * other * now))
+    return total
+
+
+def ref_total_energy(nx, ny, nz, fields, prev_h, dx=None, dy=None, dz=None):
+    ax = [np.ascontiguousarray(np.ones(n) if d is None else d, np.float32)
+          for d, n in ((dx, nx), (dy, ny), (dz, nz))]
+    ph = (_f32p * 3)(*[_p(a) for a in prev_h])
+    return float(ref().yr_total_energy(nx, ny, nz, *[_p(a) for a in ax], _fptrs(fields), ph))

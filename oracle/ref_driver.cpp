@@ -14,6 +14,7 @@
 //   yr_simulation   - yeeblock::Simulation<float>::run (runner.hpp:205-266)
 //                     for any Variant/split/worker count with a reference
 //                     SourceSpec (source.hpp:15-68).
+//   yr_total_energy - total_energy against an HSnapshot (fields.hpp:68-146).
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -197,6 +198,20 @@ std::uint64_t yr_digest(int nx, int ny, int nz, float* const* fields) {
   FieldSet<float> f(GridDims{nx, ny, nz});
   load(f, fields);
   return field_digest(f);
+}
+
+// total_energy (fields.hpp:116-146) of `fields` against an HSnapshot holding
+// prev_h[0..2] (hx, hy, hz).
+double yr_total_energy(int nx, int ny, int nz, const float* dx, const float* dy, const float* dz,
+                       float* const* fields, float* const* prev_h) {
+  const GridSpec<float> g = make_grid(nx, ny, nz, dx, dy, dz, 0.0f, 1.0f);
+  FieldSet<float> f(GridDims{nx, ny, nz}), p(GridDims{nx, ny, nz});
+  load(f, fields);
+  for (Comp c : kHComps) {
+    Array3<float>& a = p.field(c);
+    std::memcpy(a.data(), prev_h[comp_index(c) - 3], a.size_bytes());
+  }
+  return total_energy(g, f, HSnapshot<float>(p));
 }
 
 }  // extern "C"

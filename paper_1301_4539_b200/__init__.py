@@ -38,7 +38,8 @@ ABI_SYMBOLS = (
     "yb_apply_ampere_range", "yb_apply_faraday_range", "yb_apply_pec_boundary",
     "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
     "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
-    "yb_host_field_slab", "yb_host_medium_slab",
+    "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
+    "yb_snapshot_h", "yb_total_energy",
 )
 
 
@@ -120,6 +121,11 @@ def lib():
         L.yb_host_field.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _f32p]
         L.yb_host_field_slab.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_int, _f32p]
         L.yb_host_medium_slab.argtypes = [C.c_int] * 5 + [C.c_int64, C.c_int64] + [_f32p] * 4
+        L.yb_set_probes.argtypes = [vp, C.c_int] + [C.POINTER(C.c_int)] * 5
+        L.yb_read_probes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int), _f32p, C.c_int64,
+                                     C.POINTER(C.c_int64)]
+        L.yb_snapshot_h.argtypes = [vp]
+        L.yb_total_energy.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
         L.yb_halo_unpack.argtypes = [vp, C.c_int, vp]
@@ -297,6 +303,38 @@ class Simulation:
 
     def halo_unpack(self, side, src_ptr):
         _check(lib().yb_halo_unpack(self._h, side, C.c_void_p(src_ptr)))
+
+    def set_probes(self, probes):
+        """probes: [(comp, i, j, k, stride)] sampled on the device after every
+        completed step t with t % stride == 0 (probe.hpp:14-51)."""
+        n = len(probes)
+        cols = [np.ascontiguousarray([p[q] for p in probes], dtype=np.int32) for q in range(5)]
+        ptr = [c.ctypes.data_as(C.POINTER(C.c_int)) for c in cols]
+        _check(lib().yb_set_probes(self._h, n, *ptr))
+
+    def read_probes(self, capacity=1 << 20):
+        """Drains recorded samples: (steps int64, probe int32, values float32)."""
+        st = np.empty(capacity, np.int64)
+        pr = np.empty(capacity, np.int32)
+        va = np.empty(capacity, np.float32)
+        n = C.c_int64()
+        _check(lib().yb_read_probes(self._h, st.ctypes.data_as(C.POINTER(C.c_int64)),
+                                    pr.ctypes.data_as(C.POINTER(C.c_int)), _fp(va), capacity, C.byref(n)))
+        k = n.value
+        return st[:k].copy(), pr[:k].copy(), va[:k].copy()
+
+    def snapshot_h(self):
+        """HSnapshot of the current H on the device (fields.hpp:71-82)."""
+        _check(lib().yb_snapshot_h(self._h))
+
+    def total_energy(self, dx=None, dy=None, dz=None):
+        """Leapfrog invariant against the last snapshot (fields.hpp:116-146);
+        spacings default to 1 (dz has nz_global entries)."""
+        arrs = [None if d is None else np.ascontiguousarray(d, np.float64) for d in (dx, dy, dz)]
+        ptr = [None if a is None else a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs]
+        out = C.c_double()
+        _check(lib().yb_total_energy(self._h, *ptr, C.byref(out)))
+        return out.value
 
     def set_kernel_timing(self, on):
         _check(lib().yb_set_kernel_timing(self._h, 1 if on else 0))

@@ -189,6 +189,59 @@ __global__ void k_all_equal(const float* __restrict__ a, long long n, int* flag)
   if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0) atomicExch(flag, 0);
 }
 
+// Point probes: out[q] = field[comp[q]][off[q]] (sample_probes, probe.hpp:36-51).
+__global__ void k_probes(Fields F, ProbeArgs pa, float* out) {
+  const int q = threadIdx.x;
+  if (q < pa.n) out[q] = F.f[pa.comp[q]][pa.off[q]];
+}
+
+// Leapfrog invariant (total_energy, fields.hpp:116-146): per-(component,
+// block) partial sums in double with a fixed tree, then one fixed-order sum.
+// dof volume = ((1 * w_x) * w_y) * w_z as in dof_volume (fields.hpp:96-105);
+// a term is (V * e) * e for E and (V * prev) * now for H.
+__global__ void __launch_bounds__(256) k_energy(Geo g, Fields F, const float* p0, const float* p1,
+                                                const float* p2, const double* w, double* partial) {
+  const int c = blockIdx.y;
+  const bool top = at_top(g);
+  const int planes = (c == 0 || c == 1 || c == 5) ? g.nz + (top ? 1 : 0) : g.nz;  // owned planes
+  const double* wn[3] = {w, w + 2 * g.nx + 1, w + 2 * g.nx + 2 * g.ny + 2};
+  const double* wc[3] = {w + g.nx + 1, w + 2 * g.nx + g.ny + 2, w + 2 * g.nx + 2 * g.ny + 2 + g.nz + 1};
+  const bool node[3] = {c < 3 ? c != 0 : c == 3, c < 3 ? c != 1 : c == 4, c < 3 ? c != 2 : c == 5};
+  const int e[3] = {g.nx + node[0], g.ny + node[1], g.nz + node[2]};
+  const double* wx = node[0] ? wn[0] : wc[0];
+  const double* wy = node[1] ? wn[1] : wc[1];
+  const double* wz = node[2] ? wn[2] : wc[2];
+  const float* a = F.f[c];
+  const float* pv = c == 3 ? p0 : (c == 4 ? p1 : p2);
+  double acc = 0.0;
+  const long long rows = (long long)planes * e[1];
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int k = (int)(r / e[1]), j = (int)(r % e[1]);
+    const double vyz_y = wy[j], vz = wz[k];
+    const long long base = ((long long)k * g.PY + j) * g.PX;
+    for (int i = threadIdx.x; i < e[0]; i += blockDim.x) {
+      const double v = __dmul_rn(__dmul_rn(__dmul_rn(1.0, wx[i]), vyz_y), vz);
+      const double now = (double)a[base + i];
+      const double t = c < 3 ? __dmul_rn(__dmul_rn(v, now), now) : __dmul_rn(__dmul_rn(v, (double)pv[base + i]), now);
+      acc = __dadd_rn(acc, t);
+    }
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + h]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[c * gridDim.x + blockIdx.x] = red[0];
+}
+
+__global__ void k_energy_final(const double* partial, int n, double* out) {
+  double s = 0.0;
+  for (int q = 0; q < n; ++q) s = __dadd_rn(s, partial[q]);
+  *out = s;
+}
+
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + 1 + bx - 1) / bx, g.ny + 1, g.nz + 1); }
 // node box plus the ghost planes: local planes -kGhost..nz+1
 dim3 ghost_grid(const Geo& g, int bx) {
@@ -253,6 +306,18 @@ cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded,
                                 cudaStream_t st) {
   k_gather_dense<<<dim3((e[0] + 127) / 128, e[1], e[2]), 128, 0, st>>>(g, e[0], e[1], e[2], padded,
                                                                        dense);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probes(const Fields& F, const ProbeArgs& pa, float* out, cudaStream_t st) {
+  k_probes<<<1, 64, 0, st>>>(F, pa, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_energy(const Geo& g, const Fields& F, const float* const* prev_h, const double* w,
+                          double* partial, double* out, cudaStream_t st) {
+  k_energy<<<dim3(kEnergyBlocks, 6), 256, 0, st>>>(g, F, prev_h[0], prev_h[1], prev_h[2], w, partial);
+  k_energy_final<<<1, 1, 0, st>>>(partial, 6 * kEnergyBlocks, out);
   return cudaGetLastError();
 }
 

@@ -63,6 +63,10 @@ struct Src {
   std::vector<float> table;
 };
 
+struct Probe {
+  int comp, i, j, k, stride;
+};
+
 struct TimerPair {
   cudaEvent_t a, b;
 };
@@ -112,6 +116,13 @@ struct yb_sim {
   dim3 grid2{1, 1, 1};
   unsigned long long* sched = nullptr;  // device work counter of the fused kernel
   unsigned long long sched_base = 0;
+  std::vector<Probe> probes;
+  float* probe_dev = nullptr;  // recorded values (device)
+  size_t probe_cap = 0;        // capacity of probe_dev (floats)
+  std::vector<std::pair<int64_t, int>> probe_meta;  // (step, probe) per recorded value
+  float* snap_h[3] = {};        // HSnapshot (planes 0..nz of hx, hy, hz)
+  bool have_snap = false;
+  double* energy_dev = nullptr;  // weights | partials | result
   int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
 };
 
@@ -560,6 +571,9 @@ int yb_destroy(yb_sim* s) {
     if (s->cell[q]) cudaFree(s->cell[q] - yb::kGhost * s->g.plane);
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
+  cudaFree(s->probe_dev);
+  for (float* p : s->snap_h) cudaFree(p);
+  cudaFree(s->energy_dev);
   for (auto& t : s->timers) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -835,25 +849,157 @@ int yb_clear_sources(yb_sim* s) {
   return YB_OK;
 }
 
+static bool probe_fires(const yb_sim* s, int64_t step) {
+  for (const Probe& p : s->probes)
+    if (step % p.stride == 0) return true;
+  return false;
+}
+
+// Records every probe firing at the current step_index (on the device).
+static int sample_probes_dev(yb_sim* s) {
+  yb::ProbeArgs pa{};
+  for (size_t q = 0; q < s->probes.size(); ++q) {
+    const Probe& p = s->probes[q];
+    if (s->step_index % p.stride) continue;
+    pa.comp[pa.n] = p.comp;
+    pa.off[pa.n] = ((long long)p.k * s->g.PY + p.j) * s->g.PX + p.i;
+    ++pa.n;
+    s->probe_meta.push_back({s->step_index, (int)q});
+  }
+  if (!pa.n) return YB_OK;
+  const size_t need = s->probe_meta.size();
+  if (need > s->probe_cap) {  // grow (rare): copy the recorded values over
+    size_t cap = std::max<size_t>(1024, 2 * s->probe_cap);
+    while (cap < need) cap *= 2;
+    float* nb = nullptr;
+    YB_CU(cudaMalloc(&nb, cap * sizeof(float)));
+    if (s->probe_dev) {
+      YB_CU(cudaMemcpyAsync(nb, s->probe_dev, (need - pa.n) * sizeof(float), cudaMemcpyDeviceToDevice,
+                            s->stream));
+      YB_CU(cudaStreamSynchronize(s->stream));
+      YB_CU(cudaFree(s->probe_dev));
+    }
+    s->probe_dev = nb;
+    s->probe_cap = cap;
+  }
+  YB_CU(yb::launch_probes(fields_of(s, s->cur), pa, s->probe_dev + (need - pa.n), s->stream));
+  s->launches += 1;
+  return YB_OK;
+}
+
 int yb_advance(yb_sim* s, int64_t nsteps) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
   YB_CU(cudaSetDevice(s->device));
   if (s->variant != YB_VARIANT_NAIVE)
     if (int rc = prepare_fused(s)) return rc;
-  int64_t t = 0;
-  if (s->variant == YB_VARIANT_TB2)
-    for (; t + 2 <= nsteps; t += 2) {
+  const bool probes = !s->probes.empty();
+  for (int64_t t = 0; t < nsteps;) {
+    // two steps per launch unless a probe wants the level in between
+    if (s->variant == YB_VARIANT_TB2 && t + 2 <= nsteps && !(probes && probe_fires(s, s->step_index + 1))) {
       if (int rc = step_tb2(s)) return rc;
       s->step_index += 2;
       s->steps += 2;
+      t += 2;
+    } else {
+      const int rc = s->variant == YB_VARIANT_NAIVE ? step_naive(s) : step_fused(s);
+      if (rc) return rc;
+      ++s->step_index;
+      ++s->steps;
+      ++t;
     }
-  for (; t < nsteps; ++t) {
-    const int rc = s->variant == YB_VARIANT_NAIVE ? step_naive(s) : step_fused(s);
-    if (rc) return rc;
-    ++s->step_index;
-    ++s->steps;
+    if (probes && probe_fires(s, s->step_index))
+      if (int rc = sample_probes_dev(s)) return rc;
   }
+  return YB_OK;
+}
+
+int yb_snapshot_h(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  YB_CU(cudaSetDevice(s->device));
+  const size_t n = (size_t)s->g.plane * (s->g.nz + 1);
+  for (int c = 0; c < 3; ++c) {
+    if (!s->snap_h[c]) {
+      YB_CU(cudaMalloc(&s->snap_h[c], n * sizeof(float)));
+      s->dev_bytes += n * sizeof(float);
+    }
+    YB_CU(cudaMemcpyAsync(s->snap_h[c], s->buf[s->cur][3 + c], n * sizeof(float), cudaMemcpyDeviceToDevice,
+                          s->stream));
+  }
+  s->have_snap = true;
+  return YB_OK;
+}
+
+int yb_total_energy(yb_sim* s, const double* dx, const double* dy, const double* dz, double* energy) {
+  if (!s || !energy) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (!s->have_snap) return fail(YB_INVALID_ARGUMENT, "total_energy: no H snapshot (call yb_snapshot_h first)");
+  YB_CU(cudaSetDevice(s->device));
+  const Geo& g = s->g;
+  // dual spacing at node i: half-sum of the adjacent cells, halved at the ends
+  // (dual_spacing, fields.hpp:86-93); primal spacing at cell i: d[i].
+  std::vector<double> w;
+  auto axis = [&](const double* d, int n, int off, int nglob, int count) {
+    auto at = [&](int q) { return d ? d[q] : 1.0; };
+    for (int q = off; q <= off + count; ++q)
+      w.push_back(q == 0 ? 0.5 * at(0) : (q == nglob ? 0.5 * at(nglob - 1) : 0.5 * (at(q - 1) + at(q))));
+    for (int q = off; q < off + count; ++q) w.push_back(at(q));
+  };
+  axis(dx, g.nx, 0, g.nx, g.nx);
+  axis(dy, g.ny, 0, g.ny, g.ny);
+  axis(dz, g.nzg, g.zoff, g.nzg, g.nz);
+  const size_t nw = w.size(), np = 6 * yb::kEnergyBlocks;
+  if (!s->energy_dev) YB_CU(cudaMalloc(&s->energy_dev, (nw + np + 1) * sizeof(double)));
+  double* wd = s->energy_dev;
+  YB_CU(cudaMemcpyAsync(wd, w.data(), nw * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  const float* prev[3] = {s->snap_h[0], s->snap_h[1], s->snap_h[2]};
+  YB_CU(yb::launch_energy(g, fields_of(s, s->cur), prev, wd, wd + nw, wd + nw + np, s->stream));
+  s->launches += 2;
+  YB_CU(cudaMemcpyAsync(energy, wd + nw + np, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_set_probes(yb_sim* s, int n, const int* comp, const int* i, const int* j, const int* k,
+                  const int* stride) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (n < 0 || n > YB_MAX_PROBES) return fail(YB_INVALID_ARGUMENT, "at most %d probes", YB_MAX_PROBES);
+  if (n > 0 && (!comp || !i || !j || !k || !stride)) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (n > 0 && s->g.nzg != s->g.nz) return fail(YB_INVALID_ARGUMENT, "probes: single-domain handles only");
+  std::vector<Probe> ps;
+  for (int q = 0; q < n; ++q) {  // ProbeSpec::validate (probe.hpp:21-25)
+    if (stride[q] < 1) return fail(YB_INVALID_ARGUMENT, "ProbeSpec: stride must be >= 1");
+    if (int rc = check_comp(comp[q])) return rc;
+    int e[3];
+    comp_ext(s->g, comp[q], e);
+    if (i[q] < 0 || i[q] >= e[0] || j[q] < 0 || j[q] >= e[1] || k[q] < 0 || k[q] >= e[2])
+      return fail(YB_INVALID_ARGUMENT, "ProbeSpec: position outside grid");
+    ps.push_back({comp[q], i[q], j[q], k[q], stride[q]});
+  }
+  s->probes = ps;
+  return YB_OK;
+}
+
+int yb_read_probes(yb_sim* s, int64_t* steps, int* probe, float* values, int64_t capacity,
+                   int64_t* count) {
+  if (!s || !count || capacity < 0) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  const int64_t n = std::min<int64_t>(capacity, (int64_t)s->probe_meta.size());
+  *count = n;
+  if (n == 0) return YB_OK;
+  if (!steps || !probe || !values) return fail(YB_INVALID_ARGUMENT, "null argument");
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(cudaMemcpyAsync(values, s->probe_dev, n * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  for (int64_t q = 0; q < n; ++q) {
+    steps[q] = s->probe_meta[q].first;
+    probe[q] = s->probe_meta[q].second;
+  }
+  const int64_t rest = (int64_t)s->probe_meta.size() - n;
+  if (rest > 0) {  // keep the unread tail at the front
+    YB_CU(cudaMemcpyAsync(s->probe_dev, s->probe_dev + n, rest * sizeof(float), cudaMemcpyDeviceToDevice,
+                          s->stream));
+    YB_CU(cudaStreamSynchronize(s->stream));
+  }
+  s->probe_meta.erase(s->probe_meta.begin(), s->probe_meta.begin() + n);
   return YB_OK;
 }
 

@@ -100,6 +100,17 @@ cudaError_t launch_scatter_dense(const Geo& g, const int* e, const float* dense,
                                  cudaStream_t st);
 cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded, float* dense,
                                 cudaStream_t st);
+struct ProbeArgs {
+  int n;
+  int comp[64];
+  long long off[64];
+};
+cudaError_t launch_probes(const Fields& F, const ProbeArgs& pa, float* out, cudaStream_t st);
+// weights: x node[nx+1], x cell[nx], y node[ny+1], y cell[ny], z node[nz+1], z cell[nz]
+// (local planes); partial: 6*nblk doubles; out: 1 double
+constexpr int kEnergyBlocks = 296;
+cudaError_t launch_energy(const Geo& g, const Fields& F, const float* const* prev_h, const double* w,
+                          double* partial, double* out, cudaStream_t st);
 cudaError_t launch_all_equal(const float* a, long long n, int* flag, int num_sms, cudaStream_t st);
 
 }  // namespace yb

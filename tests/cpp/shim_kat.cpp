@@ -193,6 +193,20 @@ int main() {
     CHECK(a.step_index == 5 && b.step_index == 5);
     CHECK(field_digest_hex(a) == field_digest_hex(b));
   }
+  // kernel_test.cpp:265-283 total_energy KATs, on the device
+  {
+    auto g = unit_grid(4, 0.5f);
+    Simulation<float> sim(g);
+    sim.snapshot_h();
+    CHECK(sim.total_energy() == 0.0);
+    sim.fields().ez(2, 2, 1) = 2.0f;
+    CHECK(sim.total_energy() == 4.0);
+    sim.fields().zero();
+    sim.fields().hx(2, 1, 1) = 3.0f;
+    sim.snapshot_h();
+    sim.fields().hx(2, 1, 1) = 0.5f;
+    CHECK(sim.total_energy() == 1.5);
+  }
   if (failures) {
     std::fprintf(stderr, "%d failure(s)\n", failures);
     return 1;

@@ -19,6 +19,11 @@ Cases (all fp32, Standard step order, schedule.hpp:171-210):
               (kernel_test.cpp:84-106).
   kat_faraday 4^3, c*dt/h = 0.5, ey(1,1,2)=1 then ez(1,2,1)=1, Faraday only
               (kernel_test.cpp:108-130).
+  energy      total_energy (fields.hpp:116-146): (a) 13x11x9 stretched
+              spacing, seeded E/H and a seeded H snapshot -> one value;
+              (b) 20^3 unit grid, Gaussian Ez source for 30 steps then free,
+              the leapfrog invariant after each of 60 single steps (the
+              measure_energy_drift pattern, bench.hpp:273-303).
 """
 import os
 import sys
@@ -99,6 +104,27 @@ def main():
     g[2][1, 2, 1] = 1.0  # ez(1,2,1)
     O.ref_run_kernels(n, n, n, g, 1, dx=ones, dy=ones, dz=ones, dt=0.5, phases=4)
     save("kat_faraday", dims=np.array([n, n, n]), **fields_dict("ey", f), **fields_dict("ez", g))
+
+    # energy
+    nx, ny, nz = 13, 11, 9
+    dx = np.linspace(0.7, 1.4, nx).astype(np.float32)
+    dy = np.linspace(1.2, 0.6, ny).astype(np.float32)
+    dz = np.linspace(0.9, 1.1, nz).astype(np.float32)
+    f = O.fill_fields(nx, ny, nz, 31)
+    prev = O.fill_fields(nx, ny, nz, 32)[3:]
+    e_static = O.ref_total_energy(nx, ny, nz, f, prev, dx, dy, dz)
+    n, steps = 20, 60
+    tab = O.gauss_table(30, t0=12.0, w=4.0)
+    src = O.Source(2, n // 2, n // 2, n // 2, tab)
+    g = O.zeros_state(n, n, n)
+    series = []
+    for t in range(steps):
+        h = [a.copy() for a in g[3:]]
+        O.ref_run_kernels(n, n, n, g, 1, step0=t, source=src)
+        series.append(O.ref_total_energy(n, n, n, g, h))
+    save("energy", dims=np.array([nx, ny, nz]), dx=dx, dy=dy, dz=dz, static=np.array(e_static),
+         seeds=np.array([31, 32]), n=np.array(n), steps=np.array(steps), table=tab,
+         series=np.array(series), **fields_dict("out", g))
 
 
 if __name__ == "__main__":

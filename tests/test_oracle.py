@@ -210,3 +210,39 @@ def test_live_reference_matches_oracle(oracle):
     e = [x.copy() for x in f0]
     oracle.run(nx, ny, nz, e, oracle.Coeffs(nx, ny, nz), 7)
     assert d1 == d2 == oracle.digest(nx, ny, nz, e)
+
+
+def test_energy_oracle_pinned(oracle):
+    """total_energy restatement vs the reference's values (golden/energy.npz,
+    fields.hpp:116-146): a stretched-grid value and a 60-step series."""
+    d = np.load(os.path.join(GOLD, "energy.npz"))
+    nx, ny, nz = (int(v) for v in d["dims"])
+    f = oracle.fill_fields(nx, ny, nz, int(d["seeds"][0]))
+    prev = oracle.fill_fields(nx, ny, nz, int(d["seeds"][1]))[3:]
+    got = oracle.total_energy(nx, ny, nz, f, prev, d["dx"], d["dy"], d["dz"])
+    assert abs(got - float(d["static"])) <= 1e-12 * abs(float(d["static"]))
+    n, steps = int(d["n"]), int(d["steps"])
+    src = oracle.Source(2, n // 2, n // 2, n // 2, d["table"])
+    g = oracle.zeros_state(n, n, n)
+    co = oracle.Coeffs(n, n, n)
+    for t in range(steps):
+        h = [a.copy() for a in g[3:]]
+        oracle.run(n, n, n, g, co, 1, step0=t, sources=[src])
+        want = float(d["series"][t])
+        assert abs(oracle.total_energy(n, n, n, g, h) - want) <= 1e-12 * abs(want), t
+    assert bits_equal(g, [d[f"out_{c}"] for c in oracle.COMP_NAMES])
+
+
+def test_energy_kats(oracle):
+    """kernel_test.cpp:265-283: E^2 with unit dual volume; H cross term."""
+    n = 4
+    f = oracle.zeros_state(n, n, n)
+    h = [a.copy() for a in f[3:]]
+    assert oracle.total_energy(n, n, n, f, h) == 0.0
+    f[2][1, 2, 2] = 2.0  # ez(2,2,1)
+    assert oracle.total_energy(n, n, n, f, h) == 4.0
+    f = oracle.zeros_state(n, n, n)
+    f[3][1, 1, 2] = 3.0  # hx(2,1,1)
+    prev = [a.copy() for a in f[3:]]
+    f[3][1, 1, 2] = 0.5
+    assert oracle.total_energy(n, n, n, f, prev) == 1.5

@@ -292,3 +292,127 @@ def test_cpp_shim_known_answers(yb, tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "shim KATs ok" in r.stdout
+
+
+PROBES = [(2, 20, 16, 14, 1), (3, 5, 6, 7, 3), (5, 10, 10, 29, 2), (0, 0, 0, 0, 5), (4, 39, 0, 28, 4)]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_device_probes_vs_oracle(yb, oracle, variant):
+    """On-device point probes (probe.hpp:14-51 sample after each completed
+    step t with t % stride == 0): same records and bit-identical values as the
+    oracle stepped one step at a time. The two-step kernel splits pairs where
+    a probe fires in between (stride 1 and 3 here)."""
+    nx, ny, nz, steps = 40, 33, 29, 13
+    f = oracle.fill_fields(nx, ny, nz, 21)
+    tab = oracle.gauss_table(steps)
+    src = (2, 20, 16, 14, tab)
+    with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+        sim.generate_medium(3, 4)
+        sim.add_source(*src)
+        sim.upload(f)
+        sim.set_probes(PROBES)
+        sim.run(5)
+        st0, pr0, va0 = sim.read_probes(capacity=3)  # partial drain keeps the tail
+        sim.run(steps - 5)
+        st1, pr1, va1 = sim.read_probes()
+        assert sim.read_probes()[0].size == 0
+    st, pr, va = (np.concatenate(x) for x in ((st0, st1), (pr0, pr1), (va0, va1)))
+    ca, cb, da, db = oracle.cell_coeffs(nx, ny, nz, 3, 4)
+    co = oracle.Coeffs(nx, ny, nz, ca=ca, cb=cb, da=da, db=db)
+    want = []
+    for t in range(steps):
+        oracle.run(nx, ny, nz, f, co, 1, step0=t, sources=[oracle.Source(*src)])
+        for q, (c, i, j, k, s) in enumerate(PROBES):
+            if (t + 1) % s == 0:
+                want.append((t + 1, q, f[c][k, j, i]))
+    assert list(zip(st.tolist(), pr.tolist())) == [(a, b) for a, b, _ in want]
+    assert np.array_equal(va.view(np.uint32), np.array([v for *_, v in want], np.float32).view(np.uint32))
+
+
+def test_probe_validation(yb):
+    with yb.Simulation(8, 8, 8) as sim:
+        for bad in [(2, 0, 0, 0, 0), (2, 9, 0, 0, 1), (0, 8, 0, 0, 1), (3, 0, 8, 0, 1), (5, 0, 0, 9, 1), (6, 0, 0, 0, 1)]:
+            with pytest.raises(yb.YeeInvalidArgument):
+                sim.set_probes([bad])
+        with pytest.raises(yb.YeeInvalidArgument):
+            sim.set_probes([(2, 1, 1, 1, 1)] * 65)
+        sim.set_probes([(5, 7, 7, 8, 1)])  # hz has nz+1 planes
+        sim.run(2)
+        st, pr, va = sim.read_probes()
+        assert st.tolist() == [1, 2] and pr.tolist() == [0, 0]
+        sim.set_probes([])
+        sim.run(2)
+        assert sim.read_probes()[0].size == 0
+
+
+def test_energy_vs_reference_golden(yb, oracle):
+    """Device total_energy (fields.hpp:116-146) against the reference's values
+    (golden/energy.npz): stretched spacing, and the per-step leapfrog
+    invariant of a sourced 20^3 run (measure_energy_drift pattern). Double
+    accumulation in a different order: relative 1e-12."""
+    d = load("energy")
+    nx, ny, nz = (int(v) for v in d["dims"])
+    f = oracle.fill_fields(nx, ny, nz, int(d["seeds"][0]))
+    prev = oracle.fill_fields(nx, ny, nz, int(d["seeds"][1]))
+    with yb.Simulation(nx, ny, nz) as sim:
+        with pytest.raises(yb.YeeInvalidArgument):
+            sim.total_energy()
+        sim.upload(prev)
+        sim.snapshot_h()
+        sim.upload(f)
+        got = sim.total_energy(d["dx"], d["dy"], d["dz"])
+    assert abs(got - float(d["static"])) <= 1e-12 * abs(float(d["static"]))
+    n, steps = int(d["n"]), int(d["steps"])
+    for variant in VARIANTS:
+        with yb.Simulation(n, n, n, variant=variant) as sim:
+            sim.add_source(2, n // 2, n // 2, n // 2, d["table"])
+            for t in range(steps):
+                sim.snapshot_h()
+                sim.run(1)
+                want = float(d["series"][t])
+                assert abs(sim.total_energy() - want) <= 1e-12 * abs(want), (variant, t)
+            assert_bits(sim.download(), gfields(d, "out"), "energy run")
+
+
+def test_energy_drift_single_precision(yb, oracle):
+    """SPEC.md:539 / bench.hpp:273-303: 64^3 vacuum cavity, source on for 50
+    steps, 1000 steps: single-precision relative drift < 1e-4."""
+    n, steps, on = 64, 1000, 50
+    tab = oracle.gauss_table(on, t0=25.0, w=8.0)
+    with yb.Simulation(n, n, n) as sim:
+        sim.add_source(2, n // 2, n // 2, n // 2, tab)
+        sim.run(on)
+        sim.snapshot_h()
+        sim.run(1)
+        e0 = sim.total_energy()
+        drift = 0.0
+        for t in range(on + 1, steps):
+            sim.snapshot_h()
+            sim.run(1)
+            drift = max(drift, abs(sim.total_energy() - e0) / abs(e0))
+    assert e0 > 0 and drift < 1e-4, drift
+
+
+def test_energy_slabs_sum(yb, oracle):
+    """On z-slabs each rank sums the planes it owns; the sum over slabs equals
+    the single-domain invariant (rel 1e-12)."""
+    from paper_1301_4539_b200.slabs import partition
+    nx, ny, nzg = 40, 24, 21
+    dz = np.linspace(0.8, 1.2, nzg)
+    f = oracle.fill_fields(nx, ny, nzg, 5)
+    prev = oracle.fill_fields(nx, ny, nzg, 6)
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.upload(prev)
+        one.snapshot_h()
+        one.upload(f)
+        want = one.total_energy(dz=dz)
+    total = 0.0
+    for z0, n in partition(nzg, 3):
+        with yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg) as s:
+            s.fill(6)
+            s.snapshot_h()
+            s.fill(5)
+            total += s.total_energy(dz=dz)
+    assert abs(total - want) <= 1e-12 * abs(want)
+    assert abs(want - oracle.total_energy(nx, ny, nzg, f, prev[3:], dz=dz)) <= 1e-12 * abs(want)
