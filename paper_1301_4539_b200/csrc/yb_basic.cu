@@ -189,6 +189,11 @@ __global__ void k_all_equal(const float* __restrict__ a, long long n, int* flag)
   if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0) atomicExch(flag, 0);
 }
 
+__global__ void k_fill_value(float* p, long long n, float v) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    p[t] = v;
+}
+
 // Point probes: out[q] = field[comp[q]][off[q]] (sample_probes, probe.hpp:36-51).
 __global__ void k_probes(Fields F, ProbeArgs pa, float* out) {
   const int q = threadIdx.x;
@@ -306,6 +311,11 @@ cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded,
                                 cudaStream_t st) {
   k_gather_dense<<<dim3((e[0] + 127) / 128, e[1], e[2]), 128, 0, st>>>(g, e[0], e[1], e[2], padded,
                                                                        dense);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_value(float* p, long long n, float v, cudaStream_t st) {
+  k_fill_value<<<592, 256, 0, st>>>(p, n, v);
   return cudaGetLastError();
 }
 

@@ -620,6 +620,22 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
     v = cells[0];
   }
   s->tm_valid = false;
+  if ((which == YB_CA || which == YB_DA) && (!cells || all_equal) && v != 1.0f) {
+    // a uniform Ca / Da other than 1 is stored as a full array: the sweep
+    // kernels treat "no Ca/Da array" as exactly 1 and skip the multiply
+    if (cells) YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
+    if (!s->cell[which]) {
+      float* p = nullptr;
+      YB_CU(cudaMalloc(&p, (size_t)s->g.total * 4));
+      s->cell[which] = p + yb::kGhost * s->g.plane;
+      s->dev_bytes += (size_t)s->g.total * 4;
+    }
+    YB_CU(yb::launch_fill_value(s->cell[which] - yb::kGhost * s->g.plane, s->g.total, v, s->stream));
+    if (which == YB_CA) s->ca_s = 1.0f;
+    if (which == YB_DA) s->da_s = 1.0f;
+    YB_CU(cudaStreamSynchronize(s->stream));
+    return YB_OK;
+  }
   if (!cells || all_equal) {
     if (cells) YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
     if (s->cell[which]) {

@@ -63,6 +63,18 @@ __device__ __forceinline__ float yee_upd(float A, float v, float C1, float a, fl
   return __fadd_rn(__fmul_rn(A, v), __fsub_rn(t1, t2));
 }
 
+// Same with the leading coefficient A known to be exactly 1 when !HAS_A
+// (uniform Ca / Da are only ever stored as the scalar 1, see
+// yb_set_cell_coeffs): 1*v == v, so skipping the multiply is bit-identical.
+template <bool HAS_A>
+__device__ __forceinline__ float yee_upd_t(float A, float v, float C1, float a, float b, float C2, float c,
+                                           float d) {
+  if (HAS_A) return yee_upd(A, v, C1, a, b, C2, c, d);
+  const float t1 = __fmul_rn(C1, __fsub_rn(a, b));
+  const float t2 = __fmul_rn(C2, __fsub_rn(c, d));
+  return __fadd_rn(v, __fsub_rn(t1, t2));
+}
+
 __device__ __forceinline__ long long gidx(const Geo& g, int i, int j, int k) {
   return ((long long)k * g.PY + j) * g.PX + i;
 }

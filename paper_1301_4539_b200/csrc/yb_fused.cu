@@ -188,13 +188,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float A = DAC ? elc(pda, q) : co.da_s;
         const float B = elc(pdb, q);
         // hx(i,j,k) += cdz[k]*(ey(k+1)-ey(k)) - cdy[j]*(ez(j+1)-ez(j))
-        el(hx, q) = yee_upd(A, elc(phx, q), DBC ? B : cdz_h, elc(eyk, q), elc(pey, q),
+        el(hx, q) = yee_upd_t<DAC>(A, elc(phx, q), DBC ? B : cdz_h, elc(eyk, q), elc(pey, q),
                             DBC ? B : cdy_h, elc(pez_n, q), elc(pez, q));
         // hy(i,j,k) += cdx[i]*(ez(i+1)-ez(i)) - cdz[k]*(ex(k+1)-ex(k))
-        el(hy, q) = yee_upd(A, elc(phy, q), DBC ? B : elc(cdx_h, q), elc(ez_ip, q), elc(pez, q),
+        el(hy, q) = yee_upd_t<DAC>(A, elc(phy, q), DBC ? B : elc(cdx_h, q), elc(ez_ip, q), elc(pez, q),
                             DBC ? B : cdz_h, elc(exk, q), elc(pex, q));
         // hz(i,j,k) += cdy[j]*(ex(j+1)-ex(j)) - cdx[i]*(ey(i+1)-ey(i))
-        el(hz, q) = yee_upd(A, elc(phz, q), DBC ? B : cdy_h, elc(pex_n, q), elc(pex, q),
+        el(hz, q) = yee_upd_t<DAC>(A, elc(phz, q), DBC ? B : cdy_h, elc(pex_n, q), elc(pex, q),
                             DBC ? B : elc(cdx_h, q), elc(ey_ip, q), elc(pey, q));
       }
       if (jlt) {
@@ -250,15 +250,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float B = elc(cb4, q);
         const float An = CAC ? elc(ca4n, q) : co.ca_s;
         const float Bn = elc(cb4n, q);
-        el(exw, q) = yee_upd(A, elc(ex, q), CBC ? B : cdy_e, elc(hz, q), elc(hz_jm, q), CBC ? B : cdz_e,
+        el(exw, q) = yee_upd_t<CAC>(A, elc(ex, q), CBC ? B : cdy_e, elc(hz, q), elc(hz_jm, q), CBC ? B : cdz_e,
                              elc(hy, q), elc(phy, q));
-        el(eyw, q) = yee_upd(A, elc(ey, q), CBC ? B : cdz_e, elc(hx, q), elc(phx, q),
+        el(eyw, q) = yee_upd_t<CAC>(A, elc(ey, q), CBC ? B : cdz_e, elc(hx, q), elc(phx, q),
                              CBC ? B : elc(cdx_e, q), elc(hz, q), elc(hz_im, q));
-        el(ezw, q) = yee_upd(A, elc(ez, q), CBC ? B : elc(cdx_e, q), elc(hy, q), elc(hy_im, q),
+        el(ezw, q) = yee_upd_t<CAC>(A, elc(ez, q), CBC ? B : elc(cdx_e, q), elc(hy, q), elc(hy_im, q),
                              CBC ? B : cdy_e, elc(hx, q), elc(hx_jm, q));
-        el(exn, q) = yee_upd(An, elc(ex_n, q), CBC ? Bn : cdy_en, elc(hz_n, q), elc(hz, q),
+        el(exn, q) = yee_upd_t<CAC>(An, elc(ex_n, q), CBC ? Bn : cdy_en, elc(hz_n, q), elc(hz, q),
                              CBC ? Bn : cdz_e, elc(hy_n, q), elc(phy_n, q));
-        el(ezn, q) = yee_upd(An, elc(ez_n, q), CBC ? Bn : elc(cdx_e, q), elc(hy_n, q), elc(hy_n_im, q),
+        el(ezn, q) = yee_upd_t<CAC>(An, elc(ez_n, q), CBC ? Bn : elc(cdx_e, q), elc(hy_n, q), elc(hy_n_im, q),
                              CBC ? Bn : cdy_en, elc(hx_n, q), elc(hx, q));
       }
       if (!(xint && jin && jnin && kin)) {  // only lanes on a boundary column/row/plane
@@ -280,10 +280,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float B = CBC ? *SM(S_CB, r, cc) : 0.f;
         hx_c = *SM(3, r, cc);
         const float hy_c = *SM(4, r, cc), hz_c = *SM(5, r, cc);
-        eyc = (ih_in && jlt && kin) ? yee_upd(A, *SM(1, r, cc), CBC ? B : cdz_e, hx_c, phx_c,
+        eyc = (ih_in && jlt && kin) ? yee_upd_t<CAC>(A, *SM(1, r, cc), CBC ? B : cdz_e, hx_c, phx_c,
                                               CBC ? B : cdx_e_h, hz_c, hz.w)
                                     : 0.f;
-        ezc = (ih_in && jin) ? yee_upd(A, *SM(2, r, cc), CBC ? B : cdx_e_h, hy_c, hy.w,
+        ezc = (ih_in && jin) ? yee_upd_t<CAC>(A, *SM(2, r, cc), CBC ? B : cdx_e_h, hy_c, hy.w,
                                        CBC ? B : cdy_e, hx_c, *SM(3, r - 1, cc))
                              : 0.f;
       }

@@ -105,6 +105,7 @@ struct ProbeArgs {
   int comp[64];
   long long off[64];
 };
+cudaError_t launch_fill_value(float* p, long long n, float v, cudaStream_t st);
 cudaError_t launch_probes(const Fields& F, const ProbeArgs& pa, float* out, cudaStream_t st);
 // weights: x node[nx+1], x cell[nx], y node[ny+1], y cell[ny], z node[nz+1], z cell[nz]
 // (local planes); partial: 6*nblk doubles; out: 1 double

@@ -58,7 +58,7 @@ struct F4x3 {
 // are forced to +0 afterwards; the mask pass only runs where some element can
 // be masked (boundary tiles, rows, planes), decided warp-uniformly.
 template <bool CAC, bool CBC>
-__device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int i0, bool xint, int j,
+__device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int i0, bool xedge, int j,
                                           int kg, float cdy, float cdz, float4 cdx, float4 ca,
                                           float4 cb, float4 ex, float4 ey, float4 ez, float4 hx,
                                           float4 hy, float4 hz, float4 hx_jm, float4 hz_jm,
@@ -68,16 +68,16 @@ __device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int 
   for (int q = 0; q < 4; ++q) {
     const float A = CAC ? elc(ca, q) : co.ca_s;
     const float B = elc(cb, q);
-    el(o.x, q) = yee_upd(A, elc(ex, q), CBC ? B : cdy, elc(hz, q), elc(hz_jm, q), CBC ? B : cdz,
+    el(o.x, q) = yee_upd_t<CAC>(A, elc(ex, q), CBC ? B : cdy, elc(hz, q), elc(hz_jm, q), CBC ? B : cdz,
                          elc(hy, q), elc(hy_km, q));
-    el(o.y, q) = yee_upd(A, elc(ey, q), CBC ? B : cdz, elc(hx, q), elc(hx_km, q),
+    el(o.y, q) = yee_upd_t<CAC>(A, elc(ey, q), CBC ? B : cdz, elc(hx, q), elc(hx_km, q),
                          CBC ? B : elc(cdx, q), elc(hz, q), elc(hz_im, q));
-    el(o.z, q) = yee_upd(A, elc(ez, q), CBC ? B : elc(cdx, q), elc(hy, q), elc(hy_im, q),
+    el(o.z, q) = yee_upd_t<CAC>(A, elc(ez, q), CBC ? B : elc(cdx, q), elc(hy, q), elc(hy_im, q),
                          CBC ? B : cdy, elc(hx, q), elc(hx_jm, q));
   }
   const bool kin = kg >= 1 && kg < g.nzg;
   const bool jin = j >= 1 && j < g.ny;
-  if (!(xint && jin && kin)) {
+  if (!(jin && kin)) {  // warp-uniform: PEC rows / planes, ghost rows
     const bool jlt = j >= 0 && j < g.ny, kz = kg >= 0 && kg < g.nzg;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -87,6 +87,14 @@ __device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int 
       if (!(iin && jlt && kin)) el(o.y, q) = 0.f;
       if (!(iin && jin && kz)) el(o.z, q) = 0.f;
     }
+  } else if (xedge) {  // the one or two lanes at i = 0 / i >= nx
+    if (i0 == 0) {
+      o.y.x = 0.f;
+      o.z.x = 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q >= g.nx) el(o.x, q) = el(o.y, q) = el(o.z, q) = 0.f;
   }
   return o;
 }
@@ -102,9 +110,9 @@ __device__ __forceinline__ void e_update1(const CoefArgs& co, const Geo& g, int 
   const bool jin = j >= 1 && j < g.ny, jlt = j >= 0 && j < g.ny;
   const bool iin = i >= 1 && i < g.nx, ilt = i >= 0 && i < g.nx;
   const float A = CAC ? ca : co.ca_s;
-  ox = (ilt && jin && kin) ? yee_upd(A, ex, CBC ? cb : cdy, hz, hz_jm, CBC ? cb : cdz, hy, hy_km) : 0.f;
-  oy = (iin && jlt && kin) ? yee_upd(A, ey, CBC ? cb : cdz, hx, hx_km, CBC ? cb : cdx, hz, hz_im) : 0.f;
-  oz = (iin && jin && kg >= 0 && kg < g.nzg) ? yee_upd(A, ez, CBC ? cb : cdx, hy, hy_im, CBC ? cb : cdy, hx, hx_jm)
+  ox = (ilt && jin && kin) ? yee_upd_t<CAC>(A, ex, CBC ? cb : cdy, hz, hz_jm, CBC ? cb : cdz, hy, hy_km) : 0.f;
+  oy = (iin && jlt && kin) ? yee_upd_t<CAC>(A, ey, CBC ? cb : cdz, hx, hx_km, CBC ? cb : cdx, hz, hz_im) : 0.f;
+  oz = (iin && jin && kg >= 0 && kg < g.nzg) ? yee_upd_t<CAC>(A, ez, CBC ? cb : cdx, hy, hy_im, CBC ? cb : cdy, hx, hx_jm)
                                              : 0.f;
 }
 
@@ -127,7 +135,7 @@ __device__ __forceinline__ float src_add(const SrcArgs& s, int sb, int comp, int
 // a z-slab the ghost planes -2..-1 and nz..nz+1 stand in for the neighbours.
 struct Item {
   int x0, y0, kz0, kz1, pstart, pin_end, pend, up;
-  bool pro;
+  bool pro, src;  // src: some source lies in the item's (halo-extended) box
 };
 
 __device__ __forceinline__ Item make_item(const Geo& g, int item, int T, int ntx, int zchunk) {
@@ -143,7 +151,14 @@ __device__ __forceinline__ Item make_item(const Geo& g, int item, int T, int ntx
   it.pin_end = min(it.kz1 + 1, top ? g.nz - 1 : g.nz + 1);
   it.pend = it.kz1 + 1;
   it.up = min(it.kz1, top ? g.nz - 1 : g.nz);
+  it.src = false;
   return it;
+}
+
+__device__ __forceinline__ void mark_sources(const SrcArgs& s, Item& it) {
+  for (int q = 0; q < s.n; ++q)
+    it.src |= s.act[q] != 0 && s.i[q] >= it.x0 - 1 && s.i[q] <= it.x0 + kTX + 1 && s.j[q] >= it.y0 - 1 &&
+              s.j[q] <= it.y0 + kTB2Rows + 1 && s.k[q] >= it.pstart && s.k[q] <= it.pend;
 }
 
 // Stage layout: fields (12 rows from y0-2), then Ca, Cb (11 rows from y0-1),
@@ -182,14 +197,18 @@ struct Bufs {
 };
 
 struct Cursor {
-  int cs;
+  int s;        // next stage
+  uint32_t ph;  // its full-barrier phase parity
   bool peeked;
   __device__ int wait(const Bufs& B, int S) {
-    const int s = cs % S;
-    if (!peeked) mbar_wait(smem_u32(&B.full[s]), (uint32_t)((cs / S) & 1));
+    if (!peeked) mbar_wait(smem_u32(&B.full[s]), ph);
     peeked = false;
-    ++cs;
-    return s;
+    const int r = s;
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+    return r;
   }
 };
 
@@ -211,7 +230,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
   const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
   const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const bool xint = i0 >= 1 && i0 + 4 <= g.nx;  // this lane touches neither i=0 nor i>=nx
+  const bool xedge = i0 == 0 || i0 + 4 > g.nx;  // this lane touches i = 0 or i >= nx
   F4x3 h0p = {z4, z4, z4};
   float4 cap = z4, cbp = z4, dap = z4, dbp = z4, dap2 = z4, dbp2 = z4;
 
@@ -243,12 +262,12 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       if (CBC) cbn = lds4(F + L::off_cb + er * BX + c);
       if (DAC && er <= RW - 2) dan = lds4(F + L::off_da + er * BX + c);
       if (DBC && er <= RW - 2) dbn = lds4(F + L::off_db + er * BX + c);
-      e1c = e_update4<CAC, CBC>(co, g, i0, xint, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn,
+      e1c = e_update4<CAC, CBC>(co, g, i0, xedge, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn,
                                 lds4(F + 0 * kTB2SlotF + rs * BX + c), lds4(F + 1 * kTB2SlotF + rs * BX + c),
                                 lds4(F + 2 * kTB2SlotF + rs * BX + c), h0n.x, h0n.y, h0n.z,
                                 lds4(F + 3 * kTB2SlotF + (rs - 1) * BX + c),
                                 lds4(F + 5 * kTB2SlotF + (rs - 1) * BX + c), hy_im, hz_im, h0p.x, h0p.y);
-      if (src_row(a.src, 1, j, p)) {
+      if (it.src && src_row(a.src, 1, j, p)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           el(e1c.x, q) = __fadd_rn(el(e1c.x, q), src_add(a.src, 1, 0, i0 + q, j, p));
@@ -278,11 +297,11 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       for (int q = 0; q < 4; ++q) {
         const float A = DAC ? elc(dap, q) : co.da_s;
         const float Bq = elc(dbp, q);
-        el(h1c.x, q) = yee_upd(A, elc(h0p.x, q), DBC ? Bq : cdz_h, elc(e1c.y, q), elc(ey_h, q),
+        el(h1c.x, q) = yee_upd_t<DAC>(A, elc(h0p.x, q), DBC ? Bq : cdz_h, elc(e1c.y, q), elc(ey_h, q),
                                DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
-        el(h1c.y, q) = yee_upd(A, elc(h0p.y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
+        el(h1c.y, q) = yee_upd_t<DAC>(A, elc(h0p.y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
                                DBC ? Bq : cdz_h, elc(e1c.x, q), elc(ex_h, q));
-        el(h1c.z, q) = yee_upd(A, elc(h0p.z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
+        el(h1c.z, q) = yee_upd_t<DAC>(A, elc(h0p.z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
                                DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
       }
       sts4(B.H1(pb, 0, er, c), h1c.x);
@@ -300,11 +319,11 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       const float4 hz = lds4(B.H1(hb, 2, er, c));
       const float4 hy_im = shift_im(hy, l, *B.H1(hb, 1, er, CL));
       const float4 hz_im = shift_im(hz, l, *B.H1(hb, 2, er, CL));
-      e2c = e_update4<CAC, CBC>(co, g, i0, xint, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
+      e2c = e_update4<CAC, CBC>(co, g, i0, xedge, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
                                 lds4(B.E1(hb, 0, er, c)), lds4(B.E1(hb, 1, er, c)), lds4(B.E1(hb, 2, er, c)),
                                 hx, hy, hz, lds4(B.H1(hb, 0, er - 1, c)), lds4(B.H1(hb, 2, er - 1, c)), hy_im,
                                 hz_im, lds4(B.H1(hb ^ 1, 0, er, c)), lds4(B.H1(hb ^ 1, 1, er, c)));
-      if (src_row(a.src, 2, j, kh)) {
+      if (it.src && src_row(a.src, 2, j, kh)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           el(e2c.x, q) = __fadd_rn(el(e2c.x, q), src_add(a.src, 2, 0, i0 + q, j, kh));
@@ -340,11 +359,11 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       for (int q = 0; q < 4; ++q) {
         const float A = DAC ? elc(dap2, q) : co.da_s;
         const float Bq = elc(dbp2, q);
-        el(h2.x, q) = yee_upd(A, elc(h1x, q), DBC ? Bq : cdz_h, elc(e2c.y, q), elc(ey_h, q),
+        el(h2.x, q) = yee_upd_t<DAC>(A, elc(h1x, q), DBC ? Bq : cdz_h, elc(e2c.y, q), elc(ey_h, q),
                               DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
-        el(h2.y, q) = yee_upd(A, elc(h1y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
+        el(h2.y, q) = yee_upd_t<DAC>(A, elc(h1y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
                               DBC ? Bq : cdz_h, elc(e2c.x, q), elc(ex_h, q));
-        el(h2.z, q) = yee_upd(A, elc(h1z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
+        el(h2.z, q) = yee_upd_t<DAC>(A, elc(h1z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
                               DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
       }
       if (j < g.ny) {
@@ -416,7 +435,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
                           cb, Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], hx, hy, hz, Fr[3 * kTB2SlotF - BX],
                           Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1], Fr[5 * kTB2SlotF - 1],
                           *B.H0e((p - 1) & 1, 0, r, e1i), *B.H0e((p - 1) & 1, 1, r, e1i), ox, oy, oz);
-      if (src_row(a.src, 1, j, p)) {
+      if (it.src && src_row(a.src, 1, j, p)) {
         ox = __fadd_rn(ox, src_add(a.src, 1, 0, i, j, p));
         oy = __fadd_rn(oy, src_add(a.src, 1, 1, i, j, p));
         oz = __fadd_rn(oz, src_add(a.src, 1, 2, i, j, p));
@@ -449,11 +468,11 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
       // it is the PEC zero, not the stale buffer content
       const float exk = l1 ? *B.E1(p & 1, 0, r, col) : 0.f;
       const float eyk = l1 ? *B.E1(p & 1, 1, r, col) : 0.f;
-      *B.H1(hb, 0, r, col) = yee_upd(A, *B.H0e(hb, 0, r, e2i), DBC ? Bq : cdz_h, eyk, ey_h,
+      *B.H1(hb, 0, r, col) = yee_upd_t<DAC>(A, *B.H0e(hb, 0, r, e2i), DBC ? Bq : cdz_h, eyk, ey_h,
                                      DBC ? Bq : cdy_h, *B.E1(hb, 2, r + 1, col), ez_h);
-      *B.H1(hb, 1, r, col) = yee_upd(A, *B.H0e(hb, 1, r, e2i), DBC ? Bq : cdx, *B.E1(hb, 2, r, col + 1), ez_h,
+      *B.H1(hb, 1, r, col) = yee_upd_t<DAC>(A, *B.H0e(hb, 1, r, e2i), DBC ? Bq : cdx, *B.E1(hb, 2, r, col + 1), ez_h,
                                      DBC ? Bq : cdz_h, exk, ex_h);
-      *B.H1(hb, 2, r, col) = yee_upd(A, *B.H0e(hb, 2, r, e2i), DBC ? Bq : cdy_h, *B.E1(hb, 0, r + 1, col), ex_h,
+      *B.H1(hb, 2, r, col) = yee_upd_t<DAC>(A, *B.H0e(hb, 2, r, e2i), DBC ? Bq : cdy_h, *B.E1(hb, 0, r + 1, col), ex_h,
                                      DBC ? Bq : cdx, *B.E1(hb, 1, r, col + 1), ey_h);
     }
     consumer_sync();  // (B)
@@ -467,7 +486,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
                           *B.H1(hb, 0, r - 1, CR), *B.H1(hb, 2, r - 1, CR), *B.H1(hb, 1, r, CR - 1),
                           *B.H1(hb, 2, r, CR - 1), *B.H1(hb ^ 1, 0, r, CR), *B.H1(hb ^ 1, 1, r, CR), ox, oy,
                           oz);
-      if (src_row(a.src, 2, j, kh)) {
+      if (it.src && src_row(a.src, 2, j, kh)) {
         ox = __fadd_rn(ox, src_add(a.src, 2, 0, i, j, kh));
         oy = __fadd_rn(oy, src_add(a.src, 2, 1, i, j, kh));
         oz = __fadd_rn(oz, src_add(a.src, 2, 2, i, j, kh));
@@ -573,15 +592,16 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
 
   uint64_t st_pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(st_pol));
-  Cursor cur{0, false};
+  Cursor cur{0, 0u, false};
   int c_seq = 0;
   for (;;) {
-    mbar_wait(smem_u32(&B.full[cur.cs % S]), (uint32_t)((cur.cs / S) & 1));
+    mbar_wait(smem_u32(&B.full[cur.s]), cur.ph);
     cur.peeked = true;
     const int item = item_q[c_seq % kQ];
     ++c_seq;
     if (item < 0) break;
-    const Item it = make_item(g, item, T, a.ntx, a.zchunk);
+    Item it = make_item(g, item, T, a.ntx, a.zchunk);
+    mark_sources(a.src, it);
     if (w == EDGE)
       tb2_edge<CAC, CBC, DAC, DBC>(a, it, B, cur, l);
     else
