@@ -92,9 +92,11 @@ __device__ __forceinline__ F4x3 e_update4(const CoefArgs& co, const Geo& g, int 
       o.y.x = 0.f;
       o.z.x = 0.f;
     }
+    if (i0 + 4 > g.nx) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + q >= g.nx) el(o.x, q) = el(o.y, q) = el(o.z, q) = 0.f;
+      for (int q = 0; q < 4; ++q)
+        if (i0 + q >= g.nx) el(o.x, q) = el(o.y, q) = el(o.z, q) = 0.f;
+    }
   }
   return o;
 }
@@ -216,57 +218,86 @@ struct Cursor {
 // Warp er owns row j = y0-1+er at every level. Carried across planes in
 // registers: H0(p-1), Ca/Cb(p-1), Da/Db(p-1), Da/Db(p-2) of its own row;
 // E1(p-1) and H1(p-2) of its own row are re-read from shared memory.
+// Every shared-memory operand is a per-warp base pointer (selected by the
+// plane parity) plus a compile-time offset; the i-1 /
+// i+1 neighbours of a lane's float4 are read as one scalar from the row in
+// shared memory (column c-1 / c+4; the edge columns for lanes 0 / 31).
 template <bool CAC, bool CBC, bool DAC, bool DBC>
-__device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
-                                         int er, int l, uint64_t st_pol) {
+struct Rows {
   using L = StageLayout<CAC, CBC, DAC, DBC>;
-  const Geo& g = a.g;
-  const CoefArgs& co = a.co;
-  const int S = a.nstages;
-  const int j = it.y0 - 1 + er;
-  const int rs = er + 1;  // field stage row
-  const int c = 4 + 4 * l;
-  const int i0 = it.x0 + 4 * l;
-  const float cdy_e = co.cdy_e[max(j, 0)], cdy_h = co.cdy_h[max(j, 0)];
-  const float4 cdx_e = ldg4(co.cdx_e + i0), cdx_h = ldg4(co.cdx_h + i0);
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const bool xedge = i0 == 0 || i0 + 4 > g.nx;  // this lane touches i = 0 or i >= nx
-  F4x3 h0p = {z4, z4, z4};
-  float4 cap = z4, cbp = z4, dap = z4, dbp = z4, dap2 = z4, dbp2 = z4;
+  static constexpr int E1C = RW * BX, E1B = 3 * E1C;              // comp / buffer strides
+  static constexpr int H1C = (RW - 1) * BX, H1B = 3 * H1C;
+  static constexpr int E2C = (RW - 2) * BX, E2B = 3 * E2C;
 
-  if (it.pro) {  // prologue: hx, hy of plane pstart-1
-    const int s = cur.wait(B, S);
-    const float* F = B.stages + (size_t)s * L::floats;
-    h0p.x = lds4(F + 3 * kTB2SlotF + rs * BX + c);
-    h0p.y = lds4(F + 4 * kTB2SlotF + rs * BX + c);
+  const FusedArgs& a;
+  const Item& it;
+  const Bufs& B;
+  Cursor& cur;
+  const int er, l, j, c, i0;
+  const bool xedge;
+  const uint64_t st_pol;
+  float* const e1o;  // E1 buffer 0, comp 0, row er, column c
+  float* const h1o;  // H1 buffer 0, comp 0, row er, column c
+  float* const e2o;  // E2 buffer 0, comp 0, row er-1, column c
+  float cdy_e, cdy_h;
+  float4 cdx_e, cdx_h;
+  F4x3 h0p;
+  float4 cap, cbp, dap, dbp, dap2, dbp2;
+
+  __device__ __forceinline__ Rows(const FusedArgs& a_, const Item& it_, const Bufs& B_, Cursor& cur_, int er_,
+                                  int l_, uint64_t pol)
+      : a(a_), it(it_), B(B_), cur(cur_), er(er_), l(l_), j(it_.y0 - 1 + er_), c(4 + 4 * l_),
+        i0(it_.x0 + 4 * l_), xedge(i0 == 0 || i0 + 4 > a_.g.nx), st_pol(pol),
+        e1o(B_.e1b + er_ * BX + c), h1o(B_.h1b + er_ * BX + c), e2o(B_.e2b + (er_ - 1) * BX + c) {
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    cdy_e = a.co.cdy_e[max(j, 0)];
+    cdy_h = a.co.cdy_h[max(j, 0)];
+    cdx_e = ldg4(a.co.cdx_e + i0);
+    cdx_h = ldg4(a.co.cdx_h + i0);
+    h0p = {z4, z4, z4};
+    cap = cbp = dap = dbp = dap2 = dbp2 = z4;
+  }
+
+  __device__ __forceinline__ void prologue() {
+    const int rs = er + 1;
+    const int s = cur.wait(B, a.nstages);
+    const float* F = B.stages + (size_t)s * L::floats + rs * BX + c;
+    h0p.x = lds4(F + 3 * kTB2SlotF);
+    h0p.y = lds4(F + 4 * kTB2SlotF);
     consumer_sync();
     if (er == 0 && l == 0) mbar_arrive(smem_u32(&B.empty[s]));
   }
 
-  for (int p = it.pstart; p <= it.pend; ++p) {
+  // one wavefront plane p (buffers alternate with the plane parity)
+  __device__ __forceinline__ void plane(int p) {
+    const int PAR = p & 1, Q = PAR ^ 1;  // parity of p, p-1
+    const Geo& g = a.g;
+    const CoefArgs& co = a.co;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     // ------------------------------------------------------- L1: E1(p)
     const bool l1 = p <= it.pin_end;
     F4x3 e1c = {z4, z4, z4}, h0n = {z4, z4, z4};
     float4 can = z4, cbn = z4, dan = z4, dbn = z4;
     int s1 = -1;
     if (l1) {
-      s1 = cur.wait(B, S);
+      s1 = cur.wait(B, a.nstages);
       const float* F = B.stages + (size_t)s1 * L::floats;
+      const float* Fr = F + (er + 1) * BX + c;  // field stage row of j
       const float cdz_e = co.cdz_e[p];
-      h0n.x = lds4(F + 3 * kTB2SlotF + rs * BX + c);
-      h0n.y = lds4(F + 4 * kTB2SlotF + rs * BX + c);
-      h0n.z = lds4(F + 5 * kTB2SlotF + rs * BX + c);
-      const float4 hy_im = shift_im(h0n.y, l, F[4 * kTB2SlotF + rs * BX + c - 1]);
-      const float4 hz_im = shift_im(h0n.z, l, F[5 * kTB2SlotF + rs * BX + c - 1]);
-      if (CAC) can = lds4(F + L::off_ca + er * BX + c);
-      if (CBC) cbn = lds4(F + L::off_cb + er * BX + c);
-      if (DAC && er <= RW - 2) dan = lds4(F + L::off_da + er * BX + c);
-      if (DBC && er <= RW - 2) dbn = lds4(F + L::off_db + er * BX + c);
-      e1c = e_update4<CAC, CBC>(co, g, i0, xedge, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn,
-                                lds4(F + 0 * kTB2SlotF + rs * BX + c), lds4(F + 1 * kTB2SlotF + rs * BX + c),
-                                lds4(F + 2 * kTB2SlotF + rs * BX + c), h0n.x, h0n.y, h0n.z,
-                                lds4(F + 3 * kTB2SlotF + (rs - 1) * BX + c),
-                                lds4(F + 5 * kTB2SlotF + (rs - 1) * BX + c), hy_im, hz_im, h0p.x, h0p.y);
+      h0n.x = lds4(Fr + 3 * kTB2SlotF);
+      h0n.y = lds4(Fr + 4 * kTB2SlotF);
+      h0n.z = lds4(Fr + 5 * kTB2SlotF);
+      const float4 hy_im = make_float4(Fr[4 * kTB2SlotF - 1], h0n.y.x, h0n.y.y, h0n.y.z);
+      const float4 hz_im = make_float4(Fr[5 * kTB2SlotF - 1], h0n.z.x, h0n.z.y, h0n.z.z);
+      const float* Fc = F + er * BX + c;  // coefficient stage row of j
+      if (CAC) can = lds4(Fc + L::off_ca);
+      if (CBC) cbn = lds4(Fc + L::off_cb);
+      if (DAC && er <= RW - 2) dan = lds4(Fc + L::off_da);
+      if (DBC && er <= RW - 2) dbn = lds4(Fc + L::off_db);
+      e1c = e_update4<CAC, CBC>(co, g, i0, xedge, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn, lds4(Fr),
+                                lds4(Fr + kTB2SlotF), lds4(Fr + 2 * kTB2SlotF), h0n.x, h0n.y, h0n.z,
+                                lds4(Fr + 3 * kTB2SlotF - BX), lds4(Fr + 5 * kTB2SlotF - BX), hy_im, hz_im, h0p.x,
+                                h0p.y);
       if (it.src && src_row(a.src, 1, j, p)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -275,9 +306,10 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
           el(e1c.z, q) = __fadd_rn(el(e1c.z, q), src_add(a.src, 1, 2, i0 + q, j, p));
         }
       }
-      sts4(B.E1(p & 1, 0, er, c), e1c.x);
-      sts4(B.E1(p & 1, 1, er, c), e1c.y);
-      sts4(B.E1(p & 1, 2, er, c), e1c.z);
+      float* w = e1o + PAR * E1B;
+      sts4(w, e1c.x);
+      sts4(w + E1C, e1c.y);
+      sts4(w + 2 * E1C, e1c.z);
     }
     consumer_sync();  // (A) E1(p) complete, stage free
     if (l1 && er == 0 && l == 0) mbar_arrive(smem_u32(&B.empty[s1]));
@@ -285,44 +317,45 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
     // ----------------------------------------------------- L2: H1(p-1)
     const int kh = p - 1;
     if (kh >= it.pstart && kh <= it.up && er <= RW - 2) {
-      const int pb = kh & 1;
       const float cdz_h = co.cdz_h[kh];
-      const float4 ex_h = lds4(B.E1(pb, 0, er, c)), ex_jp = lds4(B.E1(pb, 0, er + 1, c));
-      const float4 ey_h = lds4(B.E1(pb, 1, er, c));
-      const float4 ez_h = lds4(B.E1(pb, 2, er, c)), ez_jp = lds4(B.E1(pb, 2, er + 1, c));
-      const float4 ey_ip = shift_ip(ey_h, l, *B.E1(pb, 1, er, CR));
-      const float4 ez_ip = shift_ip(ez_h, l, *B.E1(pb, 2, er, CR));
+      const float* e = e1o + Q * E1B;  // E1(p-1), row j
+      const float4 ex_h = lds4(e), ex_jp = lds4(e + BX);
+      const float4 ey_h = lds4(e + E1C);
+      const float4 ez_h = lds4(e + 2 * E1C), ez_jp = lds4(e + 2 * E1C + BX);
+      const float4 ey_ip = make_float4(ey_h.y, ey_h.z, ey_h.w, e[E1C + 4]);
+      const float4 ez_ip = make_float4(ez_h.y, ez_h.z, ez_h.w, e[2 * E1C + 4]);
       F4x3 h1c;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float A = DAC ? elc(dap, q) : co.da_s;
         const float Bq = elc(dbp, q);
         el(h1c.x, q) = yee_upd_t<DAC>(A, elc(h0p.x, q), DBC ? Bq : cdz_h, elc(e1c.y, q), elc(ey_h, q),
-                               DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
+                                      DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
         el(h1c.y, q) = yee_upd_t<DAC>(A, elc(h0p.y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
-                               DBC ? Bq : cdz_h, elc(e1c.x, q), elc(ex_h, q));
+                                      DBC ? Bq : cdz_h, elc(e1c.x, q), elc(ex_h, q));
         el(h1c.z, q) = yee_upd_t<DAC>(A, elc(h0p.z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
-                               DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
+                                      DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
       }
-      sts4(B.H1(pb, 0, er, c), h1c.x);
-      sts4(B.H1(pb, 1, er, c), h1c.y);
-      sts4(B.H1(pb, 2, er, c), h1c.z);
+      float* w = h1o + Q * H1B;
+      sts4(w, h1c.x);
+      sts4(w + H1C, h1c.y);
+      sts4(w + 2 * H1C, h1c.z);
     }
     consumer_sync();  // (B) H1(p-1) complete
 
     // ----------------------------------------------------- L3: E2(p-1)
     F4x3 e2c = {z4, z4, z4};
     if (kh >= it.kz0 && kh <= it.up && er >= 1 && er <= RW - 2) {
-      const int hb = kh & 1;
       const float cdz_e = co.cdz_e[kh];
-      const float4 hx = lds4(B.H1(hb, 0, er, c)), hy = lds4(B.H1(hb, 1, er, c));
-      const float4 hz = lds4(B.H1(hb, 2, er, c));
-      const float4 hy_im = shift_im(hy, l, *B.H1(hb, 1, er, CL));
-      const float4 hz_im = shift_im(hz, l, *B.H1(hb, 2, er, CL));
-      e2c = e_update4<CAC, CBC>(co, g, i0, xedge, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
-                                lds4(B.E1(hb, 0, er, c)), lds4(B.E1(hb, 1, er, c)), lds4(B.E1(hb, 2, er, c)),
-                                hx, hy, hz, lds4(B.H1(hb, 0, er - 1, c)), lds4(B.H1(hb, 2, er - 1, c)), hy_im,
-                                hz_im, lds4(B.H1(hb ^ 1, 0, er, c)), lds4(B.H1(hb ^ 1, 1, er, c)));
+      const float* h = h1o + Q * H1B;    // H1(p-1), row j
+      const float* hp = h1o + PAR * H1B;  // H1(p-2), row j
+      const float4 hx = lds4(h), hy = lds4(h + H1C), hz = lds4(h + 2 * H1C);
+      const float4 hy_im = make_float4(h[H1C - 1], hy.x, hy.y, hy.z);
+      const float4 hz_im = make_float4(h[2 * H1C - 1], hz.x, hz.y, hz.z);
+      const float* e = e1o + Q * E1B;
+      e2c = e_update4<CAC, CBC>(co, g, i0, xedge, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp, lds4(e),
+                                lds4(e + E1C), lds4(e + 2 * E1C), hx, hy, hz, lds4(h - BX), lds4(h + 2 * H1C - BX),
+                                hy_im, hz_im, lds4(hp), lds4(hp + H1C));
       if (it.src && src_row(a.src, 2, j, kh)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -331,9 +364,10 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
           el(e2c.z, q) = __fadd_rn(el(e2c.z, q), src_add(a.src, 2, 2, i0 + q, j, kh));
         }
       }
-      sts4(B.E2(hb, 0, er - 1, c), e2c.x);
-      sts4(B.E2(hb, 1, er - 1, c), e2c.y);
-      sts4(B.E2(hb, 2, er - 1, c), e2c.z);
+      float* w = e2o + Q * E2B;
+      sts4(w, e2c.x);
+      sts4(w + E2C, e2c.y);
+      sts4(w + 2 * E2C, e2c.z);
       if (er <= kTB2Rows && j < g.ny && kh < it.kz1) {  // E^{n+2} of the owned rows -> HBM
         const long long gp = gidx(g, i0, j, kh);
         store_row4(a.out[0], gp, i0, g.nx, e2c.x, st_pol);
@@ -345,26 +379,26 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
     // ----------------------------------------------------- L4: H2(p-2)
     const int k4 = p - 2;
     if (k4 >= it.kz0 && k4 <= it.kz1 - 1 && er >= 1 && er <= kTB2Rows) {
-      const int pb = k4 & 1;
       const float cdz_h = co.cdz_h[k4];
-      const float4 ex_h = lds4(B.E2(pb, 0, er - 1, c)), ex_jp = lds4(B.E2(pb, 0, er, c));
-      const float4 ey_h = lds4(B.E2(pb, 1, er - 1, c));
-      const float4 ez_h = lds4(B.E2(pb, 2, er - 1, c)), ez_jp = lds4(B.E2(pb, 2, er, c));
-      const float4 ey_ip = shift_ip(ey_h, l, *B.E2(pb, 1, er - 1, CR));
-      const float4 ez_ip = shift_ip(ez_h, l, *B.E2(pb, 2, er - 1, CR));
-      const float4 h1x = lds4(B.H1(pb, 0, er, c)), h1y = lds4(B.H1(pb, 1, er, c));
-      const float4 h1z = lds4(B.H1(pb, 2, er, c));
+      const float* e = e2o + PAR * E2B;  // E2(p-2), row j
+      const float4 ex_h = lds4(e), ex_jp = lds4(e + BX);
+      const float4 ey_h = lds4(e + E2C);
+      const float4 ez_h = lds4(e + 2 * E2C), ez_jp = lds4(e + 2 * E2C + BX);
+      const float4 ey_ip = make_float4(ey_h.y, ey_h.z, ey_h.w, e[E2C + 4]);
+      const float4 ez_ip = make_float4(ez_h.y, ez_h.z, ez_h.w, e[2 * E2C + 4]);
+      const float* h = h1o + PAR * H1B;  // H1(p-2), row j
+      const float4 h1x = lds4(h), h1y = lds4(h + H1C), h1z = lds4(h + 2 * H1C);
       F4x3 h2;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float A = DAC ? elc(dap2, q) : co.da_s;
         const float Bq = elc(dbp2, q);
         el(h2.x, q) = yee_upd_t<DAC>(A, elc(h1x, q), DBC ? Bq : cdz_h, elc(e2c.y, q), elc(ey_h, q),
-                              DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
+                                     DBC ? Bq : cdy_h, elc(ez_jp, q), elc(ez_h, q));
         el(h2.y, q) = yee_upd_t<DAC>(A, elc(h1y, q), DBC ? Bq : elc(cdx_h, q), elc(ez_ip, q), elc(ez_h, q),
-                              DBC ? Bq : cdz_h, elc(e2c.x, q), elc(ex_h, q));
+                                     DBC ? Bq : cdz_h, elc(e2c.x, q), elc(ex_h, q));
         el(h2.z, q) = yee_upd_t<DAC>(A, elc(h1z, q), DBC ? Bq : cdy_h, elc(ex_jp, q), elc(ex_h, q),
-                              DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
+                                     DBC ? Bq : elc(cdx_h, q), elc(ey_ip, q), elc(ey_h, q));
       }
       if (j < g.ny) {
         const long long gp = gidx(g, i0, j, k4);
@@ -384,6 +418,14 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
       dbp = dbn;
     }
   }
+};
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+__device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
+                                         int er, int l, uint64_t st_pol) {
+  Rows<CAC, CBC, DAC, DBC> R(a, it, B, cur, er, l, st_pol);
+  if (it.pro) R.prologue();
+  for (int p = it.pstart; p <= it.pend; ++p) R.plane(p);
 }
 
 // ============================================================= edge warp
