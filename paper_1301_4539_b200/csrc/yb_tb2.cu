@@ -241,6 +241,9 @@ struct Rows {
   float* const e2o;  // E2 buffer 0, comp 0, row er-1, column c
   float cdy_e, cdy_h;
   float4 cdx_e, cdx_h;
+  // cdz values rotate through registers, loaded one plane ahead:
+  // ze = cdz_e[p], zh = cdz_h[p-1], ze1 = cdz_e[p-1], zh1 = cdz_h[p-2]
+  float ze, zh, ze1, zh1;
   F4x3 h0p;
   float4 cap, cbp, dap, dbp, dap2, dbp2;
 
@@ -256,6 +259,9 @@ struct Rows {
     cdx_h = ldg4(a.co.cdx_h + i0);
     h0p = {z4, z4, z4};
     cap = cbp = dap = dbp = dap2 = dbp2 = z4;
+    ze = a.co.cdz_e[it_.pstart];
+    zh = a.co.cdz_h[it_.pstart - 1];
+    ze1 = zh1 = 0.f;
   }
 
   __device__ __forceinline__ void prologue() {
@@ -274,6 +280,7 @@ struct Rows {
     const Geo& g = a.g;
     const CoefArgs& co = a.co;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float ze_n = co.cdz_e[p + 1], zh_n = co.cdz_h[p];  // next plane's
     // ------------------------------------------------------- L1: E1(p)
     const bool l1 = p <= it.pin_end;
     F4x3 e1c = {z4, z4, z4}, h0n = {z4, z4, z4};
@@ -283,7 +290,7 @@ struct Rows {
       s1 = cur.wait(B, a.nstages);
       const float* F = B.stages + (size_t)s1 * L::floats;
       const float* Fr = F + (er + 1) * BX + c;  // field stage row of j
-      const float cdz_e = co.cdz_e[p];
+      const float cdz_e = ze;
       h0n.x = lds4(Fr + 3 * kTB2SlotF);
       h0n.y = lds4(Fr + 4 * kTB2SlotF);
       h0n.z = lds4(Fr + 5 * kTB2SlotF);
@@ -317,7 +324,7 @@ struct Rows {
     // ----------------------------------------------------- L2: H1(p-1)
     const int kh = p - 1;
     if (kh >= it.pstart && kh <= it.up && er <= RW - 2) {
-      const float cdz_h = co.cdz_h[kh];
+      const float cdz_h = zh;
       const float* e = e1o + Q * E1B;  // E1(p-1), row j
       const float4 ex_h = lds4(e), ex_jp = lds4(e + BX);
       const float4 ey_h = lds4(e + E1C);
@@ -346,7 +353,7 @@ struct Rows {
     // ----------------------------------------------------- L3: E2(p-1)
     F4x3 e2c = {z4, z4, z4};
     if (kh >= it.kz0 && kh <= it.up && er >= 1 && er <= RW - 2) {
-      const float cdz_e = co.cdz_e[kh];
+      const float cdz_e = ze1;
       const float* h = h1o + Q * H1B;    // H1(p-1), row j
       const float* hp = h1o + PAR * H1B;  // H1(p-2), row j
       const float4 hx = lds4(h), hy = lds4(h + H1C), hz = lds4(h + 2 * H1C);
@@ -379,7 +386,7 @@ struct Rows {
     // ----------------------------------------------------- L4: H2(p-2)
     const int k4 = p - 2;
     if (k4 >= it.kz0 && k4 <= it.kz1 - 1 && er >= 1 && er <= kTB2Rows) {
-      const float cdz_h = co.cdz_h[k4];
+      const float cdz_h = zh1;
       const float* e = e2o + PAR * E2B;  // E2(p-2), row j
       const float4 ex_h = lds4(e), ex_jp = lds4(e + BX);
       const float4 ey_h = lds4(e + E2C);
@@ -408,6 +415,10 @@ struct Rows {
       }
     }
     // ---------------------------------------------------------- rotate
+    ze1 = ze;
+    zh1 = zh;
+    ze = ze_n;
+    zh = zh_n;
     dap2 = dap;
     dbp2 = dbp;
     if (l1) {
@@ -452,6 +463,11 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
   // L3 task: column CR, rows 1..9 for lanes 0..8
   const int e3r = l + 1;
   const bool l3_lane = l < RW - 2;
+  // lane-invariant coefficients of the three tasks
+  const int j1 = it.y0 - 1 + e1r, i1 = ie(e1i), j2 = it.y0 - 1 + e2r, i2 = ie(e2i), j3 = it.y0 - 1 + e3r;
+  const float cdy1 = co.cdy_e[max(j1, 0)], cdx1 = co.cdx_e[max(i1, 0)];
+  const float cdy2 = co.cdy_h[max(j2, 0)], cdx2 = co.cdx_h[max(i2, 0)];
+  const float cdy3 = co.cdy_e[max(j3, 0)], cdx3 = co.cdx_e[ie(1)];
 
   if (it.pro) {  // prologue: H0 hx, hy of plane pstart-1 at the edge columns
     const int s = cur.wait(B, S);
@@ -473,7 +489,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
       const float ca = CAC ? F[L::off_ca + r * BX + col] : 0.f;
       const float cb = CBC ? F[L::off_cb + r * BX + col] : 0.f;
       float ox, oy, oz;
-      e_update1<CAC, CBC>(co, g, i, j, p + g.zoff, co.cdy_e[max(j, 0)], co.cdz_e[p], co.cdx_e[max(i, 0)], ca,
+      e_update1<CAC, CBC>(co, g, i, j, p + g.zoff, cdy1, co.cdz_e[p], cdx1, ca,
                           cb, Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], hx, hy, hz, Fr[3 * kTB2SlotF - BX],
                           Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1], Fr[5 * kTB2SlotF - 1],
                           *B.H0e((p - 1) & 1, 0, r, e1i), *B.H0e((p - 1) & 1, 1, r, e1i), ox, oy, oz);
@@ -504,7 +520,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
       const int r = e2r, col = ce(e2i), i = ie(e2i), j = it.y0 - 1 + r;
       const float A = DAC ? *B.De(hb, 0, r, e2i) : co.da_s;
       const float Bq = DBC ? *B.De(hb, 1, r, e2i) : 0.f;
-      const float cdz_h = co.cdz_h[kh], cdy_h = co.cdy_h[max(j, 0)], cdx = co.cdx_h[max(i, 0)];
+      const float cdz_h = co.cdz_h[kh], cdy_h = cdy2, cdx = cdx2;
       const float ex_h = *B.E1(hb, 0, r, col), ey_h = *B.E1(hb, 1, r, col), ez_h = *B.E1(hb, 2, r, col);
       // E1(p) at this column (z+1 neighbour); in the top drain plane p = nz
       // it is the PEC zero, not the stale buffer content
@@ -522,7 +538,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
     if (l3_lane && kh >= it.kz0 && kh <= it.up) {
       const int r = e3r, i = ie(1), j = it.y0 - 1 + r;
       float ox, oy, oz;
-      e_update1<CAC, CBC>(co, g, i, j, kh + g.zoff, co.cdy_e[max(j, 0)], co.cdz_e[kh], co.cdx_e[i],
+      e_update1<CAC, CBC>(co, g, i, j, kh + g.zoff, cdy3, co.cdz_e[kh], cdx3,
                           *B.Ce(hb, 0, r), *B.Ce(hb, 1, r), *B.E1(hb, 0, r, CR), *B.E1(hb, 1, r, CR),
                           *B.E1(hb, 2, r, CR), *B.H1(hb, 0, r, CR), *B.H1(hb, 1, r, CR), *B.H1(hb, 2, r, CR),
                           *B.H1(hb, 0, r - 1, CR), *B.H1(hb, 2, r - 1, CR), *B.H1(hb, 1, r, CR - 1),
