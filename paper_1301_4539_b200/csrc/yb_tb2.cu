@@ -38,6 +38,13 @@ constexpr int CL = 3, CR = 4 + kTX;  // edge columns x0-1, x0+128 (and CR+1)
 
 constexpr int kConsumers = 32 * (RW + 1);  // row warps + edge warp
 
+// A consumer warp is done reading a stage: every lane's loads have been
+// consumed, lane 0 arrives on the stage's "empty" barrier (count RW + 1).
+__device__ __forceinline__ void release_stage(uint64_t* empty, int s, int l) {
+  __syncwarp();
+  if (l == 0) mbar_arrive(smem_u32(&empty[s]));
+}
+
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
@@ -270,8 +277,7 @@ struct Rows {
     const float* F = B.stages + (size_t)s * L::floats + rs * BX + c;
     h0p.x = lds4(F + 3 * kTB2SlotF);
     h0p.y = lds4(F + 4 * kTB2SlotF);
-    consumer_sync();
-    if (er == 0 && l == 0) mbar_arrive(smem_u32(&B.empty[s]));
+    release_stage(B.empty, s, l);
   }
 
   // one wavefront plane p (buffers alternate with the plane parity)
@@ -318,8 +324,10 @@ struct Rows {
       sts4(w + E1C, e1c.y);
       sts4(w + 2 * E1C, e1c.z);
     }
-    consumer_sync();  // (A) E1(p) complete, stage free
-    if (l1 && er == 0 && l == 0) mbar_arrive(smem_u32(&B.empty[s1]));
+    // No CTA barrier between L1 and L2: L2 reads E1(p-1) (ordered by the
+    // previous plane's barrier B) and its own row of E1(p) from registers;
+    // the only shared resource L1 frees is the stage.
+    if (l1) release_stage(B.empty, s1, l);
 
     // ----------------------------------------------------- L2: H1(p-1)
     const int kh = p - 1;
@@ -475,7 +483,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
     const int pb = (it.pstart - 1) & 1;
     *B.H0e(pb, 0, e1r, e1i) = F[3 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
     *B.H0e(pb, 1, e1r, e1i) = F[4 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
-    consumer_sync();
+    release_stage(B.empty, s, l);
   }
 
   for (int p = it.pstart; p <= it.pend; ++p) {
@@ -512,8 +520,9 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
         *B.Ce(p & 1, 0, r) = ca;
         *B.Ce(p & 1, 1, r) = cb;
       }
+      release_stage(B.empty, s1, l);
     }
-    consumer_sync();  // (A)
+    __syncwarp();  // L1 lane tasks hand E1 / H0e / De / Ce over to the L2 / L3 lanes
 
     const int kh = p - 1, hb = kh & 1;
     if (l2_lane && kh >= it.pstart && kh <= it.up) {
@@ -586,7 +595,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_u32(&B.full[s]), 1);
-      mbar_init(smem_u32(&B.empty[s]), 1);
+      mbar_init(smem_u32(&B.empty[s]), RW + 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
