@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define YB_ABI_VERSION 1
+#define YB_ABI_VERSION 2
 
 /* Status codes. The shim maps INVALID_ARGUMENT -> std::invalid_argument,
  * OUT_OF_RANGE -> std::out_of_range, the rest -> std::runtime_error. */
@@ -81,6 +81,8 @@ typedef struct {
   double bytes_per_cell_update; /* algorithmic HBM bytes per cell-update, one sweep */
   size_t device_bytes;     /* device memory held by the handle */
   int halo_depth;          /* z-slab mode: ghost planes refreshed per exchange = steps per exchange */
+  int quiescent_skip;      /* yb_set_quiescent_skip state */
+  int64_t skipped_items;   /* work items skipped as quiescent (RunStats::skipped_tiles analogue) */
 } yb_info;
 
 /* Last error message of the calling thread ("" if none). */
@@ -169,6 +171,15 @@ int yb_read_probes(yb_sim* sim, int64_t* steps, int* probe, float* values, int64
  * sum covers the planes the slab owns (sum over ranks for the total). */
 int yb_snapshot_h(yb_sim* sim);
 int yb_total_energy(yb_sim* sim, const double* dx, const double* dy, const double* dz, double* energy);
+
+/* Quiescent skip (runner.hpp:60-73, :287-313; RunOptions::quiescent_skip):
+ * when on, a sweep work item whose whole input box is exactly +0 in both
+ * state buffers and touches no active source is not computed (its result is
+ * +0 bit for bit). Tracked as one bit per (tile, plane), set once the
+ * tile-plane may hold a nonzero value; rebuilt by a device scan after any
+ * host-side change of the state. Results are identical with it on or off.
+ * Default off. The naive variant ignores it. */
+int yb_set_quiescent_skip(yb_sim* sim, int on);
 
 /* Simulation::run(n) time loop (runner.hpp:243-266) with the Standard step
  * (schedule.hpp:171-210): advances step_index by n. Asynchronous on the

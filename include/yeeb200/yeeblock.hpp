@@ -336,7 +336,7 @@ template <class Real>
 struct RunOptions {
   std::vector<SourceSpec> sources;
   std::vector<ProbeSpec> probes;
-  bool quiescent_skip = true;  // accepted; the GPU path always updates every DoF
+  bool quiescent_skip = true;  // skip all-zero work items (runner.hpp:60-73); results unchanged
   int device = 0;
   int variant = YB_VARIANT_FUSED;
   std::function<void(const FieldSet<Real>&, long long)> after_step;
@@ -367,6 +367,7 @@ class Simulation {
     d.variant = opts_.variant;
     detail::check(yb_create(&d, &h_));
     detail::check(yb_set_axis_coeffs(h_, coeffs_.cdx.data(), coeffs_.cdy.data(), coeffs_.cdz.data()));
+    detail::check(yb_set_quiescent_skip(h_, opts_.quiescent_skip ? 1 : 0));
     if (!opts_.probes.empty()) {  // sampled on the device (sample_probes, probe.hpp:36-51)
       std::vector<int> c, i, j, k, st;
       for (const ProbeSpec& p : opts_.probes) {
@@ -438,6 +439,9 @@ class Simulation {
     have_mirror_ = false;
     stats_.total_seconds += now() - t0;
     stats_.steps += n_steps;
+    yb_info inf{};
+    detail::check(yb_get_info(h_, &inf));
+    stats_.skipped_tiles = inf.skipped_items;
     return records;
   }
 

@@ -19,7 +19,8 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libyeeb200.so")
+# YB_LIB: an alternative build of the same library (A/B of kernel variants)
+LIB_PATH = os.environ.get("YB_LIB") or os.path.join(HERE, "libyeeb200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 EX, EY, EZ, HX, HY, HZ = range(6)
@@ -39,7 +40,7 @@ ABI_SYMBOLS = (
     "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
     "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
-    "yb_snapshot_h", "yb_total_energy",
+    "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip",
 )
 
 
@@ -67,7 +68,7 @@ class Info(C.Structure):
                 ("n_cell_arrays", C.c_int), ("variant", C.c_int), ("stages", C.c_int),
                 ("grid_x", C.c_int), ("grid_y", C.c_int), ("grid_z", C.c_int), ("zchunk", C.c_int),
                 ("bytes_per_cell_update", C.c_double), ("device_bytes", C.c_size_t),
-                ("halo_depth", C.c_int)]
+                ("halo_depth", C.c_int), ("quiescent_skip", C.c_int), ("skipped_items", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -125,6 +126,7 @@ def lib():
         L.yb_read_probes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int), _f32p, C.c_int64,
                                      C.POINTER(C.c_int64)]
         L.yb_snapshot_h.argtypes = [vp]
+        L.yb_set_quiescent_skip.argtypes = [vp, C.c_int]
         L.yb_total_energy.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
@@ -322,6 +324,11 @@ class Simulation:
                                     pr.ctypes.data_as(C.POINTER(C.c_int)), _fp(va), capacity, C.byref(n)))
         k = n.value
         return st[:k].copy(), pr[:k].copy(), va[:k].copy()
+
+    def set_quiescent_skip(self, on=True):
+        """Skip work items whose input box is all +0 (runner.hpp:60-73);
+        results are unchanged. info()['skipped_items'] counts them."""
+        _check(lib().yb_set_quiescent_skip(self._h, 1 if on else 0))
 
     def snapshot_h(self):
         """HSnapshot of the current H on the device (fields.hpp:71-82)."""

@@ -189,6 +189,27 @@ __global__ void k_all_equal(const float* __restrict__ a, long long n, int* flag)
   if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0) atomicExch(flag, 0);
 }
 
+// One block per (tile, plane): 8 warps over the tile's rows, lanes over its
+// columns (float4); the last tile column / row also covers the padding and
+// the i = nx / j = ny faces.
+__global__ void __launch_bounds__(256) k_qscan(Geo g, Fields A, Fields Bf, QMap q, int k0) {
+  const int tile = blockIdx.x, k = k0 + (int)blockIdx.y;
+  const int tx = tile % q.ntx, ty = tile / q.ntx;
+  const int x0 = tx * kTX, y0 = ty * 8;
+  const int xe = tx == q.ntx - 1 ? g.PX : x0 + kTX, ye = ty == q.nty - 1 ? g.PY : y0 + 8;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  bool nz = false;
+  for (int j = y0 + w; j < ye; j += 8)
+    for (int i = x0 + 4 * l; i < xe; i += 128) {
+      const long long p = ((long long)k * g.PY + j) * g.PX + i;
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        nz |= nonzero4(*reinterpret_cast<const float4*>(A.f[c] + p)) |
+              nonzero4(*reinterpret_cast<const float4*>(Bf.f[c] + p));
+    }
+  if (__syncthreads_or(nz) && threadIdx.x == 0) qmap_mark(q, tile, k);
+}
+
 __global__ void k_fill_value(float* p, long long n, float v) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     p[t] = v;
@@ -311,6 +332,13 @@ cudaError_t launch_gather_dense(const Geo& g, const int* e, const float* padded,
                                 cudaStream_t st) {
   k_gather_dense<<<dim3((e[0] + 127) / 128, e[1], e[2]), 128, 0, st>>>(g, e[0], e[1], e[2], padded,
                                                                        dense);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qscan(const Geo& g, const Fields& a, const Fields& b, const QMap& q, int k0, int k1,
+                         cudaStream_t st) {
+  if (k1 < k0) return cudaSuccess;
+  k_qscan<<<dim3(q.ntx * q.nty, k1 - k0 + 1), 256, 0, st>>>(g, a, b, q, k0);
   return cudaGetLastError();
 }
 

@@ -124,6 +124,11 @@ struct yb_sim {
   bool have_snap = false;
   double* energy_dev = nullptr;  // weights | partials | result
   int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
+  bool qskip = false;         // yb_set_quiescent_skip
+  bool q_valid = false;       // quiescent map matches the state buffers
+  unsigned* qbits = nullptr;  // quiescent map (tiles x words)
+  int qwords = 0, qtiles = 0;
+  unsigned long long* qskipped = nullptr;  // device counter of skipped items
 };
 
 namespace {
@@ -310,6 +315,39 @@ yb::SrcArgs sources_at(const yb_sim* s, int64_t step, bool two = false) {
   return a;
 }
 
+// Quiescent map for the sweep kernels (nullptr bits when skipping is off).
+yb::QMap qmap_of(const yb_sim* s) {
+  yb::QMap q{};
+  q.ntx = s->ntx;
+  q.nty = s->nty;
+  q.words = s->qwords;
+  q.bits = s->qskip ? s->qbits : nullptr;
+  return q;
+}
+
+// (Re)builds the quiescent map from both state buffers when it is stale.
+int qmap_refresh(yb_sim* s) {
+  if (!s->qskip || s->q_valid) return YB_OK;
+  const int planes = s->g.nz + 2 * yb::kGhost;  // local planes -kGhost .. nz+kGhost-1
+  const int words = (planes + 31) / 32, tiles = s->ntx * s->nty;
+  if (words != s->qwords || tiles != s->qtiles) {
+    cudaFree(s->qbits);
+    s->qbits = nullptr;
+    YB_CU(cudaMalloc(&s->qbits, (size_t)tiles * words * 4));
+    s->qwords = words;
+    s->qtiles = tiles;
+  }
+  if (!s->qskipped) {
+    YB_CU(cudaMalloc(&s->qskipped, sizeof(unsigned long long)));
+    YB_CU(cudaMemsetAsync(s->qskipped, 0, sizeof(unsigned long long), s->stream));
+  }
+  YB_CU(cudaMemsetAsync(s->qbits, 0, (size_t)tiles * words * 4, s->stream));
+  YB_CU(yb::launch_qscan(s->g, fields_of(s, 0), fields_of(s, 1), qmap_of(s), -yb::kGhost,
+                         s->g.nz + yb::kGhost - 1, s->stream));
+  s->q_valid = true;
+  return YB_OK;
+}
+
 int collect_timers(yb_sim* s) {
   if (s->timers_used == 0) return YB_OK;
   YB_CU(cudaStreamSynchronize(s->stream));
@@ -341,6 +379,8 @@ int step_fused(yb_sim* s) {
     a.out[c] = s->buf[nxt][c];
   }
   a.src = sources_at(s, s->step_index);
+  a.qm = qmap_of(s);
+  a.skipped = s->qskipped;
   const int mask = cell_mask(s);
   const size_t smem = yb::fused_smem_bytes(6 + popcount4(mask), s->stages);
   TimerPair* tp = nullptr;
@@ -382,6 +422,8 @@ int step_tb2(yb_sim* s) {
     a.out[c] = s->buf[nxt][c];
   }
   a.src = sources_at(s, s->step_index, true);
+  a.qm = qmap_of(s);
+  a.skipped = s->qskipped;
   const int mask = cell_mask(s);
   const size_t smem = yb::tb2_smem_bytes(mask, s->stages2);
   TimerPair* tp = nullptr;
@@ -572,6 +614,8 @@ int yb_destroy(yb_sim* s) {
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
   cudaFree(s->probe_dev);
+  cudaFree(s->qbits);
+  cudaFree(s->qskipped);
   for (float* p : s->snap_h) cudaFree(p);
   cudaFree(s->energy_dev);
   for (auto& t : s->timers) {
@@ -799,6 +843,7 @@ int yb_upload_field(yb_sim* s, int comp, const float* dense) {
   if (!s || !dense) return fail(YB_INVALID_ARGUMENT, "null argument");
   if (int rc = check_comp(comp)) return rc;
   YB_CU(cudaSetDevice(s->device));
+  s->q_valid = false;
   return copy_dense(s, comp, s->buf[s->cur][comp], dense, nullptr);
 }
 
@@ -815,6 +860,7 @@ int yb_zero_fields(yb_sim* s) {
   for (int c = 0; c < 6; ++c)
     YB_CU(cudaMemsetAsync(s->buf[s->cur][c] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   s->step_index = 0;
+  s->q_valid = false;
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
 }
@@ -824,6 +870,7 @@ int yb_fill_fields(yb_sim* s, uint64_t seed) {
   YB_CU(cudaSetDevice(s->device));
   YB_CU(yb::launch_fill_fields(s->g, fields_of(s, s->cur), seed, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
+  s->q_valid = false;
   return YB_OK;
 }
 
@@ -907,8 +954,10 @@ int yb_advance(yb_sim* s, int64_t nsteps) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
   YB_CU(cudaSetDevice(s->device));
-  if (s->variant != YB_VARIANT_NAIVE)
+  if (s->variant != YB_VARIANT_NAIVE) {
     if (int rc = prepare_fused(s)) return rc;
+    if (int rc = qmap_refresh(s)) return rc;
+  }
   const bool probes = !s->probes.empty();
   for (int64_t t = 0; t < nsteps;) {
     // two steps per launch unless a probe wants the level in between
@@ -1068,6 +1117,7 @@ int yb_apply_ampere_range(yb_sim* s, const int* box) {
   int b[6];
   if (int rc = check_box(s, box, b)) return fail(rc, "apply_ampere_range: range out of bounds");
   YB_CU(cudaSetDevice(s->device));
+  s->q_valid = false;
   YB_CU(yb::launch_naive_ampere(s->g, fields_of(s, s->cur), coef_args(s), b, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
@@ -1079,6 +1129,7 @@ int yb_apply_faraday_range(yb_sim* s, const int* box) {
   int b[6];
   if (int rc = check_box(s, box, b)) return fail(rc, "apply_faraday_range: range out of bounds");
   YB_CU(cudaSetDevice(s->device));
+  s->q_valid = false;
   YB_CU(yb::launch_naive_faraday(s->g, fields_of(s, s->cur), coef_args(s), b, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
@@ -1088,6 +1139,7 @@ int yb_apply_pec_boundary(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   YB_CU(cudaSetDevice(s->device));
+  s->q_valid = false;
   YB_CU(yb::launch_naive_pec(s->g, fields_of(s, s->cur), s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
@@ -1167,7 +1219,20 @@ int yb_halo_pack(yb_sim* s, int side, void* dst) {
 
 int yb_halo_unpack(yb_sim* s, int side, const void* src) {
   if (!s || !src || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
-  return halo_copy(s, side, const_cast<char*>(static_cast<const char*>(src)), false);
+  if (int rc = halo_copy(s, side, const_cast<char*>(static_cast<const char*>(src)), false)) return rc;
+  if (s->qskip && s->q_valid) {  // the ghost planes just written: mark the nonzero tile-planes
+    const int d = halo_depth(s);
+    const int k0 = side == 0 ? -d : s->g.nz, k1 = side == 0 ? -1 : s->g.nz + d - 1;
+    YB_CU(yb::launch_qscan(s->g, fields_of(s, 0), fields_of(s, 1), qmap_of(s), k0, k1, s->stream));
+  }
+  return YB_OK;
+}
+
+int yb_set_quiescent_skip(yb_sim* s, int on) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  s->qskip = on != 0;
+  s->q_valid = false;
+  return YB_OK;
 }
 
 int yb_set_stream(yb_sim* s, void* stream) {
@@ -1215,6 +1280,13 @@ int yb_get_info(yb_sim* s, yb_info* info) {
   }
   info->device_bytes = s->dev_bytes;
   info->halo_depth = halo_depth(s);
+  info->quiescent_skip = s->qskip ? 1 : 0;
+  if (s->qskipped) {
+    unsigned long long v = 0;
+    YB_CU(cudaMemcpyAsync(&v, s->qskipped, sizeof v, cudaMemcpyDeviceToHost, s->stream));
+    YB_CU(cudaStreamSynchronize(s->stream));
+    info->skipped_items = (int64_t)v;
+  }
   return YB_OK;
 }
 

@@ -75,6 +75,52 @@ __device__ __forceinline__ float yee_upd_t(float A, float v, float C1, float a, 
   return __fadd_rn(v, __fsub_rn(t1, t2));
 }
 
+// Quiescent map (yb_set_quiescent_skip): bit (tile, plane) set once that
+// tile-plane may hold a nonzero DoF in either state buffer. Tiles are the
+// kTX x 8 sweep tiles (the last tile column / row also owns the i = nx /
+// j = ny faces); planes are local, -kGhost .. nz + kGhost - 1.
+struct QMap {
+  unsigned* bits;  // nullptr: skipping off
+  int words;       // 32-bit words per tile
+  int ntx, nty;
+};
+
+__device__ __forceinline__ void qmap_mark(const QMap& q, int tile, int k) {
+  const int b = k + kGhost;
+  atomicOr(&q.bits[(size_t)tile * q.words + (b >> 5)], 1u << (b & 31));
+}
+
+// any bit set for tiles tx-1..tx+1 x ty-1..ty+1 and planes k0..k1?
+__device__ __forceinline__ bool qmap_dirty(const QMap& q, int tx, int ty, int k0, int k1) {
+  const int b0 = k0 + kGhost, b1 = k1 + kGhost;
+  for (int y = max(ty - 1, 0); y <= min(ty + 1, q.nty - 1); ++y)
+    for (int x = max(tx - 1, 0); x <= min(tx + 1, q.ntx - 1); ++x) {
+      const unsigned* w = q.bits + (size_t)(y * q.ntx + x) * q.words;
+      for (int wi = b0 >> 5; wi <= (b1 >> 5); ++wi) {
+        unsigned m = __ldcg(w + wi);
+        if (wi == (b0 >> 5)) m &= ~0u << (b0 & 31);
+        if (wi == (b1 >> 5) && (b1 & 31) != 31) m &= (1u << ((b1 & 31) + 1)) - 1u;
+        if (m) return true;
+      }
+    }
+  return false;
+}
+
+// any source listed for this launch inside the box [x0,x1] x [y0,y1] x [k0,k1]
+__device__ __forceinline__ bool src_in_box(const SrcArgs& s, int x0, int x1, int y0, int y1, int k0, int k1) {
+  for (int q = 0; q < s.n; ++q)
+    if (s.act[q] && s.i[q] >= x0 && s.i[q] <= x1 && s.j[q] >= y0 && s.j[q] <= y1 && s.k[q] >= k0 &&
+        s.k[q] <= k1)
+      return true;
+  return false;
+}
+
+__device__ __forceinline__ bool nonzero4(float4 v) {
+  return (__float_as_uint(v.x) | __float_as_uint(v.y) | __float_as_uint(v.z) | __float_as_uint(v.w)) != 0u;
+}
+
+constexpr int kSkipItem = 1 << 30;  // item_q flag: the item is quiescent, no data staged
+
 __device__ __forceinline__ long long gidx(const Geo& g, int i, int j, int k) {
   return ((long long)k * g.PY + j) * g.PX + i;
 }

@@ -33,7 +33,7 @@
 namespace yb {
 namespace {
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fused(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm) {
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
@@ -91,12 +91,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
           return;
         }
-        p_item = it;
-        p_e = 0;
         const int kz0 = (it / T) * a.zchunk;
         const int kz1 = min(kz0 + a.zchunk, g.nz);
         const bool pro = kz0 > 0 || !at_bottom(g);
         const int kend = (kz1 == g.nz && at_top(g)) ? g.nz - 1 : kz1;
+        if (QS) {  // quiescent item: input box all +0, no source -> skip
+          const int tl = it % T, tx = tl % a.ntx, ty = tl / a.ntx;
+          const int x0 = tx * kTX, y0 = ty * kTY;
+          if (!src_in_box(a.src, x0 - 4, x0 + kTX + 3, y0 - 1, y0 + kTY, kz0 - 1, kend) &&
+              !qmap_dirty(a.qm, tx, ty, kz0 - 1, kend)) {
+            item_q[(p_seq - 1) % kQ] = it | kSkipItem;
+            atomicAdd(a.skipped, 1ull);
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+            continue;  // the item occupies this one (empty) stage
+          }
+        }
+        p_item = it;
+        p_e = 0;
         p_nE = (pro ? 1 : 0) + kend - kz0 + 1;
       }
       const int chunk = p_item / T, tile = p_item - chunk * T;
@@ -153,6 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int item = item_q[c_seq % kQ];
     ++c_seq;
     if (item < 0) break;
+    if (QS && (item & kSkipItem)) {  // quiescent: consume the empty stage, nothing to write
+      release(wait_elem());
+      continue;
+    }
     const int chunk = item / T, tile = item - chunk * T;
     const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
     const int kz0 = chunk * a.zchunk;
@@ -203,6 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         store_row4(a.out[4], p, i0, g.nx, hy, st_pol);
         store_row4(a.out[5], p, i0, g.nx, hz, st_pol);
       }
+      if (QS && __any_sync(~0u, jlt && (nonzero4(hx) | nonzero4(hy) | nonzero4(hz))) && l == 0)
+        qmap_mark(a.qm, tile, kh);
     };
 
     if (kz0 > 0 || !at_bottom(g)) {  // prologue element: H^{n+1/2} on plane kz0-1
@@ -320,6 +337,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         store_row4(a.out[1], p, i0, g.nx, eyw, st_pol);
         store_row4(a.out[2], p, i0, g.nx, ezw, st_pol);
       }
+      if (QS && k < kz1 &&
+          __any_sync(~0u, jlt && (nonzero4(exw) | nonzero4(eyw) | nonzero4(ezw))) && l == 0)
+        qmap_mark(a.qm, tile, k);
       if (k > kz0) h_row(k - 1, exw, eyw);
       pex = exw;
       pey = eyw;
@@ -341,36 +361,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 cudaError_t launch_t(const FusedArgs& a, const TMaps& tm, dim3 grid, size_t smem, cudaStream_t st) {
-  k_fused<CAC, CBC, DAC, DBC><<<grid, kThreads, smem, st>>>(a, tm);
+  k_fused<CAC, CBC, DAC, DBC, QS><<<grid, kThreads, smem, st>>>(a, tm);
   return cudaGetLastError();
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 cudaError_t set_limit_t() {
-  return cudaFuncSetAttribute(k_fused<CAC, CBC, DAC, DBC>,
+  return cudaFuncSetAttribute(k_fused<CAC, CBC, DAC, DBC, QS>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 using LaunchFn = cudaError_t (*)(const FusedArgs&, const TMaps&, dim3, size_t, cudaStream_t);
 using LimitFn = cudaError_t (*)();
 
-#define YB_T(m) launch_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
-#define YB_L(m) set_limit_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
-const LaunchFn kLaunch[16] = {YB_T(0),  YB_T(1),  YB_T(2),  YB_T(3), YB_T(4),  YB_T(5),
-                              YB_T(6),  YB_T(7),  YB_T(8),  YB_T(9), YB_T(10), YB_T(11),
-                              YB_T(12), YB_T(13), YB_T(14), YB_T(15)};
-const LimitFn kLimit[16] = {YB_L(0),  YB_L(1),  YB_L(2),  YB_L(3), YB_L(4),  YB_L(5),
-                            YB_L(6),  YB_L(7),  YB_L(8),  YB_L(9), YB_L(10), YB_L(11),
-                            YB_L(12), YB_L(13), YB_L(14), YB_L(15)};
+#define YB_T(m) launch_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m & 16) != 0>
+#define YB_L(m) set_limit_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m & 16) != 0>
+const LaunchFn kLaunch[32] = {YB_T(0),  YB_T(1),  YB_T(2),  YB_T(3),  YB_T(4),  YB_T(5),  YB_T(6),  YB_T(7),
+                              YB_T(8),  YB_T(9),  YB_T(10), YB_T(11), YB_T(12), YB_T(13), YB_T(14), YB_T(15),
+                              YB_T(16), YB_T(17), YB_T(18), YB_T(19), YB_T(20), YB_T(21), YB_T(22), YB_T(23),
+                              YB_T(24), YB_T(25), YB_T(26), YB_T(27), YB_T(28), YB_T(29), YB_T(30), YB_T(31)};
+const LimitFn kLimit[32] = {YB_L(0),  YB_L(1),  YB_L(2),  YB_L(3),  YB_L(4),  YB_L(5),  YB_L(6),  YB_L(7),
+                            YB_L(8),  YB_L(9),  YB_L(10), YB_L(11), YB_L(12), YB_L(13), YB_L(14), YB_L(15),
+                            YB_L(16), YB_L(17), YB_L(18), YB_L(19), YB_L(20), YB_L(21), YB_L(22), YB_L(23),
+                            YB_L(24), YB_L(25), YB_L(26), YB_L(27), YB_L(28), YB_L(29), YB_L(30), YB_L(31)};
 #undef YB_T
 #undef YB_L
 
 }  // namespace
 
 cudaError_t fused_set_smem_limits() {
-  for (int m = 0; m < 16; ++m) {
+  for (int m = 0; m < 32; ++m) {
     const cudaError_t e = kLimit[m]();
     if (e != cudaSuccess) return e;
   }
@@ -379,7 +401,7 @@ cudaError_t fused_set_smem_limits() {
 
 cudaError_t launch_fused(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid,
                          size_t smem, cudaStream_t st) {
-  return kLaunch[cell_mask & 15](a, tm, grid, smem, st);
+  return kLaunch[(cell_mask & 15) | (a.qm.bits ? 16 : 0)](a, tm, grid, smem, st);
 }
 
 }  // namespace yb

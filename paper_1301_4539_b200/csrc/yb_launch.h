@@ -68,6 +68,8 @@ struct FusedArgs {
   const float* in[6];
   float* out[6];
   SrcArgs src;
+  QMap qm;                       // quiescent map (qm.bits == nullptr: off)
+  unsigned long long* skipped;   // skipped-item counter
 };
 
 // smem bytes of the fused kernel for `narr` staged arrays and `stages` ring depth.
@@ -105,6 +107,10 @@ struct ProbeArgs {
   int comp[64];
   long long off[64];
 };
+// Sets the quiescent bit of every (tile, plane k in [k0, k1]) holding a
+// nonzero DoF in either state buffer.
+cudaError_t launch_qscan(const Geo& g, const Fields& a, const Fields& b, const QMap& q, int k0, int k1,
+                         cudaStream_t st);
 cudaError_t launch_fill_value(float* p, long long n, float v, cudaStream_t st);
 cudaError_t launch_probes(const Fields& F, const ProbeArgs& pa, float* out, cudaStream_t st);
 // weights: x node[nx+1], x cell[nx], y node[ny+1], y cell[ny], z node[nz+1], z cell[nz]

@@ -229,7 +229,7 @@ struct Cursor {
 // plane parity) plus a compile-time offset; the i-1 /
 // i+1 neighbours of a lane's float4 are read as one scalar from the row in
 // shared memory (column c-1 / c+4; the edge columns for lanes 0 / 31).
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 struct Rows {
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   static constexpr int E1C = RW * BX, E1B = 3 * E1C;              // comp / buffer strides
@@ -383,11 +383,16 @@ struct Rows {
       sts4(w, e2c.x);
       sts4(w + E2C, e2c.y);
       sts4(w + 2 * E2C, e2c.z);
-      if (er <= kTB2Rows && j < g.ny && kh < it.kz1) {  // E^{n+2} of the owned rows -> HBM
+      const bool own = er <= kTB2Rows && j < g.ny && kh < it.kz1;
+      if (own) {  // E^{n+2} of the owned rows -> HBM
         const long long gp = gidx(g, i0, j, kh);
         store_row4(a.out[0], gp, i0, g.nx, e2c.x, st_pol);
         store_row4(a.out[1], gp, i0, g.nx, e2c.y, st_pol);
         store_row4(a.out[2], gp, i0, g.nx, e2c.z, st_pol);
+      }
+      if (QS) {
+        const bool nz = own && (nonzero4(e2c.x) | nonzero4(e2c.y) | nonzero4(e2c.z));
+        if (__any_sync(~0u, nz) && l == 0) qmap_mark(a.qm, (it.y0 / kTB2Rows) * a.ntx + it.x0 / kTX, kh);
       }
     }
 
@@ -421,6 +426,10 @@ struct Rows {
         store_row4(a.out[4], gp, i0, g.nx, h2.y, st_pol);
         store_row4(a.out[5], gp, i0, g.nx, h2.z, st_pol);
       }
+      if (QS && j < g.ny) {
+        const bool nz = nonzero4(h2.x) | nonzero4(h2.y) | nonzero4(h2.z);
+        if (__any_sync(~0u, nz) && l == 0) qmap_mark(a.qm, (it.y0 / kTB2Rows) * a.ntx + it.x0 / kTX, k4);
+      }
     }
     // ---------------------------------------------------------- rotate
     ze1 = ze;
@@ -439,10 +448,10 @@ struct Rows {
   }
 };
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
                                          int er, int l, uint64_t st_pol) {
-  Rows<CAC, CBC, DAC, DBC> R(a, it, B, cur, er, l, st_pol);
+  Rows<CAC, CBC, DAC, DBC, QS> R(a, it, B, cur, er, l, st_pol);
   if (it.pro) R.prologue();
   for (int p = it.pstart; p <= it.pend; ++p) R.plane(p);
 }
@@ -453,7 +462,7 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
 // level — L1: 11 + 11 + 10 = 32 tasks, L2: 20, L3: 9 — and all state that
 // crosses planes (H0, Da/Db, Ca/Cb of these columns) lives in shared memory
 // (Bufs::h0e/de/cee), so any lane can pick up any task.
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
                                          int l) {
   using L = StageLayout<CAC, CBC, DAC, DBC>;
@@ -567,7 +576,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
   }
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm) {
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
@@ -626,9 +635,20 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
           mbar_arrive(bar);
           return;
         }
+        const Item pi = make_item(g, it, T, a.ntx, a.zchunk);
+        if (QS) {  // quiescent item: input box all +0, no source in either step -> skip
+          const int tl = it % T;
+          const int k0 = pi.pro ? pi.pstart - 1 : pi.pstart;
+          if (!src_in_box(a.src, pi.x0 - 4, pi.x0 + kTX + 3, pi.y0 - 2, pi.y0 + kTB2Rows + 1, k0, pi.pin_end) &&
+              !qmap_dirty(a.qm, tl % a.ntx, tl / a.ntx, k0, pi.pin_end)) {
+            item_q[(p_seq - 1) % kQ] = it | kSkipItem;
+            atomicAdd(a.skipped, 1ull);
+            mbar_arrive(bar);
+            continue;  // the item occupies this one (empty) stage
+          }
+        }
         p_item = it;
         p_e = 0;
-        const Item pi = make_item(g, it, T, a.ntx, a.zchunk);
         p_nE = (pi.pro ? 1 : 0) + pi.pin_end - pi.pstart + 1;
       }
       const Item pi = make_item(g, p_item, T, a.ntx, a.zchunk);
@@ -667,45 +687,51 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
     const int item = item_q[c_seq % kQ];
     ++c_seq;
     if (item < 0) break;
+    if (QS && (item & kSkipItem)) {  // quiescent: consume the empty stage, nothing to write
+      release_stage(B.empty, cur.wait(B, S), l);
+      continue;
+    }
     Item it = make_item(g, item, T, a.ntx, a.zchunk);
     mark_sources(a.src, it);
     if (w == EDGE)
-      tb2_edge<CAC, CBC, DAC, DBC>(a, it, B, cur, l);
+      tb2_edge<CAC, CBC, DAC, DBC, QS>(a, it, B, cur, l);
     else
-      tb2_rows<CAC, CBC, DAC, DBC>(a, it, B, cur, w, l, st_pol);
+      tb2_rows<CAC, CBC, DAC, DBC, QS>(a, it, B, cur, w, l, st_pol);
   }
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 cudaError_t launch_t(const FusedArgs& a, const TMaps& tm, dim3 grid, size_t smem, cudaStream_t st) {
-  k_tb2<CAC, CBC, DAC, DBC><<<grid, kTB2Threads, smem, st>>>(a, tm);
+  k_tb2<CAC, CBC, DAC, DBC, QS><<<grid, kTB2Threads, smem, st>>>(a, tm);
   return cudaGetLastError();
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC>
+template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
 cudaError_t set_limit_t() {
-  return cudaFuncSetAttribute(k_tb2<CAC, CBC, DAC, DBC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_tb2<CAC, CBC, DAC, DBC, QS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               227 * 1024);
 }
 
 using LaunchFn = cudaError_t (*)(const FusedArgs&, const TMaps&, dim3, size_t, cudaStream_t);
 using LimitFn = cudaError_t (*)();
 
-#define YB_T(m) launch_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
-#define YB_L(m) set_limit_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
-const LaunchFn kLaunch[16] = {YB_T(0),  YB_T(1),  YB_T(2),  YB_T(3), YB_T(4),  YB_T(5),
-                              YB_T(6),  YB_T(7),  YB_T(8),  YB_T(9), YB_T(10), YB_T(11),
-                              YB_T(12), YB_T(13), YB_T(14), YB_T(15)};
-const LimitFn kLimit[16] = {YB_L(0),  YB_L(1),  YB_L(2),  YB_L(3), YB_L(4),  YB_L(5),
-                            YB_L(6),  YB_L(7),  YB_L(8),  YB_L(9), YB_L(10), YB_L(11),
-                            YB_L(12), YB_L(13), YB_L(14), YB_L(15)};
+#define YB_T(m) launch_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m & 16) != 0>
+#define YB_L(m) set_limit_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m & 16) != 0>
+const LaunchFn kLaunch[32] = {YB_T(0),  YB_T(1),  YB_T(2),  YB_T(3),  YB_T(4),  YB_T(5),  YB_T(6),  YB_T(7),
+                              YB_T(8),  YB_T(9),  YB_T(10), YB_T(11), YB_T(12), YB_T(13), YB_T(14), YB_T(15),
+                              YB_T(16), YB_T(17), YB_T(18), YB_T(19), YB_T(20), YB_T(21), YB_T(22), YB_T(23),
+                              YB_T(24), YB_T(25), YB_T(26), YB_T(27), YB_T(28), YB_T(29), YB_T(30), YB_T(31)};
+const LimitFn kLimit[32] = {YB_L(0),  YB_L(1),  YB_L(2),  YB_L(3),  YB_L(4),  YB_L(5),  YB_L(6),  YB_L(7),
+                            YB_L(8),  YB_L(9),  YB_L(10), YB_L(11), YB_L(12), YB_L(13), YB_L(14), YB_L(15),
+                            YB_L(16), YB_L(17), YB_L(18), YB_L(19), YB_L(20), YB_L(21), YB_L(22), YB_L(23),
+                            YB_L(24), YB_L(25), YB_L(26), YB_L(27), YB_L(28), YB_L(29), YB_L(30), YB_L(31)};
 #undef YB_T
 #undef YB_L
 
 }  // namespace
 
 cudaError_t tb2_set_smem_limits() {
-  for (int m = 0; m < 16; ++m) {
+  for (int m = 0; m < 32; ++m) {
     const cudaError_t e = kLimit[m]();
     if (e != cudaSuccess) return e;
   }
@@ -714,7 +740,7 @@ cudaError_t tb2_set_smem_limits() {
 
 cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid, size_t smem,
                        cudaStream_t st) {
-  return kLaunch[cell_mask & 15](a, tm, grid, smem, st);
+  return kLaunch[(cell_mask & 15) | (a.qm.bits ? 16 : 0)](a, tm, grid, smem, st);
 }
 
 }  // namespace yb

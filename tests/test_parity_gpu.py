@@ -416,3 +416,98 @@ def test_energy_slabs_sum(yb, oracle):
             total += s.total_energy(dz=dz)
     assert abs(total - want) <= 1e-12 * abs(want)
     assert abs(want - oracle.total_energy(nx, ny, nzg, f, prev[3:], dz=dz)) <= 1e-12 * abs(want)
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("shape,zchunk,medium", [((136, 72, 40), 4, (4, -1)), ((200, 40, 33), 0, (-1, -1)),
+                                                 ((64, 48, 40), 3, (2, 2)), ((37, 29, 23), 0, (7, 7))])
+def test_quiescent_skip_bit_exact(yb, oracle, variant, shape, zchunk, medium):
+    """runner.hpp:60-73: skipping all-zero work items changes nothing. A
+    point source in a zero field (the configs 1/2/4 situation), skip on vs
+    off vs the oracle; the skip must actually fire early on."""
+    nx, ny, nz = shape
+    steps = 23
+    tab = oracle.gauss_table(steps, t0=4.0, w=2.0)
+    src = (2, nx // 3, ny // 2, nz // 4, tab)
+    outs = []
+    for skip in (False, True):
+        with yb.Simulation(nx, ny, nz, variant=variant, zchunk=zchunk) as sim:
+            sim.generate_medium(*medium)
+            sim.add_source(*src)
+            sim.set_quiescent_skip(skip)
+            sim.run(steps)
+            outs.append(sim.download())
+            inf = sim.info()
+            assert inf["quiescent_skip"] == int(skip)
+            if skip and nx * ny * nz > 100000:
+                assert inf["skipped_items"] > 0
+    assert_bits(outs[1], outs[0], "skip vs no skip")
+    want = oracle_run(oracle, nx, ny, nz, oracle.zeros_state(nx, ny, nz), steps,
+                      medium=medium if medium != (-1, -1) else None, src=src)
+    assert_bits(outs[1], want, "skip vs oracle")
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+def test_quiescent_skip_stale_buffers(yb, oracle, variant):
+    """After a run leaves nonzero state in both buffers, an upload of a mostly
+    zero state must rebuild the quiescent map (both buffers are scanned): the
+    result equals a fresh simulation's."""
+    nx, ny, nz = 140, 40, 30
+    tab = oracle.gauss_table(12, t0=3.0, w=2.0)
+    f = oracle.zeros_state(nx, ny, nz)
+    f[2][5, 20, 70] = 1.0  # one nonzero Ez
+    with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+        sim.set_quiescent_skip(True)
+        sim.fill(9)
+        sim.run(7)  # both buffers now hold nonzero data everywhere
+        sim.upload(f)
+        sim.step_index = 0
+        sim.add_source(2, 100, 10, 25, tab)
+        sim.run(12)
+        got = sim.download()
+        assert sim.info()["skipped_items"] > 0
+    want = oracle_run(oracle, nx, ny, nz, [a.copy() for a in f], 12, src=(2, 100, 10, 25, tab))
+    assert_bits(got, want, "stale buffers")
+
+
+def test_quiescent_skip_slabs(yb, oracle):
+    """z-slabs with skipping on: ghost planes written by the halo exchange are
+    scanned into the map; the assembled result equals one domain."""
+    from paper_1301_4539_b200.slabs import partition
+    nx, ny, nzg, steps = 136, 40, 29, 11
+    tab = oracle.gauss_table(steps, t0=3.0, w=2.0)
+    src = (2, 60, 20, 13, tab)
+    for variant in (0, 2):
+        sims = []
+        for z0, n in partition(nzg, 3):
+            s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant)
+            s.generate_medium(3, -1)
+            s.add_source(*src)
+            s.set_quiescent_skip(True)
+            sims.append(s)
+        import torch
+        bufs = [(torch.empty(lo.halo_bytes(1, False), dtype=torch.uint8, device="cuda"),
+                 torch.empty(hi.halo_bytes(0, False), dtype=torch.uint8, device="cuda"))
+                for lo, hi in zip(sims[:-1], sims[1:])]
+        depth = sims[0].info()["halo_depth"]
+        done = 0
+        while done < steps:
+            n = min(depth, steps - done)
+            for (lo, hi), (up, down) in zip(zip(sims[:-1], sims[1:]), bufs):
+                lo.halo_pack(1, up.data_ptr())
+                hi.halo_pack(0, down.data_ptr())
+                hi.halo_unpack(0, up.data_ptr())
+                lo.halo_unpack(1, down.data_ptr())
+            for s in sims:
+                s.run(n)
+            done += n
+        out = oracle.zeros_state(nx, ny, nzg)
+        for s in sims:
+            d = s.download()
+            top = s.z_offset + s.nz == nzg
+            for c in range(6):
+                k = s.nz + (1 if c in (0, 1, 5) and top else 0)
+                out[c][s.z_offset:s.z_offset + k] = d[c][:k]
+            s.close()
+        want = oracle_run(oracle, nx, ny, nzg, oracle.zeros_state(nx, ny, nzg), steps, medium=(3, -1), src=src)
+        assert_bits(out, want, f"slabs skip variant {variant}")
