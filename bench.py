@@ -305,7 +305,7 @@ def main():
     # e2e through the public API with pinned host buffers (run_simulation
     # semantics): per-cell coefficients + fields uploaded, the config's full
     # step count (with halo exchanges), fields downloaded.
-    e2e = None
+    e2e = e2e_skip = None
     if not args.no_e2e:
         def pin(shape):
             return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
@@ -326,28 +326,35 @@ def main():
                                      [pin((nzc, ny, nx)) if q in want else None for q in range(4)])
             cell_arrays = {q: med[q] for q in want}
         e_steps = cfg_steps
-        s2 = make_sim()
-        if table is not None:
-            s2.add_source(*src, table)
-        ex2 = HaloExchange(s2, rank, world, f"cuda:{local}") if world > 1 else None
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for q, a_ in cell_arrays.items():
-            s2.set_cell_coeffs(q, a_)
-        s2.upload(host_f)
-        if ex2 is None:
-            s2.run(e_steps)
-        else:
-            run_steps(s2, ex2, e_steps, depth)
-        s2.download(out=host_out)
-        dt = time.perf_counter() - t0
-        s2.close()
-        if dist:
-            tt = torch.tensor([dt], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+
+        def run_e2e(qskip):
+            s2 = make_sim()
+            if table is not None:
+                s2.add_source(*src, table)
+            s2.set_quiescent_skip(qskip)
+            ex2 = HaloExchange(s2, rank, world, f"cuda:{local}") if world > 1 else None
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for q, a_ in cell_arrays.items():
+                s2.set_cell_coeffs(q, a_)
+            s2.upload(host_f)
+            if ex2 is None:
+                s2.run(e_steps)
+            else:
+                run_steps(s2, ex2, e_steps, depth)
+            s2.download(out=host_out)
+            dt = time.perf_counter() - t0
+            skipped = s2.info()["skipped_items"]
+            s2.close()
+            if dist:
+                tt = torch.tensor([dt], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
+            return dt, skipped
+
+        dt, _ = run_e2e(False)
         h2d = sum(a_.nbytes for a_ in host_f) + sum(a_.nbytes for a_ in cell_arrays.values())
         d2h = sum(a_.nbytes for a_ in host_out)
         e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
@@ -355,6 +362,13 @@ def main():
                "steps": e_steps, "wall_s": dt, "per_gpu_bytes": True,
                "path": "Simulation: set_cell_coeffs + upload (pinned host) -> run(config steps) -> "
                        "download (pinned host)"}
+        if fs is None:  # zero initial fields + point source: the reference's quiescent skip applies
+            dq, skipped = run_e2e(True)
+            e2e_skip = {"value": cells_total * e_steps / dq / 1e9, "unit": UNIT, "wall_s": dq,
+                        "skipped_items": skipped,
+                        "note": "same e2e run with yb_set_quiescent_skip(1) (RunOptions::quiescent_skip, "
+                                "runner.hpp:60-73): all-zero work items skipped, results bit-identical; "
+                                "informational, not the headline"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -366,6 +380,8 @@ def main():
                 "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": config, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        if e2e_skip is not None:
+            line["e2e_quiescent_skip"] = e2e_skip
         print(json.dumps(line), flush=True)
     sim.close()
     if dist:
