@@ -322,6 +322,18 @@ struct ProbeRecord {
   double value = 0.0;
 };
 
+/// One line per sample: step<TAB>time<TAB>probe<TAB>value, the value at
+/// `value_digits` significant digits (format_probe_records, probe.hpp:56-66).
+inline std::string format_probe_records(const std::vector<ProbeRecord>& records, int value_digits) {
+  std::string out;
+  char line[128];
+  for (const ProbeRecord& r : records) {
+    std::snprintf(line, sizeof(line), "%lld\t%.17g\t%d\t%.*g\n", r.step, r.time, r.probe, value_digits, r.value);
+    out += line;
+  }
+  return out;
+}
+
 // ------------------------------------------------ runner (runner.hpp)
 struct RunStats {
   long long steps = 0;
@@ -399,6 +411,8 @@ class Simulation {
   const GridSpec<Real>& grid() const { return grid_; }
   const Coefficients<Real>& coeffs() const { return coeffs_; }
   const RunStats& stats() const { return stats_; }
+  /// The C-ABI handle (extension: timing, info, halo exchange).
+  yb_sim* handle() const { return h_; }
 
   /// Per-cell coefficients (extension): `cells` nx*ny*nz in cell order, or
   /// empty to fall back to the uniform/per-axis default.

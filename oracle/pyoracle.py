@@ -121,6 +121,9 @@ def ref():
         R.yr_digest.restype = C.c_uint64
         R.yr_total_energy.argtypes = [C.c_int] * 3 + [_f32p] * 3 + [_f32p * 6, _f32p * 3]
         R.yr_total_energy.restype = C.c_double
+        R.yr_run_case.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int, C.c_int,
+                                  C.c_char_p, C.c_char_p, C.c_int64]
+        R.yr_run_case.restype = C.c_int64
         _ref = R
     return _ref
 
@@ -337,3 +340,15 @@ def ref_total_energy(nx, ny, nz, fields, prev_h, dx=None, dy=None, dz=None):
           for d, n in ((dx, nx), (dy, ny), (dz, nz))]
     ph = (_f32p * 3)(*[_p(a) for a in prev_h])
     return float(ref().yr_total_energy(nx, ny, nz, *[_p(a) for a in ax], _fptrs(fields), ph))
+
+
+def ref_run_case(size, steps, source_steps=50, sigma_dt=8.0, amplitude=1.0, probe_stride=20,
+                 quiescent_skip=True):
+    """The reference bench harness's run_case (bench.hpp:105-127): (checksum hex, probe text)."""
+    chk = C.create_string_buffer(17)
+    buf = C.create_string_buffer(1 << 20)
+    n = ref().yr_run_case(size, steps, source_steps, sigma_dt, amplitude, probe_stride, int(quiescent_skip),
+                          chk, buf, len(buf))
+    if n < 0:
+        raise RuntimeError(ref().yr_last_error().decode())
+    return chk.value.decode(), buf.value.decode()

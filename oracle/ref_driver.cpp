@@ -15,6 +15,8 @@
 //                     for any Variant/split/worker count with a reference
 //                     SourceSpec (source.hpp:15-68).
 //   yr_total_energy - total_energy against an HSnapshot (fields.hpp:68-146).
+//   yr_run_case     - the reference bench harness's run_case (bench.hpp:105-127):
+//                     cube cavity, default source and probes -> checksum + probe text.
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -212,6 +214,33 @@ double yr_total_energy(int nx, int ny, int nz, const float* dx, const float* dy,
     std::memcpy(a.data(), prev_h[comp_index(c) - 3], a.size_bytes());
   }
   return total_energy(g, f, HSnapshot<float>(p));
+}
+
+// run_case<float>(cfg, Standard, split 1x1x1, 1 thread) of the reference
+// bench harness (bench.hpp:105-127). checksum: 17-byte buffer (16 hex + NUL);
+// probes: the format_probe_records text (probe.hpp:56-66), NUL-terminated;
+// returns its length, or -1 on error / -2 if `cap` is too small.
+std::int64_t yr_run_case(int size, std::int64_t steps, std::int64_t source_steps, double sigma_dt,
+                         double amplitude, int probe_stride, int quiescent_skip, char* checksum,
+                         char* probes, std::int64_t cap) {
+  try {
+    BenchConfig cfg;
+    cfg.size = size;
+    cfg.steps = steps;
+    cfg.source_steps = source_steps;
+    cfg.source_sigma_dt = sigma_dt;
+    cfg.source_amplitude = amplitude;
+    cfg.probe_stride = probe_stride;
+    cfg.quiescent_skip = quiescent_skip != 0;
+    const CaseResult r = run_case<float>(cfg, Variant::Standard, Split{1, 1, 1}, 1);
+    std::snprintf(checksum, 17, "%s", r.checksum.c_str());
+    if ((std::int64_t)r.probe_text.size() + 1 > cap) return -2;
+    std::memcpy(probes, r.probe_text.c_str(), r.probe_text.size() + 1);
+    return (std::int64_t)r.probe_text.size();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"

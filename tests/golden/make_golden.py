@@ -24,6 +24,10 @@ Cases (all fp32, Standard step order, schedule.hpp:171-210):
               (b) 20^3 unit grid, Gaussian Ez source for 30 steps then free,
               the leapfrog invariant after each of 60 single steps (the
               measure_energy_drift pattern, bench.hpp:273-303).
+  bench_case  the reference bench harness's run_case (bench.hpp:105-127):
+              cube cavity make_uniform_grid<float>(N, 1, c0, 0.99), default
+              source (Ez pulse at the centre) and six default probes ->
+              checksum and the format_probe_records text, for two configs.
 """
 import os
 import sys
@@ -125,6 +129,17 @@ def main():
     save("energy", dims=np.array([nx, ny, nz]), dx=dx, dy=dy, dz=dz, static=np.array(e_static),
          seeds=np.array([31, 32]), n=np.array(n), steps=np.array(steps), table=tab,
          series=np.array(series), **fields_dict("out", g))
+
+    # bench_case
+    cases = [(24, 40, 25, 8.0, 1.0, 5), (32, 60, 50, 8.0, 1.0, 20)]
+    out = {}
+    for q, (n, st, ss, sd, amp, stride) in enumerate(cases):
+        chk, text = O.ref_run_case(n, st, source_steps=ss, sigma_dt=sd, amplitude=amp, probe_stride=stride)
+        out[f"case{q}"] = np.array([n, st, ss, stride])
+        out[f"case{q}_params"] = np.array([sd, amp])
+        out[f"case{q}_checksum"] = np.array(chk)
+        out[f"case{q}_probes"] = np.array(text)
+    save("bench_case", ncases=np.array(len(cases)), **out)
 
 
 if __name__ == "__main__":
