@@ -214,7 +214,12 @@ int yb_field_digest(yb_sim* sim, uint64_t* out);
  * components carry nz+1 planes; the top one belongs to the rank above unless
  * this is the global top). Per-cell coefficient uploads in slab mode carry
  * nz+4 cell planes: global planes z_offset-2 .. z_offset+nz+1 (planes outside
- * the grid are ignored). Axis coefficient cdz is the GLOBAL array. */
+ * the grid are ignored). Axis coefficient cdz is the GLOBAL array.
+ * pack / unpack are enqueued on the handle's stream: on a caller stream
+ * (yb_set_stream) they are stream-ordered and return at once, so a
+ * transport enqueued on the same stream (e.g. NCCL through torch) needs no
+ * host synchronisation; on the handle's own stream they complete before
+ * returning. */
 int yb_halo_bytes(yb_sim* sim, int side, int receive, size_t* bytes);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);

@@ -180,6 +180,7 @@ class Simulation:
         d = _Desc(nx, ny, nz, device, variant, zchunk, z_offset, nz_global)
         _check(lib().yb_create(C.byref(d), C.byref(h)))
         self._h = h
+        self.stream_ptr = 0
         self.set_axis_coeffs(np.full(nx, S, np.float32) if cdx is None else cdx,
                              np.full(ny, S, np.float32) if cdy is None else cdy,
                              np.full(self.nz_global, S, np.float32) if cdz is None else cdz)
@@ -292,7 +293,10 @@ class Simulation:
         return v.value
 
     def set_stream(self, stream_ptr):
+        """Work on a caller stream (e.g. torch.cuda.current_stream().cuda_stream);
+        0 / None restores the handle's own stream."""
         _check(lib().yb_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+        self.stream_ptr = stream_ptr or 0
 
     # z-slab halo planes (device pointers, e.g. torch CUDA tensor .data_ptr())
     def halo_bytes(self, side, receive):

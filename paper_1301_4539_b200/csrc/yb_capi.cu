@@ -1204,11 +1204,11 @@ static int halo_copy(yb_sim* s, int side, char* ext, bool pack) {
   for (int q = 0; q < n; ++q) {
     float* dev = s->buf[s->cur][comp[q]] + (long long)plane[q] * s->g.plane;
     if (pack)
-      YB_CU(cudaMemcpyAsync(ext + q * pb, dev, pb, cudaMemcpyDeviceToDevice, s->stream));
+      YB_CU(cudaMemcpyAsync(ext + q * pb, dev, pb, cudaMemcpyDefault, s->stream));
     else
-      YB_CU(cudaMemcpyAsync(dev, ext + q * pb, pb, cudaMemcpyDeviceToDevice, s->stream));
+      YB_CU(cudaMemcpyAsync(dev, ext + q * pb, pb, cudaMemcpyDefault, s->stream));
   }
-  YB_CU(cudaStreamSynchronize(s->stream));
+  if (s->stream == s->own_stream) YB_CU(cudaStreamSynchronize(s->stream));  // else stream-ordered
   return YB_OK;
 }
 

@@ -55,12 +55,20 @@ class HaloExchange:
             ops.append(dist.P2POp(dist.isend, send, peer, self.group))
             ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
         if ops:
+            # NCCL: wait() makes the current torch stream wait for the
+            # transfer. When the sim works on that stream (set_stream), pack ->
+            # send/recv -> unpack -> the next sweep are all stream-ordered and
+            # the host never blocks; otherwise synchronise before unpacking.
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-            if self.device.type == "cuda":
-                torch.cuda.synchronize(self.device)  # unpack runs on the sim's own stream
+            if self.device.type == "cuda" and not self._stream_ordered():
+                torch.cuda.synchronize(self.device)
         for side, (_, recv) in self.buf.items():
             self.sim.halo_unpack(side, recv.data_ptr())
+
+    def _stream_ordered(self):
+        ptr = getattr(self.sim, "stream_ptr", 0)
+        return bool(ptr) and ptr == torch.cuda.current_stream(self.device).cuda_stream
 
 
 def run_steps(sim, exchanger: HaloExchange, nsteps: int, depth: int = 1):

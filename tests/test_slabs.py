@@ -218,3 +218,51 @@ def test_gpu_slabs_bit_exact(yb, oracle, nranks, medium, fseed, src, variant, up
         assert bits_equal(out[c], want[c]), c
     for s in sims:
         s.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 2])
+def test_gpu_slabs_stream_ordered(yb, oracle, variant):
+    """Slabs on a shared caller stream: halo pack/unpack are stream-ordered
+    (no host synchronisation between sweeps and exchanges) — same result."""
+    nx, ny, nzg, steps = 136, 40, 29, 11
+    tab = oracle.gauss_table(steps)
+    srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        sims = []
+        for z0, n in partition(nzg, 3):
+            s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant)
+            s.generate_medium(7, 7)
+            for q in srcs:
+                s.add_source(*q)
+            s.fill(8)
+            s.set_stream(st.cuda_stream)
+            sims.append(s)
+        ex = _DeviceExchange(sims)
+        depth = sims[0].info()["halo_depth"]
+        done = 0
+        while done < steps:
+            n = min(depth, steps - done)
+            ex.exchange()
+            for s in sims:
+                s.run(n, sync=False)
+            done += n
+        st.synchronize()
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in sims:
+        d = s.download()
+        at_top = s.z_offset + s.nz == nzg
+        for c in range(6):
+            k = s.nz + (1 if c in (0, 1, 5) and at_top else 0)
+            out[c][s.z_offset:s.z_offset + k] = d[c][:k]
+        s.close()
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(7, 7)
+        for q in srcs:
+            one.add_source(*q)
+        one.fill(8)
+        one.run(steps)
+        want = one.download()
+    for c in range(6):
+        assert bits_equal(out[c], want[c]), c
