@@ -167,6 +167,9 @@ def main():
                     help="auto: tb2 (two steps per sweep; z-slabs exchange every two steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N>1: exchange, then sweep (default: boundary planes first, exchange overlapped "
+                         "with the interior sweep)")
     ap.add_argument("--zchunk", type=int, default=0, help="fused: z planes per work item (0 = auto)")
     args = ap.parse_args()
     rank, world, local = dist_env()
@@ -251,7 +254,7 @@ def main():
         if exch is None:
             s_.run(n, sync=False)
         else:
-            run_steps(s_, exch, n, depth)
+            run_steps(s_, exch, n, depth, overlap=not args.no_overlap)
 
     advance(sim, args.warmup)
     sim.synchronize()
@@ -300,7 +303,10 @@ def main():
     config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
                    "ctas": info1["grid_x"], "n_cell_arrays": info1["n_cell_arrays"]})
     if exch is not None:
-        config["halo_bytes_per_step_per_gpu"] = exch.bytes_per_exchange
+        config["halo_bytes_per_exchange_per_gpu"] = exch.bytes_per_exchange
+        config["exchange_every_steps"] = depth
+        config["exchange"] = ("NCCL P2P, serial" if args.no_overlap else
+                              "NCCL P2P, overlapped with the interior sweep (split sweeps)")
 
     # e2e through the public API with pinned host buffers (run_simulation
     # semantics): per-cell coefficients + fields uploaded, the config's full
@@ -343,7 +349,7 @@ def main():
             if ex2 is None:
                 s2.run(e_steps)
             else:
-                run_steps(s2, ex2, e_steps, depth)
+                run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
             s2.download(out=host_out)
             dt = time.perf_counter() - t0
             skipped = s2.info()["skipped_items"]

@@ -221,6 +221,14 @@ int yb_field_digest(yb_sim* sim, uint64_t* out);
  * host synchronisation; on the handle's own stream they complete before
  * returning. */
 int yb_halo_bytes(yb_sim* sim, int side, int receive, size_t* bytes);
+/* Split sweep for overlapping the exchange with compute: yb_advance_begin(n)
+ * (n <= halo depth) launches the sweep over the slab's boundary planes
+ * [0, n) and [nz-n, nz) only; yb_halo_pack then reads those NEW planes, so
+ * the transfer can run while yb_advance_end launches the interior planes and
+ * completes the n steps; yb_halo_unpack after yb_advance_end. Bit-identical
+ * to yb_advance(n). No probes; not the NAIVE variant. */
+int yb_advance_begin(yb_sim* sim, int64_t nsteps);
+int yb_advance_end(yb_sim* sim);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
 

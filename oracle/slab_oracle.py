@@ -71,7 +71,8 @@ class OracleSlab:
         return len(self._planes(side, not receive)) * (self.ny + 3) * (self.nx + 3) * 4
 
     def halo_pack(self, side, ptr):
-        buf = np.ascontiguousarray(np.stack([self.f[c][self.d + k] for c, k in self._planes(side, True)]))
+        f = getattr(self, "_pack_from", None) or self.f
+        buf = np.ascontiguousarray(np.stack([f[c][self.d + k] for c, k in self._planes(side, True)]))
         C.memmove(ptr, buf.ctypes.data, buf.nbytes)
 
     def halo_unpack(self, side, ptr):
@@ -81,6 +82,24 @@ class OracleSlab:
         for q, (c, k) in enumerate(pl):
             self.f[c][self.d + k] = buf[q]
         self.since_exchange = 0
+
+    # -------- split sweeps (yb_advance_begin / yb_advance_end semantics):
+    # begin computes the n steps into a pending copy that halo_pack reads;
+    # end commits it.
+    def advance_begin(self, nsteps):
+        saved = [a.copy() for a in self.f]
+        step0, since = self.step_index, self.since_exchange
+        self.run(nsteps)
+        self.pending = [a.copy() for a in self.f]
+        self.pending_state = (self.step_index, self.since_exchange)
+        self.f = saved
+        self.step_index, self.since_exchange = step0, since
+        self._pack_from = self.pending
+
+    def advance_end(self):
+        self.f = self.pending
+        self.step_index, self.since_exchange = self.pending_state
+        self.pending = self._pack_from = None
 
     # -------- steps
     def run(self, nsteps, sync=True):

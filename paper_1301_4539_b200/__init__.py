@@ -40,7 +40,7 @@ ABI_SYMBOLS = (
     "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
     "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
-    "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip",
+    "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
 )
 
 
@@ -127,6 +127,8 @@ def lib():
                                      C.POINTER(C.c_int64)]
         L.yb_snapshot_h.argtypes = [vp]
         L.yb_set_quiescent_skip.argtypes = [vp, C.c_int]
+        L.yb_advance_begin.argtypes = [vp, C.c_int64]
+        L.yb_advance_end.argtypes = [vp]
         L.yb_total_energy.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
@@ -267,6 +269,15 @@ class Simulation:
         _check(lib().yb_advance(self._h, nsteps))
         if sync:
             self.synchronize()
+
+    def advance_begin(self, nsteps):
+        """Split sweep, part 1: the slab's boundary planes (halo_pack then
+        reads the new planes); enqueued only."""
+        _check(lib().yb_advance_begin(self._h, nsteps))
+
+    def advance_end(self):
+        """Split sweep, part 2: the interior planes; completes the steps."""
+        _check(lib().yb_advance_end(self._h))
 
     def run_timed(self, nsteps):
         ms = C.c_float()

@@ -124,6 +124,8 @@ struct yb_sim {
   bool have_snap = false;
   double* energy_dev = nullptr;  // weights | partials | result
   int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
+  int pending = 0;            // steps of a split sweep in flight (yb_advance_begin)
+  bool pending_full = false;  // ... whose boundary launch already covered every plane
   bool qskip = false;         // yb_set_quiescent_skip
   bool q_valid = false;       // quiescent map matches the state buffers
   unsigned* qbits = nullptr;  // quiescent map (tiles x words)
@@ -361,15 +363,35 @@ int collect_timers(yb_sim* s) {
   return YB_OK;
 }
 
-int step_fused(yb_sim* s) {
+// z-chunk ranges of one sweep launch: [zb0, ze0) then [zb1, ze1).
+struct ZPart {
+  int zb0, ze0, zb1, ze1;
+};
+ZPart zfull(const yb_sim* s) { return {0, s->g.nz, s->g.nz, s->g.nz}; }
+
+// Fills the chunk fields of `a`; returns the launch's grid.
+dim3 set_chunks(const yb_sim* s, yb::FusedArgs& a, int zchunk, const ZPart& z) {
+  const int n0 = z.ze0 > z.zb0 ? (z.ze0 - z.zb0 + zchunk - 1) / zchunk : 0;
+  const int n1 = z.ze1 > z.zb1 ? (z.ze1 - z.zb1 + zchunk - 1) / zchunk : 0;
+  a.zchunk = zchunk;
+  a.zb0 = z.zb0;
+  a.ze0 = z.ze0;
+  a.zb1 = z.zb1;
+  a.ze1 = z.ze1;
+  a.nch0 = n0;
+  a.nitems = s->ntx * s->nty * (n0 + n1);
+  const char* one = std::getenv("YB_CTAS_PER_ITEM");
+  return dim3((one && one[0] == '1') ? a.nitems : std::min(a.nitems, s->num_sms), 1, 1);
+}
+
+int step_fused(yb_sim* s, ZPart z, int zchunk, bool flip) {
   const int nxt = s->cur ^ 1;
   yb::FusedArgs a{};
   a.g = s->g;
   a.nstages = s->stages;
-  a.zchunk = s->zchunk;
   a.ntx = s->ntx;
   a.nty = s->nty;
-  a.nitems = s->nitems;
+  const dim3 grid = set_chunks(s, a, zchunk, z);
   a.sched = s->sched;
   a.sched_base = s->sched_base;
   a.store_policy = s->store_policy;
@@ -394,25 +416,24 @@ int step_fused(yb_sim* s) {
     tp = &s->timers[s->timers_used++];
     YB_CU(cudaEventRecord(tp->a, s->stream));
   }
-  YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, s->grid, smem, s->stream));
-  s->sched_base += (unsigned long long)s->nitems + s->grid.x;  // every CTA's last fetch fails
+  YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, grid, smem, s->stream));
+  s->sched_base += (unsigned long long)a.nitems + grid.x;  // every CTA's last fetch fails
   if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
   s->launches += 1;
-  s->cur = nxt;
+  if (flip) s->cur = nxt;
   if (s->timers_used >= 4096) return collect_timers(s);
   return YB_OK;
 }
 
 // Two Standard steps in one launch (temporal depth 2).
-int step_tb2(yb_sim* s) {
+int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip) {
   const int nxt = s->cur ^ 1;
   yb::FusedArgs a{};
   a.g = s->g;
   a.nstages = s->stages2;
-  a.zchunk = s->zchunk2;
   a.ntx = s->ntx;
   a.nty = s->nty;
-  a.nitems = s->nitems2;
+  const dim3 grid = set_chunks(s, a, zchunk, z);
   a.sched = s->sched;
   a.sched_base = s->sched_base;
   a.store_policy = 1;
@@ -437,11 +458,11 @@ int step_tb2(yb_sim* s) {
     tp = &s->timers[s->timers_used++];
     YB_CU(cudaEventRecord(tp->a, s->stream));
   }
-  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], mask, s->grid2, smem, s->stream));
-  s->sched_base += (unsigned long long)s->nitems2 + s->grid2.x;
+  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], mask, grid, smem, s->stream));
+  s->sched_base += (unsigned long long)a.nitems + grid.x;
   if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
   s->launches += 1;
-  s->cur = nxt;
+  if (flip) s->cur = nxt;
   if (s->timers_used >= 4096) return collect_timers(s);
   return YB_OK;
 }
@@ -953,6 +974,7 @@ static int sample_probes_dev(yb_sim* s) {
 int yb_advance(yb_sim* s, int64_t nsteps) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end)");
   YB_CU(cudaSetDevice(s->device));
   if (s->variant != YB_VARIANT_NAIVE) {
     if (int rc = prepare_fused(s)) return rc;
@@ -962,12 +984,12 @@ int yb_advance(yb_sim* s, int64_t nsteps) {
   for (int64_t t = 0; t < nsteps;) {
     // two steps per launch unless a probe wants the level in between
     if (s->variant == YB_VARIANT_TB2 && t + 2 <= nsteps && !(probes && probe_fires(s, s->step_index + 1))) {
-      if (int rc = step_tb2(s)) return rc;
+      if (int rc = step_tb2(s, zfull(s), s->zchunk2, true)) return rc;
       s->step_index += 2;
       s->steps += 2;
       t += 2;
     } else {
-      const int rc = s->variant == YB_VARIANT_NAIVE ? step_naive(s) : step_fused(s);
+      const int rc = s->variant == YB_VARIANT_NAIVE ? step_naive(s) : step_fused(s, zfull(s), s->zchunk, true);
       if (rc) return rc;
       ++s->step_index;
       ++s->steps;
@@ -1021,6 +1043,41 @@ int yb_total_energy(yb_sim* s, const double* dx, const double* dy, const double*
   s->launches += 2;
   YB_CU(cudaMemcpyAsync(energy, wd + nw + np, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_advance_begin(yb_sim* s, int64_t nsteps) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is already in flight");
+  if (s->variant == YB_VARIANT_NAIVE) return fail(YB_INVALID_ARGUMENT, "split sweeps need the FUSED or TB2 variant");
+  if (nsteps < 1 || nsteps > 2 || (nsteps == 2 && s->variant != YB_VARIANT_TB2))
+    return fail(YB_INVALID_ARGUMENT, "split sweep: 1 step (FUSED / TB2) or 2 steps (TB2)");
+  if (!s->probes.empty()) return fail(YB_INVALID_ARGUMENT, "split sweeps do not sample probes");
+  YB_CU(cudaSetDevice(s->device));
+  if (int rc = prepare_fused(s)) return rc;
+  if (int rc = qmap_refresh(s)) return rc;
+  const int b = (int)nsteps, nz = s->g.nz;
+  s->pending_full = nz <= 2 * b + 1;  // no interior worth a launch: one whole sweep
+  const ZPart z = s->pending_full ? zfull(s) : ZPart{0, b, nz - b, nz};
+  const int zc = s->pending_full ? (nsteps == 2 ? s->zchunk2 : s->zchunk) : b;
+  if (int rc = nsteps == 2 ? step_tb2(s, z, zc, false) : step_fused(s, z, zc, false)) return rc;
+  s->pending = (int)nsteps;
+  return YB_OK;
+}
+
+int yb_advance_end(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (!s->pending) return fail(YB_INVALID_ARGUMENT, "no split sweep in flight (yb_advance_begin)");
+  YB_CU(cudaSetDevice(s->device));
+  const int n = s->pending, nz = s->g.nz;
+  if (!s->pending_full) {
+    const ZPart z{n, nz - n, nz - n, nz - n};
+    if (int rc = n == 2 ? step_tb2(s, z, s->zchunk2, false) : step_fused(s, z, s->zchunk, false)) return rc;
+  }
+  s->cur ^= 1;
+  s->step_index += n;
+  s->steps += n;
+  s->pending = 0;
   return YB_OK;
 }
 
@@ -1201,8 +1258,9 @@ static int halo_copy(yb_sim* s, int side, char* ext, bool pack) {
     for (int q = 1; q < d; ++q)
       for (int c = 0; c < 6; ++c) comp[n] = c, plane[n++] = base + q;
   }
+  const int b = s->pending && pack ? s->cur ^ 1 : s->cur;  // a split sweep's new boundary planes
   for (int q = 0; q < n; ++q) {
-    float* dev = s->buf[s->cur][comp[q]] + (long long)plane[q] * s->g.plane;
+    float* dev = s->buf[b][comp[q]] + (long long)plane[q] * s->g.plane;
     if (pack)
       YB_CU(cudaMemcpyAsync(ext + q * pb, dev, pb, cudaMemcpyDefault, s->stream));
     else
@@ -1219,6 +1277,7 @@ int yb_halo_pack(yb_sim* s, int side, void* dst) {
 
 int yb_halo_unpack(yb_sim* s, int side, const void* src) {
   if (!s || !src || side < 0 || side > 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "halo_unpack during a split sweep (after yb_advance_end)");
   if (int rc = halo_copy(s, side, const_cast<char*>(static_cast<const char*>(src)), false)) return rc;
   if (s->qskip && s->q_valid) {  // the ghost planes just written: mark the nonzero tile-planes
     const int d = halo_depth(s);

@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
           return;
         }
-        const int kz0 = (it / T) * a.zchunk;
-        const int kz1 = min(kz0 + a.zchunk, g.nz);
+        int kz0, kz1;
+        chunk_planes(a, it / T, kz0, kz1);
         const bool pro = kz0 > 0 || !at_bottom(g);
         const int kend = (kz1 == g.nz && at_top(g)) ? g.nz - 1 : kz1;
         if (QS) {  // quiescent item: input box all +0, no source -> skip
@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int chunk = p_item / T, tile = p_item - chunk * T;
       const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
-      const int kz0 = chunk * a.zchunk;
+      int kz0, kz1_unused;
+      chunk_planes(a, chunk, kz0, kz1_unused);
       const int pro = (kz0 > 0 || !at_bottom(g)) ? 1 : 0;
       float* dst = stages + (size_t)s * NARR * kSlot;
       // tensor z coordinate = local plane + kGhost (ghost plane -kGhost is z = 0)
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int chunk = item / T, tile = item - chunk * T;
     const int x0 = (tile % a.ntx) * kTX, y0 = (tile / a.ntx) * kTY;
-    const int kz0 = chunk * a.zchunk;
-    const int kz1 = min(kz0 + a.zchunk, g.nz);
+    int kz0, kz1;
+    chunk_planes(a, chunk, kz0, kz1);
     const bool top = (kz1 == g.nz) && at_top(g);  // global top: E(nz) is PEC
     const int kend = top ? g.nz - 1 : kz1;      // else stream plane kz1 (maybe the ghost)
 

@@ -59,6 +59,10 @@ struct FusedArgs {
   Geo g;
   int nstages;
   int zchunk;
+  // z-chunks of this launch: nch0 chunks over planes [zb0, ze0), then the
+  // rest over [zb1, ze1) (a whole sweep: [0, nz) and an empty second range;
+  // split sweeps: the slab's boundary planes, or its interior)
+  int zb0, ze0, zb1, ze1, nch0;
   int ntx, nty;  // tiles along x, y
   int nitems;    // work items = tiles * z-chunks, handed out by *sched
   unsigned long long* sched;     // monotonic global work counter
@@ -71,6 +75,17 @@ struct FusedArgs {
   QMap qm;                       // quiescent map (qm.bits == nullptr: off)
   unsigned long long* skipped;   // skipped-item counter
 };
+
+// planes [kz0, kz1) of z-chunk c of a launch
+__device__ __forceinline__ void chunk_planes(const FusedArgs& a, int c, int& kz0, int& kz1) {
+  if (c < a.nch0) {
+    kz0 = a.zb0 + c * a.zchunk;
+    kz1 = min(kz0 + a.zchunk, a.ze0);
+  } else {
+    kz0 = a.zb1 + (c - a.nch0) * a.zchunk;
+    kz1 = min(kz0 + a.zchunk, a.ze1);
+  }
+}
 
 // smem bytes of the fused kernel for `narr` staged arrays and `stages` ring depth.
 inline size_t fused_smem_bytes(int narr, int stages) {

@@ -147,13 +147,12 @@ struct Item {
   bool pro, src;  // src: some source lies in the item's (halo-extended) box
 };
 
-__device__ __forceinline__ Item make_item(const Geo& g, int item, int T, int ntx, int zchunk) {
+__device__ __forceinline__ Item make_item(const FusedArgs& a, const Geo& g, int item, int T, int ntx) {
   Item it;
   const int chunk = item / T, tile = item - chunk * T;
   it.x0 = (tile % ntx) * kTX;
   it.y0 = (tile / ntx) * kTB2Rows;
-  it.kz0 = chunk * zchunk;
-  it.kz1 = min(it.kz0 + zchunk, g.nz);
+  chunk_planes(a, chunk, it.kz0, it.kz1);
   const bool bot = at_bottom(g), top = at_top(g);
   it.pstart = bot ? max(it.kz0 - 1, 0) : it.kz0 - 1;
   it.pro = bot ? it.kz0 >= 2 : true;
@@ -635,7 +634,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
           mbar_arrive(bar);
           return;
         }
-        const Item pi = make_item(g, it, T, a.ntx, a.zchunk);
+        const Item pi = make_item(a, g, it, T, a.ntx);
         if (QS) {  // quiescent item: input box all +0, no source in either step -> skip
           const int tl = it % T;
           const int k0 = pi.pro ? pi.pstart - 1 : pi.pstart;
@@ -651,7 +650,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         p_e = 0;
         p_nE = (pi.pro ? 1 : 0) + pi.pin_end - pi.pstart + 1;
       }
-      const Item pi = make_item(g, p_item, T, a.ntx, a.zchunk);
+      const Item pi = make_item(a, g, p_item, T, a.ntx);
       const int x0 = pi.x0, y0 = pi.y0;
       const int pro = pi.pro ? 1 : 0;
       float* dst = B.stages + (size_t)s * L::floats;
@@ -691,7 +690,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       release_stage(B.empty, cur.wait(B, S), l);
       continue;
     }
-    Item it = make_item(g, item, T, a.ntx, a.zchunk);
+    Item it = make_item(a, g, item, T, a.ntx);
     mark_sources(a.src, it);
     if (w == EDGE)
       tb2_edge<CAC, CBC, DAC, DBC, QS>(a, it, B, cur, l);

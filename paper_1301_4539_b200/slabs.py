@@ -45,8 +45,14 @@ class HaloExchange:
                 torch.empty(sim.halo_bytes(side, False), dtype=torch.uint8, device=self.device),
                 torch.empty(sim.halo_bytes(side, True), dtype=torch.uint8, device=self.device))
         self.bytes_per_exchange = sum(s.numel() for s, _ in self.buf.values())
+        self._works = []
 
     def exchange(self):
+        self.start()
+        self.finish()
+
+    def start(self):
+        """Pack this slab's boundary planes and post the sends / receives."""
         for side, (send, _) in self.buf.items():
             self.sim.halo_pack(side, send.data_ptr())
         ops = []
@@ -54,15 +60,20 @@ class HaloExchange:
             peer = self.below if side == 0 else self.above
             ops.append(dist.P2POp(dist.isend, send, peer, self.group))
             ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
-        if ops:
+        self._works = dist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self):
+        """Complete the transfers and write the received ghost planes."""
+        if self._works:
             # NCCL: wait() makes the current torch stream wait for the
             # transfer. When the sim works on that stream (set_stream), pack ->
             # send/recv -> unpack -> the next sweep are all stream-ordered and
             # the host never blocks; otherwise synchronise before unpacking.
-            for w in dist.batch_isend_irecv(ops):
+            for w in self._works:
                 w.wait()
             if self.device.type == "cuda" and not self._stream_ordered():
                 torch.cuda.synchronize(self.device)
+        self._works = []
         for side, (_, recv) in self.buf.items():
             self.sim.halo_unpack(side, recv.data_ptr())
 
@@ -71,14 +82,30 @@ class HaloExchange:
         return bool(ptr) and ptr == torch.cuda.current_stream(self.device).cuda_stream
 
 
-def run_steps(sim, exchanger: HaloExchange, nsteps: int, depth: int = 1):
+def run_steps(sim, exchanger: HaloExchange, nsteps: int, depth: int = 1, overlap: bool = False):
     """Advance nsteps, refreshing the ghost planes every `depth` steps (the
-    sim's halo depth: 1 for one-step sweeps, 2 for two-step sweeps)."""
+    sim's halo depth: 1 for one-step sweeps, 2 for two-step sweeps).
+
+    overlap: split each sweep (advance_begin / advance_end): the boundary
+    planes are computed first, their exchange is posted, and it runs while
+    the interior planes are computed; the ghosts it delivers serve the next
+    sweep. Bit-identical to the plain schedule."""
+    if not overlap:
+        done = 0
+        while done < nsteps:
+            n = min(depth, nsteps - done)
+            exchanger.exchange()
+            sim.run(n, sync=False)
+            done += n
+        return
+    exchanger.exchange()  # ghosts of the current state
     done = 0
     while done < nsteps:
         n = min(depth, nsteps - done)
-        exchanger.exchange()
-        sim.run(n, sync=False)
+        sim.advance_begin(n)
+        exchanger.start()
+        sim.advance_end()
+        exchanger.finish()
         done += n
 
 

@@ -99,7 +99,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _gloo_worker(rank, world, port, result_path, depth):
+def _gloo_worker(rank, world, port, result_path, depth, overlap=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle import pyoracle as O
@@ -116,7 +116,7 @@ def _gloo_worker(rank, world, port, result_path, depth):
     slab.load_global(O.fill_fields(nx, ny, nzg, CASE["fseed"]))
     hx = HaloExchange(slab, rank, world, "cpu")
     from paper_1301_4539_b200.slabs import run_steps
-    run_steps(slab, hx, steps, depth)
+    run_steps(slab, hx, steps, depth, overlap=overlap)
     parts = [None] * world
     dist.all_gather_object(parts, [(slab.owned(c)[0], slab.owned(c)[1].copy()) for c in range(6)])
     if rank == 0:
@@ -128,12 +128,14 @@ def _gloo_worker(rank, world, port, result_path, depth):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,depth", [(2, 1), (3, 1), (2, 2), (3, 2)])
-def test_gloo_halo_exchange_bit_exact(oracle, tmp_path, world, depth):
+@pytest.mark.parametrize("world,depth,overlap", [(2, 1, False), (3, 1, False), (2, 2, False), (3, 2, False),
+                                                 (2, 1, True), (3, 2, True)])
+def test_gloo_halo_exchange_bit_exact(oracle, tmp_path, world, depth, overlap):
     """HaloExchange over torch.distributed (gloo, world_size 2/3, 127.0.0.1),
-    halo depth 1 and 2."""
+    halo depth 1 and 2; overlap: split sweeps with the exchange posted
+    between the boundary and the interior part (run_steps(overlap=True))."""
     path = str(tmp_path / "res.npz")
-    mp.spawn(_gloo_worker, args=(world, _free_port(), path, depth), nprocs=world, join=True)
+    mp.spawn(_gloo_worker, args=(world, _free_port(), path, depth, overlap), nprocs=world, join=True)
     got = np.load(path)
     want = reference_run(oracle, CASE["nx"], CASE["ny"], CASE["nzg"], CASE["steps"], CASE["medium"],
                          CASE["fseed"], (2, 6, 5, 8, oracle.gauss_table(CASE["steps"])))
@@ -266,3 +268,85 @@ def test_gpu_slabs_stream_ordered(yb, oracle, variant):
         want = one.download()
     for c in range(6):
         assert bits_equal(out[c], want[c]), c
+
+
+class _DeviceExchangeSplit(_DeviceExchange):
+    """start(): pack every slab (split sweeps: the new boundary planes) into
+    the buffers; finish(): unpack — the in-process stand-in for posting NCCL
+    transfers between advance_begin and advance_end."""
+
+    def start(self):
+        for (lo, hi), (up, down) in zip(zip(self.sims[:-1], self.sims[1:]), self.bufs):
+            lo.halo_pack(1, up.data_ptr())
+            hi.halo_pack(0, down.data_ptr())
+
+    def finish(self):
+        for (lo, hi), (up, down) in zip(zip(self.sims[:-1], self.sims[1:]), self.bufs):
+            hi.halo_unpack(0, up.data_ptr())
+            lo.halo_unpack(1, down.data_ptr())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,nranks,nzg", [(0, 3, 29), (2, 3, 29), (2, 2, 12), (2, 4, 23), (0, 2, 5)])
+def test_gpu_slabs_split_sweeps(yb, oracle, variant, nranks, nzg):
+    """Split sweeps (yb_advance_begin / yb_advance_end: boundary planes first,
+    exchange, interior) give the single-domain result bit for bit, including
+    slabs too thin to have an interior."""
+    nx, ny, steps = 136, 40, 11
+    tab = oracle.gauss_table(steps)
+    srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)]
+    sims = []
+    for z0, n in partition(nzg, nranks):
+        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant, zchunk=3)
+        s.generate_medium(7, 7)
+        for q in srcs:
+            s.add_source(*q)
+        s.fill(8)
+        sims.append(s)
+    ex = _DeviceExchangeSplit(sims)
+    depth = sims[0].info()["halo_depth"]
+    ex.exchange()
+    done = 0
+    while done < steps:
+        n = min(depth, steps - done)
+        for s in sims:
+            s.advance_begin(n)
+        ex.start()
+        for s in sims:
+            s.advance_end()
+        ex.finish()
+        done += n
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in sims:
+        d = s.download()
+        at_top = s.z_offset + s.nz == nzg
+        for c in range(6):
+            k = s.nz + (1 if c in (0, 1, 5) and at_top else 0)
+            out[c][s.z_offset:s.z_offset + k] = d[c][:k]
+        assert s.step_index == steps
+        s.close()
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(7, 7)
+        for q in srcs:
+            one.add_source(*q)
+        one.fill(8)
+        one.run(steps)
+        want = one.download()
+    for c in range(6):
+        assert bits_equal(out[c], want[c]), c
+
+
+@pytest.mark.gpu
+def test_split_sweep_errors(yb):
+    with yb.Simulation(40, 16, 10, z_offset=0, nz_global=20, variant=0) as s:
+        with pytest.raises(yb.YeeInvalidArgument):
+            s.advance_begin(2)  # the one-step kernel: depth 1
+        with pytest.raises(yb.YeeInvalidArgument):
+            s.advance_end()
+        s.advance_begin(1)
+        with pytest.raises(yb.YeeInvalidArgument):
+            s.run(1)
+        with pytest.raises(yb.YeeInvalidArgument):
+            s.halo_unpack(0, 0)
+        s.advance_end()
+        assert s.step_index == 1
