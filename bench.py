@@ -167,6 +167,9 @@ def main():
                     help="auto: tb2 (two steps per sweep; z-slabs exchange every two steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 halo transport: NCCL send/recv through torch.distributed, or a direct push "
+                         "into the neighbours' ghost planes over peer memory (CUDA IPC / NVLink)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange, then sweep (default: boundary planes first, exchange overlapped "
                          "with the interior sweep)")
@@ -197,7 +200,7 @@ def main():
 
     import torch
     import paper_1301_4539_b200 as Y
-    from paper_1301_4539_b200.slabs import HaloExchange, partition, run_steps
+    from paper_1301_4539_b200.slabs import HaloExchange, PeerExchange, partition, run_steps, run_steps_peer
 
     dist = None
     if world > 1:
@@ -246,13 +249,18 @@ def main():
         sim.fill(fs)
     if dist:
         dist.barrier()  # the first NCCL op involves every rank (communicator init)
-    exch = HaloExchange(sim, rank, world, f"cuda:{local}") if world > 1 else None
+    exch = None
+    if world > 1:
+        exch = (PeerExchange(sim, rank, world) if args.exchange == "p2p"
+                else HaloExchange(sim, rank, world, f"cuda:{local}"))
 
     depth = sim.info()["halo_depth"]  # steps per ghost-plane exchange
 
     def advance(s_, n):
         if exch is None:
             s_.run(n, sync=False)
+        elif args.exchange == "p2p":
+            run_steps_peer(s_, n, depth, overlap=not args.no_overlap)
         else:
             run_steps(s_, exch, n, depth, overlap=not args.no_overlap)
 
@@ -303,10 +311,14 @@ def main():
     config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
                    "ctas": info1["grid_x"], "n_cell_arrays": info1["n_cell_arrays"]})
     if exch is not None:
-        config["halo_bytes_per_exchange_per_gpu"] = exch.bytes_per_exchange
         config["exchange_every_steps"] = depth
-        config["exchange"] = ("NCCL P2P, serial" if args.no_overlap else
-                              "NCCL P2P, overlapped with the interior sweep (split sweeps)")
+        if args.exchange == "p2p":
+            config["exchange"] = ("peer-memory push (CUDA IPC / NVLink), device-side flags" +
+                                  ("" if args.no_overlap else ", overlapped with the interior sweep"))
+        else:
+            config["halo_bytes_per_exchange_per_gpu"] = exch.bytes_per_exchange
+            config["exchange"] = ("NCCL P2P, serial" if args.no_overlap else
+                                  "NCCL P2P, overlapped with the interior sweep (split sweeps)")
 
     # e2e through the public API with pinned host buffers (run_simulation
     # semantics): per-cell coefficients + fields uploaded, the config's full
@@ -338,7 +350,10 @@ def main():
             if table is not None:
                 s2.add_source(*src, table)
             s2.set_quiescent_skip(qskip)
-            ex2 = HaloExchange(s2, rank, world, f"cuda:{local}") if world > 1 else None
+            ex2 = None
+            if world > 1:
+                ex2 = (PeerExchange(s2, rank, world) if args.exchange == "p2p"
+                       else HaloExchange(s2, rank, world, f"cuda:{local}"))
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -348,6 +363,8 @@ def main():
             s2.upload(host_f)
             if ex2 is None:
                 s2.run(e_steps)
+            elif args.exchange == "p2p":
+                run_steps_peer(s2, e_steps, depth, overlap=not args.no_overlap)
             else:
                 run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
             s2.download(out=host_out)

@@ -229,6 +229,28 @@ int yb_halo_bytes(yb_sim* sim, int side, int receive, size_t* bytes);
  * to yb_advance(n). No probes; not the NAIVE variant. */
 int yb_advance_begin(yb_sim* sim, int64_t nsteps);
 int yb_advance_end(yb_sim* sim);
+
+/* Direct halo push over peer memory (NVLink P2P between GPUs; CUDA IPC
+ * between processes, or plain pointers within one process) instead of
+ * pack + NCCL + unpack. Setup: yb_peer_export writes yb_peer_handle_bytes()
+ * bytes of IPC handles (the state buffers and a flag block) for the
+ * neighbour to yb_peer_open (side 0: the slab below, 1: above; peer_nz its
+ * depth); within one process yb_peer_link takes the neighbour's handle.
+ * Per exchange: yb_peer_push copies this slab's d = halo-depth boundary
+ * planes (the new ones while a split sweep is in flight, else the current
+ * state's) into the neighbours' ghost planes and then publishes a counter in
+ * their flag words (overlap = 1: on a side stream, concurrent with the
+ * interior sweep); yb_peer_wait makes this handle's stream wait (on the
+ * device) until both neighbours have pushed as often as it has. Schedule:
+ * push; then per exchange: wait, yb_advance_begin(d), push, yb_advance_end.
+ * A wait that never completes gives up after ~2 s and yb_synchronize reports
+ * YB_RUNTIME_ERROR. */
+size_t yb_peer_handle_bytes(void);
+int yb_peer_export(yb_sim* sim, void* handles);
+int yb_peer_open(yb_sim* sim, int side, const void* handles, int peer_nz);
+int yb_peer_link(yb_sim* sim, int side, yb_sim* other);
+int yb_peer_push(yb_sim* sim, int overlap);
+int yb_peer_wait(yb_sim* sim);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
 

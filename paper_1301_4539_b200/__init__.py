@@ -41,6 +41,7 @@ ABI_SYMBOLS = (
     "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
     "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
+    "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait",
 )
 
 
@@ -129,6 +130,12 @@ def lib():
         L.yb_set_quiescent_skip.argtypes = [vp, C.c_int]
         L.yb_advance_begin.argtypes = [vp, C.c_int64]
         L.yb_advance_end.argtypes = [vp]
+        L.yb_peer_handle_bytes.restype = C.c_size_t
+        L.yb_peer_export.argtypes = [vp, vp]
+        L.yb_peer_open.argtypes = [vp, C.c_int, vp, C.c_int]
+        L.yb_peer_link.argtypes = [vp, C.c_int, vp]
+        L.yb_peer_push.argtypes = [vp, C.c_int]
+        L.yb_peer_wait.argtypes = [vp]
         L.yb_total_energy.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
@@ -278,6 +285,25 @@ class Simulation:
     def advance_end(self):
         """Split sweep, part 2: the interior planes; completes the steps."""
         _check(lib().yb_advance_end(self._h))
+
+    # direct halo push over peer memory (see yb_peer_* in include/yeeb200.h)
+    def peer_export(self):
+        buf = C.create_string_buffer(lib().yb_peer_handle_bytes())
+        _check(lib().yb_peer_export(self._h, buf))
+        return buf.raw
+
+    def peer_open(self, side, handles, peer_nz):
+        buf = C.create_string_buffer(bytes(handles), len(handles))
+        _check(lib().yb_peer_open(self._h, side, buf, peer_nz))
+
+    def peer_link(self, side, other):
+        _check(lib().yb_peer_link(self._h, side, other._h))
+
+    def peer_push(self, overlap=False):
+        _check(lib().yb_peer_push(self._h, 1 if overlap else 0))
+
+    def peer_wait(self):
+        _check(lib().yb_peer_wait(self._h))
 
     def run_timed(self, nsteps):
         ms = C.c_float()

@@ -210,6 +210,40 @@ __global__ void __launch_bounds__(256) k_qscan(Geo g, Fields A, Fields Bf, QMap 
   if (__syncthreads_or(nz) && threadIdx.x == 0) qmap_mark(q, tile, k);
 }
 
+// Peer halo push: blockIdx.y = direction (0 down, 1 up); float4 copies over
+// nplanes x 6 components x one padded plane each.
+__global__ void k_peer_copy(Geo g, PeerCopy d0, PeerCopy d1) {
+  const PeerCopy& d = blockIdx.y == 0 ? d0 : d1;
+  const long long per = g.plane / 4;  // float4 per plane (PX is a multiple of 32)
+  const long long n = per * 6 * d.nplanes;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long q = t / per, e = t - q * per;
+    const int c = (int)(q % 6), k = (int)(q / 6);
+    const float4 v = reinterpret_cast<const float4*>(d.src[c] + (long long)(d.src_k0 + k) * g.plane)[e];
+    reinterpret_cast<float4*>(d.dst[c] + (long long)(d.dst_k0 + k) * g.plane)[e] = v;
+  }
+}
+
+__global__ void k_peer_signal(unsigned* f0, unsigned* f1, unsigned epoch) {
+  __threadfence_system();
+  if (f0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f0), "r"(epoch) : "memory");
+  if (f1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f1), "r"(epoch) : "memory");
+}
+
+__global__ void k_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err) {
+  for (long long it = 0;; ++it) {
+    unsigned a, b;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(a) : "l"(flags) : "memory");
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(b) : "l"(flags + 1) : "memory");
+    if (a >= need0 && b >= need1) return;
+    if (it > (1ll << 24)) {  // ~2 s: the neighbour never signalled
+      atomicExch(err, 1);
+      return;
+    }
+    __nanosleep(100);
+  }
+}
+
 __global__ void k_fill_value(float* p, long long n, float v) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     p[t] = v;
@@ -339,6 +373,22 @@ cudaError_t launch_qscan(const Geo& g, const Fields& a, const Fields& b, const Q
                          cudaStream_t st) {
   if (k1 < k0) return cudaSuccess;
   k_qscan<<<dim3(q.ntx * q.nty, k1 - k0 + 1), 256, 0, st>>>(g, a, b, q, k0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_copy(const Geo& g, const PeerCopy& down, const PeerCopy& up, cudaStream_t st) {
+  if (!down.nplanes && !up.nplanes) return cudaSuccess;
+  k_peer_copy<<<dim3(296, 2), 256, 0, st>>>(g, down, up);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned epoch, cudaStream_t st) {
+  k_peer_signal<<<1, 1, 0, st>>>(flag_down, flag_up, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err, cudaStream_t st) {
+  k_peer_wait<<<1, 1, 0, st>>>(flags, need0, need1, err);
   return cudaGetLastError();
 }
 

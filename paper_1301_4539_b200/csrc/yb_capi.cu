@@ -67,6 +67,16 @@ struct Probe {
   int comp, i, j, k, stride;
 };
 
+// A neighbouring slab reachable through peer memory (same process, or a
+// CUDA IPC mapping of another process's allocations).
+struct PeerSide {
+  bool on = false;
+  float* buf[2][6] = {};      // its state buffers (plane 0 pointers)
+  unsigned* flags = nullptr;  // its flag words: [0] written by its lower neighbour, [1] by its upper
+  int nz = 0;
+  std::vector<void*> ipc;  // IPC mappings to close
+};
+
 struct TimerPair {
   cudaEvent_t a, b;
 };
@@ -125,6 +135,12 @@ struct yb_sim {
   double* energy_dev = nullptr;  // weights | partials | result
   int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
   int pending = 0;            // steps of a split sweep in flight (yb_advance_begin)
+  PeerSide peer[2];           // direct halo push targets (0: below, 1: above)
+  unsigned* pflags = nullptr; // my flag words [0] from below, [1] from above, [2] error
+  unsigned push_count = 0;
+  cudaStream_t peer_stream = nullptr;
+  cudaEvent_t peer_go = nullptr, peer_done = nullptr;
+  bool peer_inflight = false;
   bool pending_full = false;  // ... whose boundary launch already covered every plane
   bool qskip = false;         // yb_set_quiescent_skip
   bool q_valid = false;       // quiescent map matches the state buffers
@@ -638,6 +654,12 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->qbits);
   cudaFree(s->qskipped);
   for (float* p : s->snap_h) cudaFree(p);
+  for (PeerSide& ps : s->peer)
+    for (void* p : ps.ipc) cudaIpcCloseMemHandle(p);
+  cudaFree(s->pflags);
+  if (s->peer_stream) cudaStreamDestroy(s->peer_stream);
+  if (s->peer_go) cudaEventDestroy(s->peer_go);
+  if (s->peer_done) cudaEventDestroy(s->peer_done);
   cudaFree(s->energy_dev);
   for (auto& t : s->timers) {
     cudaEventDestroy(t.a);
@@ -1129,6 +1151,12 @@ int yb_synchronize(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   YB_CU(cudaSetDevice(s->device));
   YB_CU(cudaStreamSynchronize(s->stream));
+  if (s->peer_stream) YB_CU(cudaStreamSynchronize(s->peer_stream));
+  if (s->pflags) {
+    int err = 0;
+    YB_CU(cudaMemcpy(&err, s->pflags + 2, sizeof err, cudaMemcpyDeviceToHost));
+    if (err) return fail(YB_RUNTIME_ERROR, "peer halo wait timed out (a neighbour never signalled)");
+  }
   return collect_timers(s);
 }
 
@@ -1284,6 +1312,119 @@ int yb_halo_unpack(yb_sim* s, int side, const void* src) {
     const int k0 = side == 0 ? -d : s->g.nz, k1 = side == 0 ? -1 : s->g.nz + d - 1;
     YB_CU(yb::launch_qscan(s->g, fields_of(s, 0), fields_of(s, 1), qmap_of(s), k0, k1, s->stream));
   }
+  return YB_OK;
+}
+
+// ------------------------------------------------------------ peer halos
+static int ensure_pflags(yb_sim* s) {
+  if (s->pflags) return YB_OK;
+  YB_CU(cudaSetDevice(s->device));
+  YB_CU(cudaMalloc(&s->pflags, 4 * sizeof(unsigned)));
+  YB_CU(cudaMemset(s->pflags, 0, 4 * sizeof(unsigned)));
+  return YB_OK;
+}
+
+size_t yb_peer_handle_bytes(void) { return 13 * sizeof(cudaIpcMemHandle_t); }
+
+int yb_peer_export(yb_sim* s, void* out) {
+  if (!s || !out) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (int rc = ensure_pflags(s)) return rc;
+  cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(out);
+  for (int b = 0; b < 2; ++b)
+    for (int c = 0; c < 6; ++c) YB_CU(cudaIpcGetMemHandle(&h[b * 6 + c], s->buf[b][c] - yb::kGhost * s->g.plane));
+  YB_CU(cudaIpcGetMemHandle(&h[12], s->pflags));
+  return YB_OK;
+}
+
+static int check_peer_args(yb_sim* s, int side, int peer_nz) {
+  if (!s || side < 0 || side > 1 || peer_nz < 1) return fail(YB_INVALID_ARGUMENT, "bad argument");
+  if (s->g.nzg == s->g.nz) return fail(YB_INVALID_ARGUMENT, "peer halos need a z-slab handle");
+  if ((side == 0 && at_bottom(s->g)) || (side == 1 && at_top(s->g)))
+    return fail(YB_INVALID_ARGUMENT, "no neighbour on that side (global boundary)");
+  return ensure_pflags(s);
+}
+
+int yb_peer_open(yb_sim* s, int side, const void* handles, int peer_nz) {
+  if (!handles) return fail(YB_INVALID_ARGUMENT, "null handles");
+  if (int rc = check_peer_args(s, side, peer_nz)) return rc;
+  YB_CU(cudaSetDevice(s->device));
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+  PeerSide& ps = s->peer[side];
+  for (int q = 0; q < 13; ++q) {
+    void* p = nullptr;
+    YB_CU(cudaIpcOpenMemHandle(&p, h[q], cudaIpcMemLazyEnablePeerAccess));
+    ps.ipc.push_back(p);
+    if (q < 12)
+      ps.buf[q / 6][q % 6] = static_cast<float*>(p) + yb::kGhost * s->g.plane;  // same PX, PY by construction
+    else
+      ps.flags = static_cast<unsigned*>(p);
+  }
+  ps.nz = peer_nz;
+  ps.on = true;
+  return YB_OK;
+}
+
+int yb_peer_link(yb_sim* s, int side, yb_sim* other) {
+  if (!other) return fail(YB_INVALID_ARGUMENT, "null peer");
+  if (int rc = check_peer_args(s, side, other->g.nz)) return rc;
+  if (int rc = ensure_pflags(other)) return rc;
+  if (other->g.nx != s->g.nx || other->g.ny != s->g.ny) return fail(YB_INVALID_ARGUMENT, "peer x/y extents differ");
+  PeerSide& ps = s->peer[side];
+  for (int b = 0; b < 2; ++b)
+    for (int c = 0; c < 6; ++c) ps.buf[b][c] = other->buf[b][c];
+  ps.flags = other->pflags;
+  ps.nz = other->g.nz;
+  ps.on = true;
+  return YB_OK;
+}
+
+int yb_peer_push(yb_sim* s, int overlap) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (!s->peer[0].on && !s->peer[1].on) return fail(YB_INVALID_ARGUMENT, "no peer linked");
+  YB_CU(cudaSetDevice(s->device));
+  const int d = halo_depth(s), nz = s->g.nz;
+  const int b = s->pending ? s->cur ^ 1 : s->cur;  // the planes just computed / the current state
+  yb::PeerCopy dn{}, up{};
+  if (s->peer[0].on) {  // my planes 0..d-1 -> the lower slab's ghosts nz_b..nz_b+d-1
+    for (int c = 0; c < 6; ++c) dn.src[c] = s->buf[b][c], dn.dst[c] = s->peer[0].buf[b][c];
+    dn.src_k0 = 0, dn.dst_k0 = s->peer[0].nz, dn.nplanes = d;
+  }
+  if (s->peer[1].on) {  // my planes nz-d..nz-1 -> the upper slab's ghosts -d..-1
+    for (int c = 0; c < 6; ++c) up.src[c] = s->buf[b][c], up.dst[c] = s->peer[1].buf[b][c];
+    up.src_k0 = nz - d, up.dst_k0 = -d, up.nplanes = d;
+  }
+  cudaStream_t st = s->stream;
+  if (overlap) {  // on a side stream, concurrent with what follows on the main stream
+    if (!s->peer_stream) {
+      YB_CU(cudaStreamCreateWithFlags(&s->peer_stream, cudaStreamNonBlocking));
+      YB_CU(cudaEventCreateWithFlags(&s->peer_go, cudaEventDisableTiming));
+      YB_CU(cudaEventCreateWithFlags(&s->peer_done, cudaEventDisableTiming));
+    }
+    YB_CU(cudaEventRecord(s->peer_go, s->stream));
+    YB_CU(cudaStreamWaitEvent(s->peer_stream, s->peer_go, 0));
+    st = s->peer_stream;
+  }
+  YB_CU(yb::launch_peer_copy(s->g, dn, up, st));
+  ++s->push_count;
+  YB_CU(yb::launch_peer_signal(s->peer[0].on ? s->peer[0].flags + 1 : nullptr,
+                               s->peer[1].on ? s->peer[1].flags + 0 : nullptr, s->push_count, st));
+  if (overlap) {
+    YB_CU(cudaEventRecord(s->peer_done, st));
+    s->peer_inflight = true;
+  }
+  return YB_OK;
+}
+
+int yb_peer_wait(yb_sim* s) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (!s->pflags) return fail(YB_INVALID_ARGUMENT, "no peer linked");
+  YB_CU(cudaSetDevice(s->device));
+  if (s->peer_inflight) {  // my own push must have read my planes before they are rewritten
+    YB_CU(cudaStreamWaitEvent(s->stream, s->peer_done, 0));
+    s->peer_inflight = false;
+  }
+  YB_CU(yb::launch_peer_wait(s->pflags, s->peer[0].on ? s->push_count : 0u, s->peer[1].on ? s->push_count : 0u,
+                             reinterpret_cast<int*>(s->pflags + 2), s->stream));
   return YB_OK;
 }
 

@@ -126,6 +126,19 @@ struct ProbeArgs {
 // nonzero DoF in either state buffer.
 cudaError_t launch_qscan(const Geo& g, const Fields& a, const Fields& b, const QMap& q, int k0, int k1,
                          cudaStream_t st);
+// Direct halo push over peer memory (NVLink / same device): copy `nplanes`
+// planes of all six components from src (my state) to dst (the neighbour's
+// state), then — in a separate launch — publish `epoch` in its flag word.
+struct PeerCopy {
+  const float* src[6];
+  float* dst[6];
+  int src_k0, dst_k0, nplanes;  // 0 planes: direction unused
+};
+cudaError_t launch_peer_copy(const Geo& g, const PeerCopy& down, const PeerCopy& up, cudaStream_t st);
+cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned epoch, cudaStream_t st);
+// Spins (bounded, ~seconds) until flags[0] >= need0 and flags[1] >= need1;
+// on timeout sets *err = 1.
+cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err, cudaStream_t st);
 cudaError_t launch_fill_value(float* p, long long n, float v, cudaStream_t st);
 cudaError_t launch_probes(const Fields& F, const ProbeArgs& pa, float* out, cudaStream_t st);
 // weights: x node[nx+1], x cell[nx], y node[ny+1], y cell[ny], z node[nz+1], z cell[nz]

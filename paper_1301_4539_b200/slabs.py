@@ -109,6 +109,40 @@ def run_steps(sim, exchanger: HaloExchange, nsteps: int, depth: int = 1, overlap
         done += n
 
 
+class PeerExchange:
+    """Direct halo push over peer memory (NVLink P2P, CUDA IPC): each rank
+    exports IPC handles of its state buffers, all ranks gather them once
+    (torch.distributed object collective), and each slab opens its two
+    neighbours'. Afterwards no collective runs: the library's push kernel
+    writes the boundary planes straight into the neighbours' ghost planes and
+    bumps their flag words; a device-side wait orders the next sweep."""
+
+    def __init__(self, sim, rank: int, world: int, group=None):
+        self.sim = sim
+        info = [None] * world
+        dist.all_gather_object(info, (sim.peer_export(), sim.nz), group=group)
+        if rank > 0:
+            sim.peer_open(0, *info[rank - 1])
+        if rank < world - 1:
+            sim.peer_open(1, *info[rank + 1])
+        dist.barrier(group=group)
+
+
+def run_steps_peer(sim, nsteps: int, depth: int, overlap: bool = True):
+    """run_steps for PeerExchange / peer_link'ed slabs: push the current
+    boundary planes, then per exchange: wait for the neighbours, boundary
+    sweep, push the new planes (side stream if overlap), interior sweep."""
+    sim.peer_push(False)
+    done = 0
+    while done < nsteps:
+        n = min(depth, nsteps - done)
+        sim.peer_wait()
+        sim.advance_begin(n)
+        sim.peer_push(overlap)
+        sim.advance_end()
+        done += n
+
+
 def owned_planes(comp: int, nz_local: int, at_top: bool) -> int:
     """Planes of component `comp`'s dense slab array this rank owns: node-z
     components (ex, ey, hz) have nz_local+1 planes; the last belongs to the

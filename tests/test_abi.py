@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     txt = open(os.path.join(ROOT, "include", "yeeb200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int)\s+(yb_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|size_t)\s+(yb_\w+)\(", txt, re.M)))
 
 
 def test_header_symbols_listed(yb):

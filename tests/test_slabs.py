@@ -350,3 +350,76 @@ def test_split_sweep_errors(yb):
             s.halo_unpack(0, 0)
         s.advance_end()
         assert s.step_index == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,nranks,nzg", [(2, 3, 29), (0, 3, 29), (2, 2, 12), (2, 4, 23)])
+def test_gpu_slabs_peer_push(yb, oracle, variant, nranks, nzg):
+    """Direct peer-memory halo push (yb_peer_link within one process, one GPU):
+    push / wait / split sweeps enqueued slab after slab on one stream, so every
+    device-side wait is already satisfied when it runs (no kernel waits on a
+    concurrent one). Bit-exact against one domain."""
+    nx, ny, steps = 136, 40, 11
+    tab = oracle.gauss_table(steps)
+    srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)]
+    sims = []
+    for z0, n in partition(nzg, nranks):
+        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant, zchunk=3)
+        s.generate_medium(7, 7)
+        for q in srcs:
+            s.add_source(*q)
+        s.fill(8)
+        sims.append(s)
+    for lo, hi in zip(sims[:-1], sims[1:]):
+        lo.peer_link(1, hi)
+        hi.peer_link(0, lo)
+    depth = sims[0].info()["halo_depth"]
+    for s in sims:
+        s.peer_push(False)
+    done = 0
+    while done < steps:
+        n = min(depth, steps - done)
+        for s in sims:
+            s.peer_wait()
+            s.advance_begin(n)
+        for s in sims:
+            s.peer_push(False)
+        for s in sims:
+            s.advance_end()
+        done += n
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in sims:
+        s.synchronize()
+        d = s.download()
+        at_top = s.z_offset + s.nz == nzg
+        for c in range(6):
+            k = s.nz + (1 if c in (0, 1, 5) and at_top else 0)
+            out[c][s.z_offset:s.z_offset + k] = d[c][:k]
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(7, 7)
+        for q in srcs:
+            one.add_source(*q)
+        one.fill(8)
+        one.run(steps)
+        want = one.download()
+    for c in range(6):
+        assert bits_equal(out[c], want[c]), c
+    for s in sims:
+        s.close()
+
+
+@pytest.mark.gpu
+def test_peer_errors(yb):
+    with yb.Simulation(40, 16, 10) as one:
+        with pytest.raises(yb.YeeInvalidArgument):
+            one.peer_push()
+    a = yb.Simulation(40, 16, 10, z_offset=0, nz_global=20)
+    b = yb.Simulation(40, 16, 10, z_offset=10, nz_global=20)
+    with pytest.raises(yb.YeeInvalidArgument):
+        a.peer_link(0, b)  # nothing below the global bottom
+    c = yb.Simulation(32, 16, 10, z_offset=10, nz_global=20)
+    with pytest.raises(yb.YeeInvalidArgument):
+        a.peer_link(1, c)  # x extents differ
+    assert len(a.peer_export()) == yb.lib().yb_peer_handle_bytes()
+    for s in (a, b, c):
+        s.close()
