@@ -672,6 +672,7 @@ int yb_destroy(yb_sim* s) {
 
 int yb_set_axis_coeffs(yb_sim* s, const float* cdx, const float* cdy, const float* cdz) {
   if (!s || !cdx || !cdy || !cdz) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   YB_CU(cudaSetDevice(s->device));
   s->axis_ref[0].assign(cdx, cdx + s->g.nx);
   s->axis_ref[1].assign(cdy, cdy + s->g.ny);
@@ -681,6 +682,7 @@ int yb_set_axis_coeffs(yb_sim* s, const float* cdx, const float* cdy, const floa
 
 int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
   YB_CU(cudaSetDevice(s->device));
   // single domain: nz cell planes. z-slab mode: nz + 2*kGhost planes, the
@@ -764,6 +766,7 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
 
 int yb_generate_medium(yb_sim* s, int64_t eps_seed, int64_t sigma_seed) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   YB_CU(cudaSetDevice(s->device));
   const float S = courant();
   s->tm_valid = false;
@@ -884,6 +887,7 @@ int yb_host_medium_slab(int nx, int ny, int nz_global, int z_offset, int nplanes
 
 int yb_upload_field(yb_sim* s, int comp, const float* dense) {
   if (!s || !dense) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (int rc = check_comp(comp)) return rc;
   YB_CU(cudaSetDevice(s->device));
   s->q_valid = false;
@@ -892,6 +896,7 @@ int yb_upload_field(yb_sim* s, int comp, const float* dense) {
 
 int yb_download_field(yb_sim* s, int comp, float* dense) {
   if (!s || !dense) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (int rc = check_comp(comp)) return rc;
   YB_CU(cudaSetDevice(s->device));
   return copy_dense(s, comp, s->buf[s->cur][comp], nullptr, dense);
@@ -899,6 +904,7 @@ int yb_download_field(yb_sim* s, int comp, float* dense) {
 
 int yb_zero_fields(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   YB_CU(cudaSetDevice(s->device));
   for (int c = 0; c < 6; ++c)
     YB_CU(cudaMemsetAsync(s->buf[s->cur][c] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
@@ -910,6 +916,7 @@ int yb_zero_fields(yb_sim* s) {
 
 int yb_fill_fields(yb_sim* s, uint64_t seed) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   YB_CU(cudaSetDevice(s->device));
   YB_CU(yb::launch_fill_fields(s->g, fields_of(s, s->cur), seed, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
@@ -919,6 +926,7 @@ int yb_fill_fields(yb_sim* s, uint64_t seed) {
 
 int yb_set_step_index(yb_sim* s, int64_t v) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (v < 0) return fail(YB_INVALID_ARGUMENT, "negative step index");
   s->step_index = v;
   return YB_OK;
@@ -1198,6 +1206,7 @@ static bool slab_mode(const yb_sim* s) { return s->g.nzg != s->g.nz; }
 
 int yb_apply_ampere_range(yb_sim* s, const int* box) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   int b[6];
   if (int rc = check_box(s, box, b)) return fail(rc, "apply_ampere_range: range out of bounds");
@@ -1210,6 +1219,7 @@ int yb_apply_ampere_range(yb_sim* s, const int* box) {
 
 int yb_apply_faraday_range(yb_sim* s, const int* box) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   int b[6];
   if (int rc = check_box(s, box, b)) return fail(rc, "apply_faraday_range: range out of bounds");
@@ -1222,6 +1232,7 @@ int yb_apply_faraday_range(yb_sim* s, const int* box) {
 
 int yb_apply_pec_boundary(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (slab_mode(s)) return fail(YB_INVALID_ARGUMENT, "range ops act on a whole domain, not a z-slab");
   YB_CU(cudaSetDevice(s->device));
   s->q_valid = false;

@@ -348,6 +348,10 @@ def test_split_sweep_errors(yb):
             s.run(1)
         with pytest.raises(yb.YeeInvalidArgument):
             s.halo_unpack(0, 0)
+        with pytest.raises(yb.YeeInvalidArgument):
+            s.zero()
+        with pytest.raises(yb.YeeInvalidArgument):
+            s.download()
         s.advance_end()
         assert s.step_index == 1
 
