@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--variant", default="auto", choices=["auto", "fused", "naive", "tb2"],
+    ap.add_argument("--variant", default="auto", choices=["auto", "fused", "naive", "tb2", "tb4"],
                     help="auto: tb2 (two steps per sweep; z-slabs exchange every two steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -213,7 +213,8 @@ def main():
     torch.cuda.set_stream(stream)
     if args.variant == "auto":
         args.variant = "tb2"
-    variant = {"fused": Y.VARIANT_FUSED, "naive": Y.VARIANT_NAIVE, "tb2": Y.VARIANT_TB2}[args.variant]
+    variant = {"fused": Y.VARIANT_FUSED, "naive": Y.VARIANT_NAIVE, "tb2": Y.VARIANT_TB2,
+               "tb4": Y.VARIANT_TB4}[args.variant]
     if world > 1 and variant == Y.VARIANT_NAIVE:
         raise SystemExit("z-slab multi-GPU runs need a sweep variant (fused or tb2)")
 
@@ -296,12 +297,12 @@ def main():
     bpc = info1["bytes_per_cell_update"]
     kern_ms = info1["main_kernel_ms"] / max(1, info1["main_kernel_timed"])
     peak, peak_src = load_peak()
-    steps_per_launch = 2 if variant == Y.VARIANT_TB2 else 1
+    steps_per_launch = {Y.VARIANT_TB2: 2, Y.VARIANT_TB4: 4}.get(variant, 1)
     achieved = bpc * cells * steps_per_launch / (kern_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.config, args.variant),
                 "kernel": {0: "k_fused (one E+H sweep per step)", 1: "naive step (4 kernels)",
-                           2: "k_tb2 (two steps per sweep)"}[variant],
+                           2: "k_tb2 (two steps per sweep)", 3: "k_tb4 (four steps per sweep)"}[variant],
                 "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,
                 "peak_source": peak_src, "per_gpu": world > 1,
                 "one_sweep_bytes_per_cell_update": 48.0 + 4.0 * info1["n_cell_arrays"],

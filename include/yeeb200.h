@@ -52,7 +52,9 @@ enum { YB_CA = 0, YB_CB = 1, YB_DA = 2, YB_DB = 3 };
 enum {
   YB_VARIANT_FUSED = 0, /* one z-march sweep per step: TMA-staged planes, E+H fused */
   YB_VARIANT_NAIVE = 1, /* one thread per DoF, separate E/PEC/source/H launches */
-  YB_VARIANT_TB2 = 2    /* temporal blocking: two full steps per sweep (odd remainder: FUSED) */
+  YB_VARIANT_TB2 = 2,   /* temporal blocking: two full steps per sweep (odd remainder: FUSED) */
+  YB_VARIANT_TB4 = 3    /* temporal blocking: four full steps per sweep (remainder: TB2 / FUSED);
+                           single domain; the depth-8 point of the temporal-depth sweep */
 };
 
 typedef struct yb_sim yb_sim;

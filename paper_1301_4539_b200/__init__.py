@@ -26,7 +26,7 @@ CSRC = os.path.join(HERE, "csrc")
 EX, EY, EZ, HX, HY, HZ = range(6)
 COMP_NAMES = ("ex", "ey", "ez", "hx", "hy", "hz")
 CA, CB, DA, DB = range(4)
-VARIANT_FUSED, VARIANT_NAIVE, VARIANT_TB2 = 0, 1, 2
+VARIANT_FUSED, VARIANT_NAIVE, VARIANT_TB2, VARIANT_TB4 = 0, 1, 2, 3
 S_BITS = 0x3F1252DB
 S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt(3))
 

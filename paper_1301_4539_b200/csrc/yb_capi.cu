@@ -124,6 +124,8 @@ struct yb_sim {
   yb::TMaps tm2[2];  // two-step sweep maps (taller boxes)
   int stages2 = 0, zchunk2 = 0, nitems2 = 1;
   dim3 grid2{1, 1, 1};
+  yb::TMaps tm4[2];  // four-step sweep maps (64-column window boxes)
+  int stages4 = 0, zchunk4 = 0, ntx4 = 1, nty4 = 1;
   unsigned long long* sched = nullptr;  // device work counter of the fused kernel
   unsigned long long sched_base = 0;
   std::vector<Probe> probes;
@@ -206,13 +208,13 @@ yb::Fields fields_of(const yb_sim* s, int b) {
   return F;
 }
 
-int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY) {
+int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY, int box_cols = yb::kBX) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   // z coordinate = local plane + kGhost: the allocation starts at ghost plane -kGhost
   const cuuint64_t dims[3] = {(cuuint64_t)g.PX, (cuuint64_t)g.PY, (cuuint64_t)g.PZ + yb::kGhost + 1};
   const cuuint64_t strides[2] = {(cuuint64_t)g.PX * 4, (cuuint64_t)g.plane * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)yb::kBX, (cuuint32_t)box_rows, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   // YB_L2PROMO=0..3 (tuning knob): none / 64B / 128B / 256B L2 promotion
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
@@ -275,7 +277,38 @@ int prepare_fused(yb_sim* s) {
   const char* one = std::getenv("YB_CTAS_PER_ITEM");
   const int ctas = (one && one[0] == '1') ? s->nitems : std::min(s->nitems, s->num_sms);
   s->grid = dim3(ctas, 1, 1);
-  if (s->variant == YB_VARIANT_TB2) {
+  if (s->variant == YB_VARIANT_TB4) {
+    for (int b = 0; b < 2; ++b) {
+      int q = 0;
+      for (int c = 0; c < 6; ++c)
+        if (int rc = encode_map(&s->tm4[b].m[q++], s->g, s->buf[b][c], yb::kTB4BY, yb::kTB4Win)) return rc;
+      for (int a = 0; a < 4; ++a)
+        if (s->cell[a])
+          if (int rc = encode_map(&s->tm4[b].m[q++], s->g, s->cell[a], yb::kTB4BY - 1, yb::kTB4Win)) return rc;
+    }
+    int S4 = 3;
+    while (S4 > 2 && yb::tb4_smem_bytes(mask, S4) > avail) --S4;
+    s->stages4 = S4;
+    s->ntx4 = (s->g.nx + yb::kTB4Cols - 1) / yb::kTB4Cols;
+    s->nty4 = (s->g.ny + yb::kTB4Rows - 1) / yb::kTB4Rows;
+    int zc4 = s->zchunk_req;
+    if (zc4 <= 0) {  // a four-step item re-streams ~7 planes at its z boundaries
+      const long long T = (long long)s->ntx4 * s->nty4;
+      double best = 1e300;
+      for (int Z = 1; Z <= s->g.nz; ++Z) {
+        const int len = (s->g.nz + Z - 1) / Z;
+        const int Zr = (s->g.nz + len - 1) / len;
+        const long long rounds = (T * Zr + s->num_sms - 1) / s->num_sms;
+        const double cost = (double)rounds * (len + (Zr > 1 ? 7.0 : 0.0));
+        if (cost < best - 1e-9) {
+          best = cost;
+          zc4 = len;
+        }
+      }
+    }
+    s->zchunk4 = std::min(std::max(zc4, 1), s->g.nz);
+  }
+  if (s->variant == YB_VARIANT_TB2 || s->variant == YB_VARIANT_TB4) {
     for (int b = 0; b < 2; ++b) {
       int q = 0;
       for (int c = 0; c < 6; ++c)
@@ -483,6 +516,73 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip) {
   return YB_OK;
 }
 
+// Active sources of steps step .. step+3 (the four steps of one depth-4 launch).
+yb::SrcArgs4 sources_at4(const yb_sim* s, int64_t step) {
+  yb::SrcArgs4 a{};
+  for (const Src& q : s->sources) {
+    const int64_t n = (int64_t)q.table.size();
+    int act = 0;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int t = 0; t < 4; ++t)
+      if (step + t >= 0 && step + t < n) {
+        act |= 1 << t;
+        v[t] = q.table[step + t];
+      }
+    if (!act) continue;
+    a.comp[a.n] = q.comp;
+    a.i[a.n] = q.i;
+    a.j[a.n] = q.j;
+    a.k[a.n] = q.k - s->g.zoff;
+    for (int t = 0; t < 4; ++t) a.val[a.n][t] = v[t];
+    a.act[a.n] = act;
+    ++a.n;
+  }
+  return a;
+}
+
+// Four Standard steps in one launch (temporal depth 4, single domain).
+int step_tb4(yb_sim* s) {
+  const int nxt = s->cur ^ 1;
+  yb::FusedArgs a{};
+  a.g = s->g;
+  a.nstages = s->stages4;
+  a.ntx = s->ntx4;
+  a.nty = s->nty4;
+  a.zchunk = s->zchunk4;
+  a.zb0 = 0, a.ze0 = s->g.nz, a.zb1 = a.ze1 = s->g.nz;
+  a.nch0 = (s->g.nz + s->zchunk4 - 1) / s->zchunk4;
+  a.nitems = s->ntx4 * s->nty4 * a.nch0;
+  a.sched = s->sched;
+  a.sched_base = s->sched_base;
+  a.co = coef_args(s);
+  for (int c = 0; c < 6; ++c) {
+    a.in[c] = s->buf[s->cur][c];
+    a.out[c] = s->buf[nxt][c];
+  }
+  const yb::SrcArgs4 src = sources_at4(s, s->step_index);
+  const int mask = cell_mask(s);
+  const dim3 grid(std::min(a.nitems, s->num_sms), 1, 1);
+  TimerPair* tp = nullptr;
+  if (s->timing) {
+    if (s->timers_used == s->timers.size()) {
+      TimerPair p;
+      YB_CU(cudaEventCreate(&p.a));
+      YB_CU(cudaEventCreate(&p.b));
+      s->timers.push_back(p);
+    }
+    tp = &s->timers[s->timers_used++];
+    YB_CU(cudaEventRecord(tp->a, s->stream));
+  }
+  YB_CU(yb::launch_tb4(a, src, s->tm4[s->cur], mask, grid, yb::tb4_smem_bytes(mask, s->stages4), s->stream));
+  s->sched_base += (unsigned long long)a.nitems + grid.x;
+  if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
+  s->launches += 1;
+  s->cur = nxt;
+  s->q_valid = false;  // this kernel does not maintain the quiescent map
+  if (s->timers_used >= 4096) return collect_timers(s);
+  return YB_OK;
+}
+
 int step_naive(yb_sim* s) {
   const int box[6] = {0, s->g.nx + 1, 0, s->g.ny + 1, 0, s->g.nz + 1};
   const yb::Fields F = fields_of(s, s->cur);
@@ -563,8 +663,10 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (d->ny > 65000 || d->nz > 65000 || d->nx > (1 << 24))
     return fail(YB_INVALID_ARGUMENT, "grid too large for this build");
   if (d->variant != YB_VARIANT_FUSED && d->variant != YB_VARIANT_NAIVE &&
-      d->variant != YB_VARIANT_TB2)
+      d->variant != YB_VARIANT_TB2 && d->variant != YB_VARIANT_TB4)
     return fail(YB_INVALID_ARGUMENT, "unknown variant %d", d->variant);
+  if (d->variant == YB_VARIANT_TB4 && d->nz_global > 0 && d->nz_global != d->nz)
+    return fail(YB_INVALID_ARGUMENT, "the four-step variant works on a single domain (no z-slabs)");
   if (d->nz_global > 0 && (d->z_offset < 0 || d->z_offset + d->nz > d->nz_global))
     return fail(YB_INVALID_ARGUMENT, "slab [%d,%d) outside the global grid of %d planes",
                 d->z_offset, d->z_offset + d->nz, d->nz_global);
@@ -629,7 +731,8 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (int rc = upload_axis(s)) return bail(rc);
   static bool limits_set = false;
   if (!limits_set) {
-    if (yb::fused_set_smem_limits() != cudaSuccess || yb::tb2_set_smem_limits() != cudaSuccess)
+    if (yb::fused_set_smem_limits() != cudaSuccess || yb::tb2_set_smem_limits() != cudaSuccess ||
+        yb::tb4_set_smem_limits() != cudaSuccess)
       return bail(fail(YB_CUDA_ERROR, "cudaFuncSetAttribute failed"));
     limits_set = true;
   }
@@ -1012,8 +1115,23 @@ int yb_advance(yb_sim* s, int64_t nsteps) {
   }
   const bool probes = !s->probes.empty();
   for (int64_t t = 0; t < nsteps;) {
+    // four steps per launch (TB4) unless a probe wants a level in between
+    if (s->variant == YB_VARIANT_TB4 && t + 4 <= nsteps &&
+        !(probes && (probe_fires(s, s->step_index + 1) || probe_fires(s, s->step_index + 2) ||
+                     probe_fires(s, s->step_index + 3)))) {
+      if (int rc = step_tb4(s)) return rc;
+      s->step_index += 4;
+      s->steps += 4;
+      t += 4;
+      if (probes && probe_fires(s, s->step_index))
+        if (int rc = sample_probes_dev(s)) return rc;
+      continue;
+    }
+    if (s->qskip && !s->q_valid)
+      if (int rc = qmap_refresh(s)) return rc;
     // two steps per launch unless a probe wants the level in between
-    if (s->variant == YB_VARIANT_TB2 && t + 2 <= nsteps && !(probes && probe_fires(s, s->step_index + 1))) {
+    if ((s->variant == YB_VARIANT_TB2 || s->variant == YB_VARIANT_TB4) && t + 2 <= nsteps &&
+        !(probes && probe_fires(s, s->step_index + 1))) {
       if (int rc = step_tb2(s, zfull(s), s->zchunk2, true)) return rc;
       s->step_index += 2;
       s->steps += 2;
@@ -1080,7 +1198,7 @@ int yb_advance_begin(yb_sim* s, int64_t nsteps) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is already in flight");
   if (s->variant == YB_VARIANT_NAIVE) return fail(YB_INVALID_ARGUMENT, "split sweeps need the FUSED or TB2 variant");
-  if (nsteps < 1 || nsteps > 2 || (nsteps == 2 && s->variant != YB_VARIANT_TB2))
+  if (nsteps < 1 || nsteps > 2 || (nsteps == 2 && s->variant != YB_VARIANT_TB2 && s->variant != YB_VARIANT_TB4))
     return fail(YB_INVALID_ARGUMENT, "split sweep: 1 step (FUSED / TB2) or 2 steps (TB2)");
   if (!s->probes.empty()) return fail(YB_INVALID_ARGUMENT, "split sweeps do not sample probes");
   YB_CU(cudaSetDevice(s->device));
@@ -1265,7 +1383,7 @@ int yb_field_digest(yb_sim* s, uint64_t* out) {
 // components (-> the slab below's ghost planes nz..nz+d-1). Up-send: my planes
 // nz-d+1..nz-1 all six, plane nz-d hx, hy (-> the slab above's ghost planes
 // -d+1..-1 and -d). Planes are contiguous (PX*PY floats): one device copy each.
-static int halo_depth(const yb_sim* s) { return s->variant == YB_VARIANT_TB2 ? 2 : 1; }
+static int halo_depth(const yb_sim* s) { return s->variant == YB_VARIANT_FUSED || s->variant == YB_VARIANT_NAIVE ? 1 : 2; }
 static int halo_planes(const yb_sim* s, bool down) {
   const int d = halo_depth(s);
   return down ? 6 * d : 6 * (d - 1) + 2;
@@ -1483,8 +1601,12 @@ int yb_get_info(yb_sim* s, yb_info* info) {
   info->grid_z = (int)s->grid.z;
   info->zchunk = s->zchunk;
   info->bytes_per_cell_update = (48.0 + 4.0 * info->n_cell_arrays) /
-                                (s->variant == YB_VARIANT_TB2 ? 2.0 : 1.0);
-  if (s->variant == YB_VARIANT_TB2) {
+                                (s->variant == YB_VARIANT_TB2 ? 2.0 : (s->variant == YB_VARIANT_TB4 ? 4.0 : 1.0));
+  if (s->variant == YB_VARIANT_TB4) {
+    info->stages = s->stages4;
+    info->grid_x = std::min(s->ntx4 * s->nty4 * ((s->g.nz + s->zchunk4 - 1) / s->zchunk4), s->num_sms);
+    info->zchunk = s->zchunk4;
+  } else if (s->variant == YB_VARIANT_TB2) {
     info->stages = s->stages2;
     info->grid_x = (int)s->grid2.x;
     info->zchunk = s->zchunk2;

@@ -40,6 +40,14 @@ constexpr int kTB2H1 = 2 * 3 * (kTB2Rows + 2) * kBX;  // H^{n+3/2} planes (doubl
 constexpr int kTB2E2 = 2 * 3 * (kTB2Rows + 1) * kBX;  // E^{n+2} planes (double buffered)
 constexpr int kTB2Edge = 2 * 3 * kTB2RowWarps * 3 + 2 * 2 * (kTB2Rows + 2) * 2 + 2 * 2 * kTB2RowWarps;
 
+// Four-step (temporal depth 4) sweep geometry (yb_tb4.cu): 4 output rows x
+// 56 output columns; every warp works on an 11-row x 64-column window.
+constexpr int kTB4Rows = 4;
+constexpr int kTB4RowWarps = kTB4Rows + 7;  // window rows y0-3 .. y0+7
+constexpr int kTB4BY = kTB4RowWarps + 1;    // staged field rows y0-4 .. y0+7
+constexpr int kTB4Win = 64;                 // window columns x0-4 .. x0+59
+constexpr int kTB4Cols = kTB4Win - 8;       // output columns x0 .. x0+55
+
 // floats of one stage for a coefficient set (mask bit q: array q per-cell)
 inline int tb2_stage_floats(int cell_mask) {
   return 6 * kTB2SlotF + ((cell_mask & 1) + ((cell_mask >> 1) & 1)) * kTB2SlotC +
@@ -86,6 +94,19 @@ __device__ __forceinline__ void chunk_planes(const FusedArgs& a, int c, int& kz0
     kz1 = min(kz0 + a.zchunk, a.ze1);
   }
 }
+
+// Soft sources of the four steps of one depth-4 launch (bit s of act: the
+// source injects at step n+s with increment val[s]).
+struct SrcArgs4 {
+  int n;
+  int comp[kMaxSources], i[kMaxSources], j[kMaxSources], k[kMaxSources];
+  float val[kMaxSources][4];
+  int act[kMaxSources];
+};
+size_t tb4_smem_bytes(int cell_mask, int stages);
+cudaError_t tb4_set_smem_limits();
+cudaError_t launch_tb4(const FusedArgs& a, const SrcArgs4& s, const TMaps& tm, int cell_mask, dim3 grid,
+                       size_t smem, cudaStream_t st);
 
 // smem bytes of the fused kernel for `narr` staged arrays and `stages` ring depth.
 inline size_t fused_smem_bytes(int narr, int stages) {

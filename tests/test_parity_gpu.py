@@ -511,3 +511,42 @@ def test_quiescent_skip_slabs(yb, oracle):
             s.close()
         want = oracle_run(oracle, nx, ny, nzg, oracle.zeros_state(nx, ny, nzg), steps, medium=(3, -1), src=src)
         assert_bits(out, want, f"slabs skip variant {variant}")
+
+
+@pytest.mark.parametrize("name", ["c1_vacuum_src", "c3_lossy_fields", "odd_sizes", "two_tiles_partial", "thin_x",
+                                  "thin_y", "thin_z", "c4_slab_src", "c2_dielectric_src"])
+def test_tb4_vs_oracle(yb, oracle, name):
+    """Four steps per sweep (YB_VARIANT_TB4, the depth-8 point of the config-5
+    sweep): bit-exact against the oracle; step counts not divisible by four
+    finish with two-step / one-step launches."""
+    nx, ny, nz, steps, es, ss, fs, has_src = CASES[name]
+    src = None
+    if has_src and nx > 2 and ny > 2 and nz > 2:
+        src = (2, nx // 2, ny // 2, nz // 2, oracle.gauss_table(steps))
+    f = oracle.fill_fields(nx, ny, nz, fs) if fs is not None else oracle.zeros_state(nx, ny, nz)
+    with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB4) as sim:
+        sim.generate_medium(es, ss)
+        if src is not None:
+            sim.add_source(*src[:4], src[4])
+        if fs is not None:
+            sim.fill(fs)
+        sim.run(steps)
+        got = sim.download()
+    want = oracle_run(oracle, nx, ny, nz, f, steps, medium=(es, ss) if es >= 0 or ss >= 0 else None, src=src)
+    assert_bits(got, want, name)
+
+
+@pytest.mark.parametrize("zchunk", [1, 3, 9, 0])
+def test_tb4_zchunks_and_probes(yb, oracle, zchunk):
+    nx, ny, nz, steps = 120, 26, 31, 12
+    f = oracle.fill_fields(nx, ny, nz, 41)
+    with yb.Simulation(nx, ny, nz, zchunk=zchunk, variant=yb.VARIANT_TB4) as sim:
+        sim.generate_medium(42, 43)
+        sim.upload(f)
+        sim.set_probes([(2, 60, 13, 15, 3), (3, 5, 6, 7, 4)])
+        sim.run(steps)
+        got = sim.download()
+        st, pr, va = sim.read_probes()
+    want = oracle_run(oracle, nx, ny, nz, [a.copy() for a in f], steps, medium=(42, 43))
+    assert_bits(got, want, f"tb4 zchunk={zchunk}")
+    assert st.tolist() == [3, 4, 6, 8, 9, 12, 12] and pr.tolist() == [0, 1, 0, 1, 0, 0, 1]
