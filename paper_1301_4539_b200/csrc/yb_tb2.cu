@@ -16,8 +16,9 @@
 // steps n and n+1 added after their E level, schedule.hpp:175-199).
 // Row warp w owns physical row y0-1+w at every level, so its own-row values
 // of earlier planes/levels stay in registers; the x0-1 / x0+128 / x0+129
-// columns are computed by a dedicated edge warp (lane = row). Two CTA
-// barriers per plane. Chunk boundaries re-stream two planes below and one
+// columns are computed by a dedicated edge warp (lane = row). One CTA
+// barrier per plane (between L2 and L3; the stage is released by per-warp
+// arrivals on its "empty" mbarrier). Chunk boundaries re-stream two planes below and one
 // above (the wavefront's z-halo). Arithmetic: yee_upd, bit-identical to two
 // single steps.
 #include <cuda.h>
