@@ -295,10 +295,13 @@ def main():
     launches = info1["kernel_launches"] - info0["kernel_launches"]
     value = cells_total * args.steps / (ms * 1e-3) / 1e9
     bpc = info1["bytes_per_cell_update"]
-    kern_ms = info1["main_kernel_ms"] / max(1, info1["main_kernel_timed"])
+    # device time of the sweep kernels in the timed region (events around every
+    # launch on the library's stream); one launch may cover many steps
+    kern_total = info1["main_kernel_ms"]
+    n_kern = max(1, info1["main_kernel_timed"])
+    kern_ms = kern_total / n_kern
     peak, peak_src = load_peak()
-    steps_per_launch = {Y.VARIANT_TB2: 2, Y.VARIANT_TB4: 4}.get(variant, 1)
-    achieved = bpc * cells * steps_per_launch / (kern_ms * 1e-3) / 1e9
+    achieved = bpc * cells * args.steps / (kern_total * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.config, args.variant),
                 "kernel": {0: "k_fused (one E+H sweep per step)", 1: "naive step (4 kernels)",
@@ -308,7 +311,8 @@ def main():
                 "one_sweep_bytes_per_cell_update": 48.0 + 4.0 * info1["n_cell_arrays"],
                 "effective_frac_vs_one_sweep": (48.0 + 4.0 * info1["n_cell_arrays"]) * cells
                                                * args.steps / (ms * 1e-3) / 1e9 / peak,
-                "step_ms_share_of_kernel": kern_ms / (ms / args.steps * steps_per_launch)}
+                "steps_per_launch": args.steps / n_kern,
+                "step_ms_share_of_kernel": kern_total / ms}
     config.update({"variant": args.variant, "stages": info1["stages"], "zchunk": info1["zchunk"],
                    "ctas": info1["grid_x"], "n_cell_arrays": info1["n_cell_arrays"]})
     if exch is not None:

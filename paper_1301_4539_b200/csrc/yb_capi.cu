@@ -125,6 +125,11 @@ struct yb_sim {
   int stages2 = 0, zchunk2 = 0, nitems2 = 1;
   dim3 grid2{1, 1, 1};
   yb::TMaps tm4[2];  // four-step sweep maps (64-column window boxes)
+  unsigned* done = nullptr;   // multi-sweep launches: per-item completion epochs
+  int done_n = 0;
+  unsigned epoch = 0;
+  yb::SrcArgs* srcs_dev = nullptr;  // per-sweep sources of a multi-sweep launch
+  int srcs_cap = 0;
   int stages4 = 0, zchunk4 = 0, ntx4 = 1, nty4 = 1;
   unsigned long long* sched = nullptr;  // device work counter of the fused kernel
   unsigned long long sched_base = 0;
@@ -144,6 +149,7 @@ struct yb_sim {
   cudaEvent_t peer_go = nullptr, peer_done = nullptr;
   bool peer_inflight = false;
   bool pending_full = false;  // ... whose boundary launch already covered every plane
+  bool persist = false;       // multi-sweep two-step launches (YB_TB2_PERSIST=1: on; measured no gain)
   bool qskip = false;         // yb_set_quiescent_skip
   bool q_valid = false;       // quiescent map matches the state buffers
   unsigned* qbits = nullptr;  // quiescent map (tiles x words)
@@ -475,7 +481,7 @@ int step_fused(yb_sim* s, ZPart z, int zchunk, bool flip) {
 }
 
 // Two Standard steps in one launch (temporal depth 2).
-int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip) {
+int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
   const int nxt = s->cur ^ 1;
   yb::FusedArgs a{};
   a.g = s->g;
@@ -483,6 +489,31 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip) {
   a.ntx = s->ntx;
   a.nty = s->nty;
   const dim3 grid = set_chunks(s, a, zchunk, z);
+  a.nsweeps = nsweeps;
+  a.err = reinterpret_cast<int*>(s->sched) + 6;
+  if (nsweeps > 1) {  // several sweeps in one launch, items ordered by dependency
+    if (s->done_n != a.nitems) {
+      cudaFree(s->done);
+      s->done = nullptr;
+      YB_CU(cudaMalloc(&s->done, (size_t)a.nitems * sizeof(unsigned)));
+      YB_CU(cudaMemsetAsync(s->done, 0, (size_t)a.nitems * sizeof(unsigned), s->stream));
+      s->done_n = a.nitems;
+      s->epoch = 0;
+    }
+    if (s->srcs_cap < nsweeps) {
+      cudaFree(s->srcs_dev);
+      s->srcs_dev = nullptr;
+      YB_CU(cudaMalloc(&s->srcs_dev, (size_t)nsweeps * sizeof(yb::SrcArgs)));
+      s->srcs_cap = nsweeps;
+    }
+    std::vector<yb::SrcArgs> sv(nsweeps);
+    for (int q = 0; q < nsweeps; ++q) sv[q] = sources_at(s, s->step_index + 2 * q, true);
+    YB_CU(cudaMemcpyAsync(s->srcs_dev, sv.data(), sv.size() * sizeof(yb::SrcArgs), cudaMemcpyHostToDevice,
+                          s->stream));
+    a.done = s->done;
+    a.epoch = s->epoch;
+    a.srcs = s->srcs_dev;
+  }
   a.sched = s->sched;
   a.sched_base = s->sched_base;
   a.store_policy = 1;
@@ -507,11 +538,12 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip) {
     tp = &s->timers[s->timers_used++];
     YB_CU(cudaEventRecord(tp->a, s->stream));
   }
-  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], mask, grid, smem, s->stream));
-  s->sched_base += (unsigned long long)a.nitems + grid.x;
+  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], s->tm2[nxt], mask, grid, smem, s->stream));
+  s->sched_base += (unsigned long long)a.nitems * nsweeps + grid.x;
+  if (nsweeps > 1) s->epoch += (unsigned)nsweeps;
   if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
   s->launches += 1;
-  if (flip) s->cur = nxt;
+  if (flip && (nsweeps & 1)) s->cur = nxt;
   if (s->timers_used >= 4096) return collect_timers(s);
   return YB_OK;
 }
@@ -682,6 +714,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   s->variant = d->variant;
   s->zchunk_req = d->zchunk;
   if (const char* e = std::getenv("YB_STPOL")) s->store_policy = std::atoi(e);
+  if (const char* e = std::getenv("YB_TB2_PERSIST")) s->persist = std::atoi(e) != 0;
   Geo& g = s->g;
   g.nx = d->nx;
   g.ny = d->ny;
@@ -756,6 +789,8 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->probe_dev);
   cudaFree(s->qbits);
   cudaFree(s->qskipped);
+  cudaFree(s->done);
+  cudaFree(s->srcs_dev);
   for (float* p : s->snap_h) cudaFree(p);
   for (PeerSide& ps : s->peer)
     for (void* p : ps.ipc) cudaIpcCloseMemHandle(p);
@@ -1129,6 +1164,18 @@ int yb_advance(yb_sim* s, int64_t nsteps) {
     }
     if (s->qskip && !s->q_valid)
       if (int rc = qmap_refresh(s)) return rc;
+    // several two-step sweeps in one launch (single domain, no probes, no
+    // quiescent skip): items of the next sweep start as their neighbourhood
+    // finishes, so no launch gap or wave tail separates the sweeps
+    if (s->variant == YB_VARIANT_TB2 && s->persist && !probes && !s->qskip && s->g.nzg == s->g.nz &&
+        nsteps - t >= 4) {
+      const int nsw = (int)std::min<int64_t>((nsteps - t) / 2, 1024);
+      if (int rc = step_tb2(s, zfull(s), s->zchunk2, true, nsw)) return rc;
+      s->step_index += 2 * nsw;
+      s->steps += 2 * nsw;
+      t += 2 * nsw;
+      continue;
+    }
     // two steps per launch unless a probe wants the level in between
     if ((s->variant == YB_VARIANT_TB2 || s->variant == YB_VARIANT_TB4) && t + 2 <= nsteps &&
         !(probes && probe_fires(s, s->step_index + 1))) {
@@ -1282,6 +1329,11 @@ int yb_synchronize(yb_sim* s) {
     int err = 0;
     YB_CU(cudaMemcpy(&err, s->pflags + 2, sizeof err, cudaMemcpyDeviceToHost));
     if (err) return fail(YB_RUNTIME_ERROR, "peer halo wait timed out (a neighbour never signalled)");
+  }
+  {
+    int err = 0;
+    YB_CU(cudaMemcpy(&err, reinterpret_cast<int*>(s->sched) + 6, sizeof err, cudaMemcpyDeviceToHost));
+    if (err) return fail(YB_RUNTIME_ERROR, "a multi-sweep launch timed out waiting for a dependency");
   }
   return collect_timers(s);
 }

@@ -56,7 +56,7 @@ inline int tb2_stage_floats(int cell_mask) {
 
 inline size_t tb2_smem_bytes(int cell_mask, int stages) {
   return (size_t)stages * tb2_stage_floats(cell_mask) * 4 + (size_t)(kTB2E1 + kTB2H1 + kTB2E2 + kTB2Edge) * 4 +
-         (size_t)stages * 16 + 8 * 4;
+         (size_t)stages * 16 + 16 * 4;  // mbarriers, item + sweep queues
 }
 
 struct TMaps {
@@ -82,6 +82,15 @@ struct FusedArgs {
   SrcArgs src;
   QMap qm;                       // quiescent map (qm.bits == nullptr: off)
   unsigned long long* skipped;   // skipped-item counter
+  // Several sweeps in one launch (two-step kernel, single domain): sweep s
+  // reads in[] for even s / out[] for odd s and writes the other; an item of
+  // sweep s >= 1 starts once its neighbourhood finished sweep s-1
+  // (done[item] >= epoch + s), and publishes done[item] = epoch + s + 1.
+  int nsweeps;                   // 1: an ordinary launch
+  unsigned* done;                // per-item completion epochs
+  unsigned epoch;
+  const SrcArgs* srcs;           // per-sweep sources (nsweeps > 1)
+  int* err;                      // set when a dependency wait timed out
 };
 
 // planes [kz0, kz1) of z-chunk c of a launch
@@ -118,8 +127,8 @@ cudaError_t launch_fused(const FusedArgs& a, const TMaps& tm, int cell_mask, dim
                          size_t smem, cudaStream_t st);
 cudaError_t fused_set_smem_limits();
 // Two full steps per launch (maps with kTB2BY-row boxes).
-cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid, size_t smem,
-                       cudaStream_t st);
+cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, const TMaps& tm_out, int cell_mask, dim3 grid,
+                       size_t smem, cudaStream_t st);
 cudaError_t tb2_set_smem_limits();
 
 cudaError_t launch_naive_ampere(const Geo& g, const Fields& F, const CoefArgs& co, const int* box,

@@ -170,6 +170,37 @@ __device__ __forceinline__ void mark_sources(const SrcArgs& s, Item& it) {
               s.j[q] <= it.y0 + kTB2Rows + 1 && s.k[q] >= it.pstart && s.k[q] <= it.pend;
 }
 
+// Multi-sweep launches: spin (bounded) until every item whose sweep-(sw-1)
+// work overlaps this item's reads or writes has published it — the 3 x 3
+// tile neighbourhood and the z-chunks covering planes kz0-3 .. kz1+2.
+__device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int sw) {
+  const int T = a.ntx * a.nty, ch = item / T, tile = item - ch * T;
+  const int tx = tile % a.ntx, ty = tile / a.ntx;
+  int kz0, kz1;
+  chunk_planes(a, ch, kz0, kz1);
+  const int c_lo = max(kz0 - 3, 0) / a.zchunk, c_hi = min((kz1 + 2) / a.zchunk, a.nch0 - 1);
+  const int y_lo = max(ty - 1, 0), y_hi = min(ty + 1, a.nty - 1);
+  const int x_lo = max(tx - 1, 0), x_hi = min(tx + 1, a.ntx - 1);
+  const unsigned need = a.epoch + (unsigned)sw;
+  for (long long n = 0;; ++n) {  // one pass of independent relaxed loads, then acquire
+    bool ok = true;
+    for (int cc = c_lo; cc <= c_hi; ++cc)
+      for (int yy = y_lo; yy <= y_hi; ++yy)
+        for (int xx = x_lo; xx <= x_hi; ++xx) {
+          unsigned v;
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.done + (cc * T + yy * a.ntx + xx)));
+          ok &= (int)(v - need) >= 0;
+        }
+    if (ok) break;
+    if (n > (1ll << 22)) {  // ~1 s: report instead of hanging
+      atomicExch(a.err, 1);
+      break;
+    }
+    __nanosleep(128);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 // Stage layout: fields (12 rows from y0-2), then Ca, Cb (11 rows from y0-1),
 // then Da, Db (10 rows from y0-1), each present only in per-cell mode.
 template <bool CAC, bool CBC, bool DAC, bool DBC>
@@ -229,8 +260,10 @@ struct Cursor {
 // plane parity) plus a compile-time offset; the i-1 /
 // i+1 neighbours of a lane's float4 are read as one scalar from the row in
 // shared memory (column c-1 / c+4; the edge columns for lanes 0 / 31).
-template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 struct Rows {
+  // MODE: 0 plain, 1 quiescent skip, 2 several sweeps per launch
+  static constexpr bool QS = MODE == 1, MS = MODE == 2;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   static constexpr int E1C = RW * BX, E1B = 3 * E1C;              // comp / buffer strides
   static constexpr int H1C = (RW - 1) * BX, H1B = 3 * H1C;
@@ -240,6 +273,8 @@ struct Rows {
   const Item& it;
   const Bufs& B;
   Cursor& cur;
+  float* const* outm;  // this sweep's output buffers (MS)
+  const SrcArgs& srcm;  // this sweep's sources (MS)
   const int er, l, j, c, i0;
   const bool xedge;
   const uint64_t st_pol;
@@ -254,9 +289,9 @@ struct Rows {
   F4x3 h0p;
   float4 cap, cbp, dap, dbp, dap2, dbp2;
 
-  __device__ __forceinline__ Rows(const FusedArgs& a_, const Item& it_, const Bufs& B_, Cursor& cur_, int er_,
-                                  int l_, uint64_t pol)
-      : a(a_), it(it_), B(B_), cur(cur_), er(er_), l(l_), j(it_.y0 - 1 + er_), c(4 + 4 * l_),
+  __device__ __forceinline__ Rows(const FusedArgs& a_, const Item& it_, const Bufs& B_, Cursor& cur_,
+                                  float* const* out_, const SrcArgs& src_, int er_, int l_, uint64_t pol)
+      : a(a_), it(it_), B(B_), cur(cur_), outm(out_), srcm(src_), er(er_), l(l_), j(it_.y0 - 1 + er_), c(4 + 4 * l_),
         i0(it_.x0 + 4 * l_), xedge(i0 == 0 || i0 + 4 > a_.g.nx), st_pol(pol),
         e1o(B_.e1b + er_ * BX + c), h1o(B_.h1b + er_ * BX + c), e2o(B_.e2b + (er_ - 1) * BX + c) {
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -270,6 +305,9 @@ struct Rows {
     zh = a.co.cdz_h[it_.pstart - 1];
     ze1 = zh1 = 0.f;
   }
+
+  __device__ __forceinline__ float* outp(int q) const { return MS ? outm[q] : a.out[q]; }
+  __device__ __forceinline__ const SrcArgs& src() const { return MS ? srcm : a.src; }
 
   __device__ __forceinline__ void prologue() {
     const int rs = er + 1;
@@ -311,12 +349,12 @@ struct Rows {
                                 lds4(Fr + kTB2SlotF), lds4(Fr + 2 * kTB2SlotF), h0n.x, h0n.y, h0n.z,
                                 lds4(Fr + 3 * kTB2SlotF - BX), lds4(Fr + 5 * kTB2SlotF - BX), hy_im, hz_im, h0p.x,
                                 h0p.y);
-      if (it.src && src_row(a.src, 1, j, p)) {
+      if (it.src && src_row(src(), 1, j, p)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          el(e1c.x, q) = __fadd_rn(el(e1c.x, q), src_add(a.src, 1, 0, i0 + q, j, p));
-          el(e1c.y, q) = __fadd_rn(el(e1c.y, q), src_add(a.src, 1, 1, i0 + q, j, p));
-          el(e1c.z, q) = __fadd_rn(el(e1c.z, q), src_add(a.src, 1, 2, i0 + q, j, p));
+          el(e1c.x, q) = __fadd_rn(el(e1c.x, q), src_add(src(), 1, 0, i0 + q, j, p));
+          el(e1c.y, q) = __fadd_rn(el(e1c.y, q), src_add(src(), 1, 1, i0 + q, j, p));
+          el(e1c.z, q) = __fadd_rn(el(e1c.z, q), src_add(src(), 1, 2, i0 + q, j, p));
         }
       }
       float* w = e1o + PAR * E1B;
@@ -371,12 +409,12 @@ struct Rows {
       e2c = e_update4<CAC, CBC>(co, g, i0, xedge, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp, lds4(e),
                                 lds4(e + E1C), lds4(e + 2 * E1C), hx, hy, hz, lds4(h - BX), lds4(h + 2 * H1C - BX),
                                 hy_im, hz_im, lds4(hp), lds4(hp + H1C));
-      if (it.src && src_row(a.src, 2, j, kh)) {
+      if (it.src && src_row(src(), 2, j, kh)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          el(e2c.x, q) = __fadd_rn(el(e2c.x, q), src_add(a.src, 2, 0, i0 + q, j, kh));
-          el(e2c.y, q) = __fadd_rn(el(e2c.y, q), src_add(a.src, 2, 1, i0 + q, j, kh));
-          el(e2c.z, q) = __fadd_rn(el(e2c.z, q), src_add(a.src, 2, 2, i0 + q, j, kh));
+          el(e2c.x, q) = __fadd_rn(el(e2c.x, q), src_add(src(), 2, 0, i0 + q, j, kh));
+          el(e2c.y, q) = __fadd_rn(el(e2c.y, q), src_add(src(), 2, 1, i0 + q, j, kh));
+          el(e2c.z, q) = __fadd_rn(el(e2c.z, q), src_add(src(), 2, 2, i0 + q, j, kh));
         }
       }
       float* w = e2o + Q * E2B;
@@ -386,9 +424,9 @@ struct Rows {
       const bool own = er <= kTB2Rows && j < g.ny && kh < it.kz1;
       if (own) {  // E^{n+2} of the owned rows -> HBM
         const long long gp = gidx(g, i0, j, kh);
-        store_row4(a.out[0], gp, i0, g.nx, e2c.x, st_pol);
-        store_row4(a.out[1], gp, i0, g.nx, e2c.y, st_pol);
-        store_row4(a.out[2], gp, i0, g.nx, e2c.z, st_pol);
+        store_row4(outp(0), gp, i0, g.nx, e2c.x, st_pol);
+        store_row4(outp(1), gp, i0, g.nx, e2c.y, st_pol);
+        store_row4(outp(2), gp, i0, g.nx, e2c.z, st_pol);
       }
       if (QS) {
         const bool nz = own && (nonzero4(e2c.x) | nonzero4(e2c.y) | nonzero4(e2c.z));
@@ -422,9 +460,9 @@ struct Rows {
       }
       if (j < g.ny) {
         const long long gp = gidx(g, i0, j, k4);
-        store_row4(a.out[3], gp, i0, g.nx, h2.x, st_pol);
-        store_row4(a.out[4], gp, i0, g.nx, h2.y, st_pol);
-        store_row4(a.out[5], gp, i0, g.nx, h2.z, st_pol);
+        store_row4(outp(3), gp, i0, g.nx, h2.x, st_pol);
+        store_row4(outp(4), gp, i0, g.nx, h2.y, st_pol);
+        store_row4(outp(5), gp, i0, g.nx, h2.z, st_pol);
       }
       if (QS && j < g.ny) {
         const bool nz = nonzero4(h2.x) | nonzero4(h2.y) | nonzero4(h2.z);
@@ -448,10 +486,10 @@ struct Rows {
   }
 };
 
-template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
-                                         int er, int l, uint64_t st_pol) {
-  Rows<CAC, CBC, DAC, DBC, QS> R(a, it, B, cur, er, l, st_pol);
+                                         float* const* out, const SrcArgs& src, int er, int l, uint64_t st_pol) {
+  Rows<CAC, CBC, DAC, DBC, MODE> R(a, it, B, cur, out, src, er, l, st_pol);
   if (it.pro) R.prologue();
   for (int p = it.pstart; p <= it.pend; ++p) R.plane(p);
 }
@@ -462,9 +500,9 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
 // level — L1: 11 + 11 + 10 = 32 tasks, L2: 20, L3: 9 — and all state that
 // crosses planes (H0, Da/Db, Ca/Cb of these columns) lives in shared memory
 // (Bufs::h0e/de/cee), so any lane can pick up any task.
-template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, const Bufs& B, Cursor& cur,
-                                         int l) {
+                                         const SrcArgs& src, int l) {
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   const Geo& g = a.g;
   const CoefArgs& co = a.co;
@@ -510,10 +548,10 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
                           cb, Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], hx, hy, hz, Fr[3 * kTB2SlotF - BX],
                           Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1], Fr[5 * kTB2SlotF - 1],
                           *B.H0e((p - 1) & 1, 0, r, e1i), *B.H0e((p - 1) & 1, 1, r, e1i), ox, oy, oz);
-      if (it.src && src_row(a.src, 1, j, p)) {
-        ox = __fadd_rn(ox, src_add(a.src, 1, 0, i, j, p));
-        oy = __fadd_rn(oy, src_add(a.src, 1, 1, i, j, p));
-        oz = __fadd_rn(oz, src_add(a.src, 1, 2, i, j, p));
+      if (it.src && src_row(src, 1, j, p)) {
+        ox = __fadd_rn(ox, src_add(src, 1, 0, i, j, p));
+        oy = __fadd_rn(oy, src_add(src, 1, 1, i, j, p));
+        oz = __fadd_rn(oz, src_add(src, 1, 2, i, j, p));
       }
       *B.E1(p & 1, 0, r, col) = ox;
       *B.E1(p & 1, 1, r, col) = oy;
@@ -562,10 +600,10 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
                           *B.H1(hb, 0, r - 1, CR), *B.H1(hb, 2, r - 1, CR), *B.H1(hb, 1, r, CR - 1),
                           *B.H1(hb, 2, r, CR - 1), *B.H1(hb ^ 1, 0, r, CR), *B.H1(hb ^ 1, 1, r, CR), ox, oy,
                           oz);
-      if (it.src && src_row(a.src, 2, j, kh)) {
-        ox = __fadd_rn(ox, src_add(a.src, 2, 0, i, j, kh));
-        oy = __fadd_rn(oy, src_add(a.src, 2, 1, i, j, kh));
-        oz = __fadd_rn(oz, src_add(a.src, 2, 2, i, j, kh));
+      if (it.src && src_row(src, 2, j, kh)) {
+        ox = __fadd_rn(ox, src_add(src, 2, 0, i, j, kh));
+        oy = __fadd_rn(oy, src_add(src, 2, 1, i, j, kh));
+        oz = __fadd_rn(oz, src_add(src, 2, 2, i, j, kh));
       }
       *B.E2(hb, 0, r - 1, CR) = ox;
       *B.E2(hb, 1, r - 1, CR) = oy;
@@ -576,8 +614,10 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
   }
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
-__global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm) {
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
+__global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm,
+                                       const __grid_constant__ TMaps tm_o) {
+  constexpr bool QS = MODE == 1, MS = MODE == 2;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
   constexpr uint32_t kBytesF = kBX * kTB2BY * 4, kBytesC = kBX * kTB2RowsCA * 4,
@@ -598,6 +638,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   B.full = reinterpret_cast<uint64_t*>(B.edge + kTB2Edge);
   B.empty = B.full + S;
   int* item_q = reinterpret_cast<int*>(B.empty + S);
+  int* sweep_q = item_q + kQ;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int T = a.ntx * a.nty;
 
@@ -610,31 +651,53 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   }
   __syncthreads();
 
-  if (w == FACE) {  // upper-face DoFs, two steps: h <- Da*(Da*h + 0) + 0
+  if (w == FACE) {  // upper-face DoFs, two steps per sweep: h <- Da*(Da*h + 0) + 0
+    // (no sweep reads them for a valid update, so all sweeps' steps are applied
+    // here in order, into the buffer that holds the launch's final state)
     const long long nf = face_points(g);
+    if (!MS) {
+      for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {
+        face_point(g, a.in, a.out, co, t);
+        face_point(g, a.out, a.out, co, t);
+      }
+      return;
+    }
+    float* const* fin = (a.nsweeps & 1) ? a.out : const_cast<float* const*>(reinterpret_cast<const float* const*>(a.in));
     for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {
-      face_point(g, a.in, a.out, co, t);
-      face_point(g, a.out, a.out, co, t);
+      face_point(g, a.in, fin, co, t);
+      for (int q = 1; q < 2 * a.nsweeps; ++q) face_point(g, fin, fin, co, t);
     }
     return;
   }
 
   if (w == PROD) {  // TMA producer (one lane)
     if (l != 0) return;
-    int p_item = -1, p_e = 0, p_nE = 0, p_seq = 0;
+    int p_item = -1, p_e = 0, p_nE = 0, p_seq = 0, p_sweep = 0;
     for (int q = 0;; ++q) {
       const int s = q % S;
       if (q >= S) mbar_wait(smem_u32(&B.empty[s]), (uint32_t)(((q / S) - 1) & 1));
       const uint32_t bar = smem_u32(&B.full[s]);
       if (p_item < 0) {
         const unsigned long long v = atomicAdd(a.sched, 1ull) - a.sched_base;
-        const int it = v < (unsigned long long)a.nitems ? (int)v : -1;
+        int it = -1, sw = 0;
+        if (!MS) {
+          it = v < (unsigned long long)a.nitems ? (int)v : -1;
+        } else if (v < (unsigned long long)a.nitems * a.nsweeps) {
+          sw = (int)(v / (unsigned long long)a.nitems);
+          it = (int)(v - (unsigned long long)sw * a.nitems);
+        }
         item_q[p_seq % kQ] = it;
+        if (MS) sweep_q[p_seq % kQ] = sw;
         ++p_seq;
         if (it < 0) {
           mbar_arrive(bar);
           return;
         }
+        if (MS && sw > 0) {  // the neighbourhood must have finished the previous sweep
+          wait_neighbours(a, it, sw);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
+        }
+        p_sweep = sw;
         const Item pi = make_item(a, g, it, T, a.ntx);
         if (QS) {  // quiescent item: input box all +0, no source in either step -> skip
           const int tl = it % T;
@@ -654,23 +717,24 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       const Item pi = make_item(a, g, p_item, T, a.ntx);
       const int x0 = pi.x0, y0 = pi.y0;
       const int pro = pi.pro ? 1 : 0;
+      const TMaps& M = (MS && (p_sweep & 1)) ? tm_o : tm;  // this sweep's input state
       float* dst = B.stages + (size_t)s * L::floats;
       // tensor z coordinate = local plane + kGhost
       if (pro && p_e == 0) {  // hx, hy of plane pstart-1
         mbar_expect_tx(bar, 2 * kBytesF);
-        tma_load_3d(smem_u32(dst + 3 * kTB2SlotF), &tm.m[3], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
-        tma_load_3d(smem_u32(dst + 4 * kTB2SlotF), &tm.m[4], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
+        tma_load_3d(smem_u32(dst + 3 * kTB2SlotF), &M.m[3], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
+        tma_load_3d(smem_u32(dst + 4 * kTB2SlotF), &M.m[4], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
       } else {
         const int z = pi.pstart + p_e - pro + kGhost;
         mbar_expect_tx(bar, kStageBytes);
 #pragma unroll
         for (int q2 = 0; q2 < 6; ++q2)
-          tma_load_3d(smem_u32(dst + q2 * kTB2SlotF), &tm.m[q2], x0 - 4, y0 - 2, z, bar);
+          tma_load_3d(smem_u32(dst + q2 * kTB2SlotF), &M.m[q2], x0 - 4, y0 - 2, z, bar);
         int m = 6;
-        if (CAC) tma_load_3d(smem_u32(dst + L::off_ca), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
-        if (CBC) tma_load_3d(smem_u32(dst + L::off_cb), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
-        if (DAC) tma_load_3d(smem_u32(dst + L::off_da), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
-        if (DBC) tma_load_3d(smem_u32(dst + L::off_db), &tm.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (CAC) tma_load_3d(smem_u32(dst + L::off_ca), &M.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (CBC) tma_load_3d(smem_u32(dst + L::off_cb), &M.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (DAC) tma_load_3d(smem_u32(dst + L::off_da), &M.m[m++], x0 - 4, y0 - 1, z, bar);
+        if (DBC) tma_load_3d(smem_u32(dst + L::off_db), &M.m[m++], x0 - 4, y0 - 1, z, bar);
         (void)NARR;
       }
       if (++p_e == p_nE) p_item = -1;
@@ -685,62 +749,75 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
     mbar_wait(smem_u32(&B.full[cur.s]), cur.ph);
     cur.peeked = true;
     const int item = item_q[c_seq % kQ];
+    const int sw = MS ? sweep_q[c_seq % kQ] : 0;
     ++c_seq;
     if (item < 0) break;
     if (QS && (item & kSkipItem)) {  // quiescent: consume the empty stage, nothing to write
       release_stage(B.empty, cur.wait(B, S), l);
       continue;
     }
+    const SrcArgs& src = MS ? a.srcs[sw] : a.src;
+    float* const* out = (MS && (sw & 1)) ? const_cast<float* const*>(reinterpret_cast<const float* const*>(a.in)) : a.out;
     Item it = make_item(a, g, item, T, a.ntx);
-    mark_sources(a.src, it);
+    mark_sources(src, it);
     if (w == EDGE)
-      tb2_edge<CAC, CBC, DAC, DBC, QS>(a, it, B, cur, l);
+      tb2_edge<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, src, l);
     else
-      tb2_rows<CAC, CBC, DAC, DBC, QS>(a, it, B, cur, w, l, st_pol);
+      tb2_rows<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, out, src, w, l, st_pol);
+    if (MS) {  // publish: this item's part of sweep sw is in global memory
+      consumer_sync();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done + item), "r"(a.epoch + sw + 1) : "memory");
+      }
+    }
   }
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
-cudaError_t launch_t(const FusedArgs& a, const TMaps& tm, dim3 grid, size_t smem, cudaStream_t st) {
-  k_tb2<CAC, CBC, DAC, DBC, QS><<<grid, kTB2Threads, smem, st>>>(a, tm);
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
+cudaError_t launch_t(const FusedArgs& a, const TMaps& tm, const TMaps& tm_o, dim3 grid, size_t smem,
+                     cudaStream_t st) {
+  k_tb2<CAC, CBC, DAC, DBC, MODE><<<grid, kTB2Threads, smem, st>>>(a, tm, tm_o);
   return cudaGetLastError();
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC, bool QS>
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 cudaError_t set_limit_t() {
-  return cudaFuncSetAttribute(k_tb2<CAC, CBC, DAC, DBC, QS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_tb2<CAC, CBC, DAC, DBC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               227 * 1024);
 }
 
-using LaunchFn = cudaError_t (*)(const FusedArgs&, const TMaps&, dim3, size_t, cudaStream_t);
+using LaunchFn = cudaError_t (*)(const FusedArgs&, const TMaps&, const TMaps&, dim3, size_t, cudaStream_t);
 using LimitFn = cudaError_t (*)();
 
-#define YB_T(m) launch_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m & 16) != 0>
-#define YB_L(m) set_limit_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m & 16) != 0>
-const LaunchFn kLaunch[32] = {YB_T(0),  YB_T(1),  YB_T(2),  YB_T(3),  YB_T(4),  YB_T(5),  YB_T(6),  YB_T(7),
-                              YB_T(8),  YB_T(9),  YB_T(10), YB_T(11), YB_T(12), YB_T(13), YB_T(14), YB_T(15),
-                              YB_T(16), YB_T(17), YB_T(18), YB_T(19), YB_T(20), YB_T(21), YB_T(22), YB_T(23),
-                              YB_T(24), YB_T(25), YB_T(26), YB_T(27), YB_T(28), YB_T(29), YB_T(30), YB_T(31)};
-const LimitFn kLimit[32] = {YB_L(0),  YB_L(1),  YB_L(2),  YB_L(3),  YB_L(4),  YB_L(5),  YB_L(6),  YB_L(7),
-                            YB_L(8),  YB_L(9),  YB_L(10), YB_L(11), YB_L(12), YB_L(13), YB_L(14), YB_L(15),
-                            YB_L(16), YB_L(17), YB_L(18), YB_L(19), YB_L(20), YB_L(21), YB_L(22), YB_L(23),
-                            YB_L(24), YB_L(25), YB_L(26), YB_L(27), YB_L(28), YB_L(29), YB_L(30), YB_L(31)};
+// index: bits 0-3 per-cell Ca/Cb/Da/Db, then 16 * MODE
+#define YB_B(m) (m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m >> 4)
+#define YB_T(m) launch_t<YB_B(m)>
+#define YB_L(m) set_limit_t<YB_B(m)>
+#define YB_8(F, b) F(b), F(b + 1), F(b + 2), F(b + 3), F(b + 4), F(b + 5), F(b + 6), F(b + 7)
+const LaunchFn kLaunch[48] = {YB_8(YB_T, 0),  YB_8(YB_T, 8),  YB_8(YB_T, 16),
+                              YB_8(YB_T, 24), YB_8(YB_T, 32), YB_8(YB_T, 40)};
+const LimitFn kLimit[48] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16),
+                            YB_8(YB_L, 24), YB_8(YB_L, 32), YB_8(YB_L, 40)};
+#undef YB_8
 #undef YB_T
 #undef YB_L
+#undef YB_B
 
 }  // namespace
 
 cudaError_t tb2_set_smem_limits() {
-  for (int m = 0; m < 32; ++m) {
+  for (int m = 0; m < 48; ++m) {
     const cudaError_t e = kLimit[m]();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, int cell_mask, dim3 grid, size_t smem,
-                       cudaStream_t st) {
-  return kLaunch[(cell_mask & 15) | (a.qm.bits ? 16 : 0)](a, tm, grid, smem, st);
+cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, const TMaps& tm_out, int cell_mask, dim3 grid,
+                       size_t smem, cudaStream_t st) {
+  const int mode = a.nsweeps > 1 ? 2 : (a.qm.bits ? 1 : 0);
+  return kLaunch[(cell_mask & 15) | (mode << 4)](a, tm, tm_out, grid, smem, st);
 }
 
 }  // namespace yb

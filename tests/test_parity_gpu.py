@@ -550,3 +550,30 @@ def test_tb4_zchunks_and_probes(yb, oracle, zchunk):
     want = oracle_run(oracle, nx, ny, nz, [a.copy() for a in f], steps, medium=(42, 43))
     assert_bits(got, want, f"tb4 zchunk={zchunk}")
     assert st.tolist() == [3, 4, 6, 8, 9, 12, 12] and pr.tolist() == [0, 1, 0, 1, 0, 0, 1]
+
+
+@pytest.mark.parametrize("name", ["c2_dielectric_src", "c3_lossy_fields", "odd_sizes", "two_tiles_partial",
+                                  "thin_z"])
+@pytest.mark.parametrize("zchunk", [0, 1, 4])
+def test_multi_sweep_launches(yb, oracle, name, zchunk, monkeypatch):
+    """Several two-step sweeps per launch (YB_TB2_PERSIST=1): items of sweep s
+    start once their neighbourhood finished sweep s-1 (device-side completion
+    epochs). Bit-exact, with per-sweep sources."""
+    monkeypatch.setenv("YB_TB2_PERSIST", "1")
+    nx, ny, nz, steps, es, ss, fs, has_src = CASES[name]
+    src = None
+    if has_src and nx > 2 and ny > 2 and nz > 2:
+        src = (2, nx // 2, ny // 2, nz // 2, oracle.gauss_table(steps))
+    f = oracle.fill_fields(nx, ny, nz, fs) if fs is not None else oracle.zeros_state(nx, ny, nz)
+    with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2, zchunk=zchunk) as sim:
+        sim.generate_medium(es, ss)
+        if src is not None:
+            sim.add_source(*src[:4], src[4])
+        if fs is not None:
+            sim.fill(fs)
+        sim.run(steps)
+        launches = sim.info()["kernel_launches"]
+        got = sim.download()
+    assert launches <= 3 + steps % 2  # the pairs ran in one launch
+    want = oracle_run(oracle, nx, ny, nz, f, steps, medium=(es, ss) if es >= 0 or ss >= 0 else None, src=src)
+    assert_bits(got, want, name)
