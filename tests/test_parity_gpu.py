@@ -577,3 +577,22 @@ def test_multi_sweep_launches(yb, oracle, name, zchunk, monkeypatch):
     assert launches <= 3 + steps % 2  # the pairs ran in one launch
     want = oracle_run(oracle, nx, ny, nz, f, steps, medium=(es, ss) if es >= 0 or ss >= 0 else None, src=src)
     assert_bits(got, want, name)
+
+
+@pytest.mark.parametrize("variant", [0, 2, 3])
+def test_uniform_non_unit_ca_da(yb, oracle, variant):
+    """A uniform Ca / Da other than 1 (yb_set_cell_coeffs(which, NULL, v)):
+    stored as a full array (the sweep kernels treat 'no array' as exactly 1)."""
+    nx, ny, nz, steps = 44, 30, 20, 8
+    f = oracle.fill_fields(nx, ny, nz, 17)
+    with yb.Simulation(nx, ny, nz, variant=variant) as sim:
+        sim.set_cell_coeffs(yb.CA, None, 0.75)
+        sim.set_cell_coeffs(yb.DA, np.full((nz, ny, nx), 0.5, np.float32))
+        assert sim.info()["n_cell_arrays"] == 2
+        sim.upload(f)
+        sim.run(steps)
+        got = sim.download()
+    co = oracle.Coeffs(nx, ny, nz, ca_s=0.75, da_s=0.5)
+    want = [a.copy() for a in f]
+    oracle.run(nx, ny, nz, want, co, steps)
+    assert_bits(got, want, "uniform Ca/Da != 1")
