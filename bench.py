@@ -215,8 +215,8 @@ def main():
         args.variant = "tb2"
     variant = {"fused": Y.VARIANT_FUSED, "naive": Y.VARIANT_NAIVE, "tb2": Y.VARIANT_TB2,
                "tb4": Y.VARIANT_TB4}[args.variant]
-    if world > 1 and variant == Y.VARIANT_NAIVE:
-        raise SystemExit("z-slab multi-GPU runs need a sweep variant (fused or tb2)")
+    if world > 1 and variant in (Y.VARIANT_NAIVE, Y.VARIANT_TB4):
+        raise SystemExit("z-slab multi-GPU runs need the fused or tb2 variant")
 
     # z-slab decomposition (§8(e)): config 4 is strong scaling (fixed grid),
     # every other config weak scaling (each GPU keeps the config's depth).
