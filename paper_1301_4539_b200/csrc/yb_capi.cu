@@ -123,6 +123,7 @@ struct yb_sim {
   int ntx = 1, nty = 1, nitems = 1;
   yb::TMaps tm2[2];  // two-step sweep maps (taller boxes)
   int stages2 = 0, zchunk2 = 0, nitems2 = 1;
+  int zchunk2p = 0;  // z-chunk of multi-sweep launches (0: this grid does not use them)
   dim3 grid2{1, 1, 1};
   yb::TMaps tm4[2];  // four-step sweep maps (64-column window boxes)
   unsigned* done = nullptr;   // multi-sweep launches: per-item completion epochs
@@ -149,7 +150,7 @@ struct yb_sim {
   cudaEvent_t peer_go = nullptr, peer_done = nullptr;
   bool peer_inflight = false;
   bool pending_full = false;  // ... whose boundary launch already covered every plane
-  bool persist = false;       // multi-sweep two-step launches (YB_TB2_PERSIST=1: on; measured no gain)
+  bool persist = true;        // multi-sweep two-step launches (YB_TB2_PERSIST=0: off)
   bool qskip = false;         // yb_set_quiescent_skip
   bool q_valid = false;       // quiescent map matches the state buffers
   unsigned* qbits = nullptr;  // quiescent map (tiles x words)
@@ -346,6 +347,18 @@ int prepare_fused(yb_sim* s) {
     }
     zc2 = std::min(std::max(zc2, 1), s->g.nz);
     s->zchunk2 = zc2;
+    // Multi-sweep launches have no wave tail (the next sweep fills idle SMs),
+    // so they take the longest chunks that still leave >= 2 items per SM in
+    // a sweep; each chunk boundary re-streams ~3 planes. Grids too small for
+    // chunks of >= 16 planes stay on one launch per sweep (measured: a small
+    // grid's dependency waits serialise).
+    {
+      const long long T = (long long)tx * ty, need = 2LL * s->num_sms;
+      // (chunks capped at 256 planes: longer ones measured no better)
+      const int Zr = (int)std::min<long long>(s->g.nz, std::max<long long>((need + T - 1) / T, (s->g.nz + 255) / 256));
+      const int len = (s->g.nz + Zr - 1) / Zr;
+      s->zchunk2p = s->zchunk_req > 0 ? std::min(s->zchunk_req, s->g.nz) : (len >= 16 ? len : 0);
+    }
     s->nitems2 = tx * ty * ((s->g.nz + zc2 - 1) / zc2);
     s->grid2 = dim3(std::min(s->nitems2, s->num_sms), 1, 1);
   }
@@ -1167,10 +1180,10 @@ int yb_advance(yb_sim* s, int64_t nsteps) {
     // several two-step sweeps in one launch (single domain, no probes, no
     // quiescent skip): items of the next sweep start as their neighbourhood
     // finishes, so no launch gap or wave tail separates the sweeps
-    if (s->variant == YB_VARIANT_TB2 && s->persist && !probes && !s->qskip && s->g.nzg == s->g.nz &&
-        nsteps - t >= 4) {
+    if (s->variant == YB_VARIANT_TB2 && s->persist && s->zchunk2p > 0 && !probes && !s->qskip &&
+        s->g.nzg == s->g.nz && nsteps - t >= 4) {
       const int nsw = (int)std::min<int64_t>((nsteps - t) / 2, 1024);
-      if (int rc = step_tb2(s, zfull(s), s->zchunk2, true, nsw)) return rc;
+      if (int rc = step_tb2(s, zfull(s), s->zchunk2p, true, nsw)) return rc;
       s->step_index += 2 * nsw;
       s->steps += 2 * nsw;
       t += 2 * nsw;
@@ -1661,7 +1674,7 @@ int yb_get_info(yb_sim* s, yb_info* info) {
   } else if (s->variant == YB_VARIANT_TB2) {
     info->stages = s->stages2;
     info->grid_x = (int)s->grid2.x;
-    info->zchunk = s->zchunk2;
+    info->zchunk = (s->persist && s->zchunk2p > 0 && s->g.nzg == s->g.nz && !s->qskip) ? s->zchunk2p : s->zchunk2;
   }
   info->device_bytes = s->dev_bytes;
   info->halo_depth = halo_depth(s);
