@@ -139,11 +139,13 @@ def cpu_reference_rate(nx, ny, nz, budget_s=10.0, max_steps=None):
 
 
 def load_traffic(cfg, variant):
+    """ncu DRAM bytes per cell-update of this config's sweep kernel (profiles/ncu_traffic.json,
+    written by tools/ncu_summary.py from one --set full capture), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            t = json.load(fh)
-        return t.get(f"{cfg}:{variant}")
+            t = json.load(fh).get(f"{cfg}:{variant}")
+        return t.get("bytes_per_cell_update") if isinstance(t, dict) else None
     except Exception:
         return None
 
@@ -302,8 +304,12 @@ def main():
     kern_ms = kern_total / n_kern
     peak, peak_src = load_peak()
     achieved = bpc * cells * args.steps / (kern_total * 1e-3) / 1e9
+    # ncu DRAM bytes per launch, scaled to this run's launches (steps per launch x cells)
+    traffic_bpc = load_traffic(args.config, args.variant)
+    traffic = traffic_bpc * cells * args.steps / n_kern if traffic_bpc else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.config, args.variant),
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_bytes_per_cell_update": traffic_bpc,
                 "kernel": {0: "k_fused (one E+H sweep per step)", 1: "naive step (4 kernels)",
                            2: "k_tb2 (two steps per sweep)", 3: "k_tb4 (four steps per sweep)"}[variant],
                 "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,

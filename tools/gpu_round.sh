@@ -15,7 +15,10 @@ timeout 300 $CMD > $O/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv $CMD > $O/ncu_launch.log 2>&1; echo ncu_launch=$?
 for c in c2 c3; do for v in tb2 fused; do
   K=$([ "$v" = tb2 ] && echo k_tb2 || echo k_fused)
-  CMDP="python bench.py --config $c --variant $v --steps 4 --warmup 4 --no-cpu-baseline --no-e2e"
+  # tb2: warm-up 4 steps = one 2-sweep launch, timed 8 steps = one 4-sweep launch (profiled);
+  # fused: one launch per step, the 5th is profiled
+  if [ "$v" = tb2 ]; then ST=8; SK=1; else ST=4; SK=4; fi
+  CMDP="python bench.py --config $c --variant $v --steps $ST --warmup 4 --no-cpu-baseline --no-e2e"
   timeout 300 $CMDP > $O/plain_${c}_$v.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 -o $O/prof_${c}_$v $CMDP > $O/ncu_${c}_$v.log 2>&1; echo ncu_${c}_$v=$?
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $SK -c 1 -o $O/prof_${c}_$v $CMDP > $O/ncu_${c}_$v.log 2>&1; echo ncu_${c}_$v=$?
 done; done

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise an ncu --set full report of k_fused into profiles/.
 
-usage: python tools/ncu_summary.py <report.ncu-rep> <config-key> <out.txt> [cells]
+usage: python tools/ncu_summary.py <report.ncu-rep> <config-key> <out.txt> [cell-updates in the launch]
 Writes the key metrics (duration, DRAM bytes, throughputs, stall reasons,
 registers, occupancy) as text and merges the per-launch DRAM traffic into
 profiles/ncu_traffic.json under <config-key> (read by bench.py).
@@ -42,7 +42,7 @@ KEYS = [
 
 def main():
     rep, key, out = sys.argv[1:4]
-    cells = float(sys.argv[4]) if len(sys.argv) > 4 else None
+    cells = float(sys.argv[4]) if len(sys.argv) > 4 else None  # cell-updates in the profiled launch
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -76,7 +76,9 @@ def main():
         t = json.load(open(tj))
     except Exception:
         t = {}
-    t[key] = rd + wr
+    t[key] = {"bytes_per_launch": rd + wr}
+    if cells:
+        t[key]["bytes_per_cell_update"] = (rd + wr) / cells
     json.dump(t, open(tj, "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
 
