@@ -22,3 +22,16 @@ for c in c2 c3; do for v in tb2 fused; do
   timeout 300 $CMDP > $O/plain_${c}_$v.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $SK -c 1 -o $O/prof_${c}_$v $CMDP > $O/ncu_${c}_$v.log 2>&1; echo ncu_${c}_$v=$?
 done; done
+# summarise on the box (gpurun copies back <= 64 MiB): text summaries + traffic json, keep only
+# the config-2 two-step report
+cp profiles/ncu_traffic.json $O/ncu_traffic.json
+for c in c2 c3; do for v in tb2 fused; do
+  k=$([ "$v" = tb2 ] && echo k_tb2 || echo k_fused)
+  if [ "$v" = tb2 ]; then ST=8; else ST=1; fi
+  CELLS=$(python -c "print({'c2': 256**3, 'c3': 512**3}['$c'] * $ST)")
+  NCU_TRAFFIC_JSON=$O/ncu_traffic.json python tools/ncu_summary.py $O/prof_${c}_$v.ncu-rep $c:$v $O/r1_ncu_${c}_${k}.txt $CELLS > /dev/null 2>&1
+done; done
+python tools/ncu_lines.py $O/prof_c2_tb2.ncu-rep 30 > $O/r1_ncu_c2_k_tb2_lines.txt 2>&1
+rm -f $O/prof_c3_*.ncu-rep $O/prof_c2_fused.ncu-rep
+du -sh $O
+

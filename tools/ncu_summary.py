@@ -71,7 +71,8 @@ def main():
         lines.append(f"DRAM bytes per cell-update: {(rd + wr) / cells:.2f} (read {rd / cells:.2f}, "
                      f"write {wr / cells:.2f})")
     open(out, "w").write("\n".join(lines) + "\n")
-    tj = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")
+    tj = os.environ.get("NCU_TRAFFIC_JSON") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "..",
+                                                            "profiles", "ncu_traffic.json")
     try:
         t = json.load(open(tj))
     except Exception:
