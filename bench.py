@@ -9,8 +9,12 @@ plus the Cb array exceed the 126 MB L2, so no L2 flush is needed between
 steps (stated in config).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
-                  [--impl ours|reference] [--variant fused|naive]
+                  [--impl ours|reference] [--variant auto|tb2|fused|tb4|naive]
+                  [--exchange nccl|p2p] [--no-overlap] [--zchunk Z]
 
+Variant auto = tb2: two full steps per sweep; on one GPU several sweeps run in
+one launch (device-side dependencies between sweeps), on N > 1 each rank's
+z-slab exchanges ghost planes every two steps, overlapped with its interior.
 Prints ONE JSON line (rank 0). N>1: launched under torchrun, one rank per GPU.
 """
 import argparse
