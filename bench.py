@@ -267,7 +267,7 @@ def main():
         if exch is None:
             s_.run(n, sync=False)
         elif args.exchange == "p2p":
-            run_steps_peer(s_, n, depth, overlap=not args.no_overlap)
+            run_steps_peer(s_, n, depth)
         else:
             run_steps(s_, exch, n, depth, overlap=not args.no_overlap)
 
@@ -328,8 +328,8 @@ def main():
     if exch is not None:
         config["exchange_every_steps"] = depth
         if args.exchange == "p2p":
-            config["exchange"] = ("peer-memory push (CUDA IPC / NVLink), device-side flags" +
-                                  ("" if args.no_overlap else ", overlapped with the interior sweep"))
+            config["exchange"] = ("peer memory (CUDA IPC / NVLink): the sweep kernel stores its boundary "
+                                  "planes into the neighbours' ghost planes; device-side flags")
         else:
             config["halo_bytes_per_exchange_per_gpu"] = exch.bytes_per_exchange
             config["exchange"] = ("NCCL P2P, serial" if args.no_overlap else
@@ -379,7 +379,7 @@ def main():
             if ex2 is None:
                 s2.run(e_steps)
             elif args.exchange == "p2p":
-                run_steps_peer(s2, e_steps, depth, overlap=not args.no_overlap)
+                run_steps_peer(s2, e_steps, depth)
             else:
                 run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
             s2.download(out=host_out)

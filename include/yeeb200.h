@@ -253,6 +253,12 @@ int yb_peer_open(yb_sim* sim, int side, const void* handles, int peer_nz);
 int yb_peer_link(yb_sim* sim, int side, yb_sim* other);
 int yb_peer_push(yb_sim* sim, int overlap);
 int yb_peer_wait(yb_sim* sim);
+/* One exchange period over peer memory: wait for the neighbours, then (TB2,
+ * nsteps = 2) a two-step sweep whose boundary-plane stores also land in the
+ * neighbours' ghost planes — the exchange fused into the compute kernel —
+ * and a signal; for nsteps = 1 a split sweep with a push. Start a run with
+ * one yb_peer_push of the current state. */
+int yb_peer_step(yb_sim* sim, int64_t nsteps);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
 

@@ -41,7 +41,7 @@ ABI_SYMBOLS = (
     "yb_host_medium", "yb_host_field", "yb_halo_bytes", "yb_halo_pack", "yb_halo_unpack",
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
     "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
-    "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait",
+    "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait", "yb_peer_step",
 )
 
 
@@ -136,6 +136,7 @@ def lib():
         L.yb_peer_link.argtypes = [vp, C.c_int, vp]
         L.yb_peer_push.argtypes = [vp, C.c_int]
         L.yb_peer_wait.argtypes = [vp]
+        L.yb_peer_step.argtypes = [vp, C.c_int64]
         L.yb_total_energy.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
@@ -304,6 +305,11 @@ class Simulation:
 
     def peer_wait(self):
         _check(lib().yb_peer_wait(self._h))
+
+    def peer_step(self, nsteps):
+        """One exchange period over peer memory (the two-step sweep stores its
+        boundary planes straight into the neighbours' ghost planes)."""
+        _check(lib().yb_peer_step(self._h, nsteps))
 
     def run_timed(self, nsteps):
         ms = C.c_float()

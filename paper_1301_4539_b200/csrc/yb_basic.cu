@@ -9,6 +9,8 @@
 //   Source  inject_current source.hpp:61-68
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "../../include/yeeb200_inputs.h"
 #include "yb_device.cuh"
 #include "yb_launch.h"
@@ -244,6 +246,19 @@ __global__ void k_peer_wait(const unsigned* flags, unsigned need0, unsigned need
   }
 }
 
+// Halo planes <-> exchange buffer, one launch for all planes (blockIdx.y = plane).
+__global__ void k_halo_copy(Geo g, HaloList l, float* ext, bool pack) {
+  const long long per = g.plane / 4;  // float4 per plane (PX is a multiple of 32)
+  float4* e = reinterpret_cast<float4*>(ext + (long long)blockIdx.y * g.plane);
+  float4* d = reinterpret_cast<float4*>(l.plane[blockIdx.y]);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < per; t += (long long)gridDim.x * blockDim.x) {
+    if (pack)
+      e[t] = d[t];
+    else
+      d[t] = e[t];
+  }
+}
+
 __global__ void k_fill_value(float* p, long long n, float v) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     p[t] = v;
@@ -389,6 +404,14 @@ cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned 
 
 cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err, cudaStream_t st) {
   k_peer_wait<<<1, 1, 0, st>>>(flags, need0, need1, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_copy(const Geo& g, const HaloList& l, float* ext, bool pack, cudaStream_t st) {
+  if (l.n == 0) return cudaSuccess;
+  const long long per = g.plane / 4;
+  const int bx = (int)std::min<long long>((per + 255) / 256, 148);
+  k_halo_copy<<<dim3(bx, l.n), 256, 0, st>>>(g, l, ext, pack);
   return cudaGetLastError();
 }
 

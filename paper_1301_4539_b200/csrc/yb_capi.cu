@@ -143,12 +143,20 @@ struct yb_sim {
   double* energy_dev = nullptr;  // weights | partials | result
   int store_policy = 1;  // evict_first (YB_STPOL overrides; tuning knob)
   int pending = 0;            // steps of a split sweep in flight (yb_advance_begin)
+  // split sweeps: the interior launch runs on a side stream with its own
+  // work counter, concurrently with the boundary launch and the exchange
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_pre = nullptr, ev_int = nullptr;
+  unsigned long long* sched2 = nullptr;
+  unsigned long long sched2_base = 0;
+  bool on_side = false;
   PeerSide peer[2];           // direct halo push targets (0: below, 1: above)
   unsigned* pflags = nullptr; // my flag words [0] from below, [1] from above, [2] error
   unsigned push_count = 0;
   cudaStream_t peer_stream = nullptr;
   cudaEvent_t peer_go = nullptr, peer_done = nullptr;
   bool peer_inflight = false;
+  bool peer_stores = false;   // the next two-step launch also writes the neighbours' ghost planes
   bool pending_full = false;  // ... whose boundary launch already covered every plane
   bool persist = true;        // multi-sweep two-step launches (YB_TB2_PERSIST=0: off)
   bool qskip = false;         // yb_set_quiescent_skip
@@ -460,8 +468,11 @@ int step_fused(yb_sim* s, ZPart z, int zchunk, bool flip) {
   a.ntx = s->ntx;
   a.nty = s->nty;
   const dim3 grid = set_chunks(s, a, zchunk, z);
-  a.sched = s->sched;
-  a.sched_base = s->sched_base;
+  cudaStream_t st = s->on_side ? s->side : s->stream;
+  unsigned long long* sc = s->on_side ? s->sched2 : s->sched;
+  unsigned long long& base = s->on_side ? s->sched2_base : s->sched_base;
+  a.sched = sc;
+  a.sched_base = base;
   a.store_policy = s->store_policy;
   a.co = coef_args(s);
   for (int c = 0; c < 6; ++c) {
@@ -482,11 +493,11 @@ int step_fused(yb_sim* s, ZPart z, int zchunk, bool flip) {
       s->timers.push_back(p);
     }
     tp = &s->timers[s->timers_used++];
-    YB_CU(cudaEventRecord(tp->a, s->stream));
+    YB_CU(cudaEventRecord(tp->a, st));
   }
-  YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, grid, smem, s->stream));
-  s->sched_base += (unsigned long long)a.nitems + grid.x;  // every CTA's last fetch fails
-  if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
+  YB_CU(yb::launch_fused(a, s->tm[s->cur], mask, grid, smem, st));
+  base += (unsigned long long)a.nitems + grid.x;  // every CTA's last fetch fails
+  if (tp) YB_CU(cudaEventRecord(tp->b, st));
   s->launches += 1;
   if (flip) s->cur = nxt;
   if (s->timers_used >= 4096) return collect_timers(s);
@@ -502,8 +513,18 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
   a.ntx = s->ntx;
   a.nty = s->nty;
   const dim3 grid = set_chunks(s, a, zchunk, z);
+  cudaStream_t st = s->on_side ? s->side : s->stream;
+  unsigned long long* sc = s->on_side ? s->sched2 : s->sched;
+  unsigned long long& base = s->on_side ? s->sched2_base : s->sched_base;
   a.nsweeps = nsweeps;
   a.err = reinterpret_cast<int*>(s->sched) + 6;
+  if (s->peer_stores) {  // MODE 3: boundary planes straight into the neighbours' (same-parity) buffers
+    for (int c = 0; c < 6; ++c) {
+      a.pdn[c] = s->peer[0].on ? s->peer[0].buf[nxt][c] : nullptr;
+      a.pup[c] = s->peer[1].on ? s->peer[1].buf[nxt][c] : nullptr;
+    }
+    a.pdn_k0 = s->peer[0].nz;
+  }
   if (nsweeps > 1) {  // several sweeps in one launch, items ordered by dependency
     if (s->done_n != a.nitems) {
       cudaFree(s->done);
@@ -527,8 +548,8 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
     a.epoch = s->epoch;
     a.srcs = s->srcs_dev;
   }
-  a.sched = s->sched;
-  a.sched_base = s->sched_base;
+  a.sched = sc;
+  a.sched_base = base;
   a.store_policy = 1;
   a.co = coef_args(s);
   for (int c = 0; c < 6; ++c) {
@@ -549,12 +570,12 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
       s->timers.push_back(p);
     }
     tp = &s->timers[s->timers_used++];
-    YB_CU(cudaEventRecord(tp->a, s->stream));
+    YB_CU(cudaEventRecord(tp->a, st));
   }
-  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], s->tm2[nxt], mask, grid, smem, s->stream));
-  s->sched_base += (unsigned long long)a.nitems * nsweeps + grid.x;
+  YB_CU(yb::launch_tb2(a, s->tm2[s->cur], s->tm2[nxt], mask, grid, smem, st));
+  base += (unsigned long long)a.nitems * nsweeps + grid.x;
   if (nsweeps > 1) s->epoch += (unsigned)nsweeps;
-  if (tp) YB_CU(cudaEventRecord(tp->b, s->stream));
+  if (tp) YB_CU(cudaEventRecord(tp->b, st));
   s->launches += 1;
   if (flip && (nsweeps & 1)) s->cur = nxt;
   if (s->timers_used >= 4096) return collect_timers(s);
@@ -799,6 +820,10 @@ int yb_destroy(yb_sim* s) {
     if (s->cell[q]) cudaFree(s->cell[q] - yb::kGhost * s->g.plane);
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
+  cudaFree(s->sched2);
+  if (s->side) cudaStreamDestroy(s->side);
+  if (s->ev_pre) cudaEventDestroy(s->ev_pre);
+  if (s->ev_int) cudaEventDestroy(s->ev_int);
   cudaFree(s->probe_dev);
   cudaFree(s->qbits);
   cudaFree(s->qskipped);
@@ -1268,6 +1293,15 @@ int yb_advance_begin(yb_sim* s, int64_t nsteps) {
   s->pending_full = nz <= 2 * b + 1;  // no interior worth a launch: one whole sweep
   const ZPart z = s->pending_full ? zfull(s) : ZPart{0, b, nz - b, nz};
   const int zc = s->pending_full ? (nsteps == 2 ? s->zchunk2 : s->zchunk) : b;
+  if (!s->side) {
+    YB_CU(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    YB_CU(cudaEventCreateWithFlags(&s->ev_pre, cudaEventDisableTiming));
+    YB_CU(cudaEventCreateWithFlags(&s->ev_int, cudaEventDisableTiming));
+    YB_CU(cudaMalloc(&s->sched2, sizeof(unsigned long long)));
+    YB_CU(cudaMemsetAsync(s->sched2, 0, sizeof(unsigned long long), s->stream));
+    s->sched2_base = 0;
+  }
+  YB_CU(cudaEventRecord(s->ev_pre, s->stream));  // the state the interior launch will read is complete
   if (int rc = nsteps == 2 ? step_tb2(s, z, zc, false) : step_fused(s, z, zc, false)) return rc;
   s->pending = (int)nsteps;
   return YB_OK;
@@ -1279,8 +1313,17 @@ int yb_advance_end(yb_sim* s) {
   YB_CU(cudaSetDevice(s->device));
   const int n = s->pending, nz = s->g.nz;
   if (!s->pending_full) {
+    // the interior on the side stream, concurrent with the boundary launch and
+    // whatever the caller enqueued since (pack, transfers); the handle's
+    // stream then waits for it
     const ZPart z{n, nz - n, nz - n, nz - n};
-    if (int rc = n == 2 ? step_tb2(s, z, s->zchunk2, false) : step_fused(s, z, s->zchunk, false)) return rc;
+    YB_CU(cudaStreamWaitEvent(s->side, s->ev_pre, 0));
+    s->on_side = true;
+    const int rc = n == 2 ? step_tb2(s, z, s->zchunk2, false) : step_fused(s, z, s->zchunk, false);
+    s->on_side = false;
+    if (rc) return rc;
+    YB_CU(cudaEventRecord(s->ev_int, s->side));
+    YB_CU(cudaStreamWaitEvent(s->stream, s->ev_int, 0));
   }
   s->cur ^= 1;
   s->step_index += n;
@@ -1481,12 +1524,23 @@ static int halo_copy(yb_sim* s, int side, char* ext, bool pack) {
       for (int c = 0; c < 6; ++c) comp[n] = c, plane[n++] = base + q;
   }
   const int b = s->pending && pack ? s->cur ^ 1 : s->cur;  // a split sweep's new boundary planes
-  for (int q = 0; q < n; ++q) {
-    float* dev = s->buf[b][comp[q]] + (long long)plane[q] * s->g.plane;
-    if (pack)
-      YB_CU(cudaMemcpyAsync(ext + q * pb, dev, pb, cudaMemcpyDefault, s->stream));
-    else
-      YB_CU(cudaMemcpyAsync(dev, ext + q * pb, pb, cudaMemcpyDefault, s->stream));
+  cudaPointerAttributes at{};
+  const bool dev_ext = cudaPointerGetAttributes(&at, ext) == cudaSuccess && at.type == cudaMemoryTypeDevice &&
+                       at.device == s->device;
+  cudaGetLastError();  // clear a "not a device pointer" status
+  if (dev_ext) {  // one copy kernel for every plane
+    yb::HaloList l{};
+    for (int q = 0; q < n; ++q) l.plane[q] = s->buf[b][comp[q]] + (long long)plane[q] * s->g.plane;
+    l.n = n;
+    YB_CU(yb::launch_halo_copy(s->g, l, reinterpret_cast<float*>(ext), pack, s->stream));
+  } else {
+    for (int q = 0; q < n; ++q) {
+      float* dev = s->buf[b][comp[q]] + (long long)plane[q] * s->g.plane;
+      if (pack)
+        YB_CU(cudaMemcpyAsync(ext + q * pb, dev, pb, cudaMemcpyDefault, s->stream));
+      else
+        YB_CU(cudaMemcpyAsync(dev, ext + q * pb, pb, cudaMemcpyDefault, s->stream));
+    }
   }
   if (s->stream == s->own_stream) YB_CU(cudaStreamSynchronize(s->stream));  // else stream-ordered
   return YB_OK;
@@ -1607,6 +1661,32 @@ int yb_peer_push(yb_sim* s, int overlap) {
     s->peer_inflight = true;
   }
   return YB_OK;
+}
+
+int yb_peer_step(yb_sim* s, int64_t nsteps) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (!s->peer[0].on && !s->peer[1].on) return fail(YB_INVALID_ARGUMENT, "no peer linked");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight");
+  if (nsteps < 1 || nsteps > halo_depth(s)) return fail(YB_INVALID_ARGUMENT, "peer step: 1 .. halo depth steps");
+  YB_CU(cudaSetDevice(s->device));
+  if (int rc = yb_peer_wait(s)) return rc;
+  if (nsteps == 2 && s->variant == YB_VARIANT_TB2) {  // the sweep itself stores the halo (MODE 3)
+    if (int rc = prepare_fused(s)) return rc;
+    s->q_valid = false;  // this launch does not maintain the quiescent map
+    s->peer_stores = true;
+    const int rc = step_tb2(s, zfull(s), s->zchunk2, true);
+    s->peer_stores = false;
+    if (rc) return rc;
+    s->step_index += 2;
+    s->steps += 2;
+    ++s->push_count;
+    YB_CU(yb::launch_peer_signal(s->peer[0].on ? s->peer[0].flags + 1 : nullptr,
+                                 s->peer[1].on ? s->peer[1].flags + 0 : nullptr, s->push_count, s->stream));
+    return YB_OK;
+  }
+  if (int rc = yb_advance_begin(s, nsteps)) return rc;  // one step: split sweep + push
+  if (int rc = yb_peer_push(s, 0)) return rc;
+  return yb_advance_end(s);
 }
 
 int yb_peer_wait(yb_sim* s) {

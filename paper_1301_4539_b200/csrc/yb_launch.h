@@ -91,6 +91,13 @@ struct FusedArgs {
   unsigned epoch;
   const SrcArgs* srcs;           // per-sweep sources (nsweeps > 1)
   int* err;                      // set when a dependency wait timed out
+  // Peer-store mode (two-step kernel MODE 3, z-slabs over peer memory): the
+  // boundary planes 0,1 / nz-2,nz-1 this launch writes also go straight into
+  // the neighbours' ghost planes pdn_k0 + {0,1} / {-2,-1} of the same-parity
+  // buffers (NVLink stores, overlapped with the rest of the sweep).
+  float* pdn[6];                 // slab below (nullptr: none)
+  float* pup[6];                 // slab above
+  int pdn_k0;                    // the lower slab's depth (its ghost plane for my plane 0)
 };
 
 // planes [kz0, kz1) of z-chunk c of a launch
@@ -169,6 +176,13 @@ cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned 
 // Spins (bounded, ~seconds) until flags[0] >= need0 and flags[1] >= need1;
 // on timeout sets *err = 1.
 cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err, cudaStream_t st);
+// Halo planes <-> a contiguous exchange buffer: plane q of the list is
+// src[q] (or dst[q]) = one padded plane (PX*PY floats); ext holds them in order.
+struct HaloList {
+  float* plane[12];
+  int n;
+};
+cudaError_t launch_halo_copy(const Geo& g, const HaloList& l, float* ext, bool pack, cudaStream_t st);
 cudaError_t launch_fill_value(float* p, long long n, float v, cudaStream_t st);
 cudaError_t launch_probes(const Fields& F, const ProbeArgs& pa, float* out, cudaStream_t st);
 // weights: x node[nx+1], x cell[nx], y node[ny+1], y cell[ny], z node[nz+1], z cell[nz]

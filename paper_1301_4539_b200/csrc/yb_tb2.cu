@@ -262,8 +262,8 @@ struct Cursor {
 // shared memory (column c-1 / c+4; the edge columns for lanes 0 / 31).
 template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 struct Rows {
-  // MODE: 0 plain, 1 quiescent skip, 2 several sweeps per launch
-  static constexpr bool QS = MODE == 1, MS = MODE == 2;
+  // MODE: 0 plain, 1 quiescent skip, 2 several sweeps per launch, 3 peer stores
+  static constexpr bool QS = MODE == 1, MS = MODE == 2, PS = MODE == 3;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   static constexpr int E1C = RW * BX, E1B = 3 * E1C;              // comp / buffer strides
   static constexpr int H1C = (RW - 1) * BX, H1B = 3 * H1C;
@@ -307,6 +307,25 @@ struct Rows {
   }
 
   __device__ __forceinline__ float* outp(int q) const { return MS ? outm[q] : a.out[q]; }
+
+  // peer-store mode: an owned row of boundary plane k also goes to the neighbour's ghost plane
+  __device__ __forceinline__ void peer_rows(int c0, int k, const F4x3& v) {
+    const Geo& g = a.g;
+    float* const* dst = nullptr;
+    int kp = 0;
+    if (k < 2 && a.pdn[0]) {
+      dst = a.pdn;
+      kp = a.pdn_k0 + k;
+    } else if (k >= g.nz - 2 && a.pup[0]) {
+      dst = a.pup;
+      kp = k - g.nz;
+    }
+    if (!dst) return;
+    const long long gp = gidx(g, i0, j, kp);
+    store_row4(dst[c0], gp, i0, g.nx, v.x, st_pol);
+    store_row4(dst[c0 + 1], gp, i0, g.nx, v.y, st_pol);
+    store_row4(dst[c0 + 2], gp, i0, g.nx, v.z, st_pol);
+  }
   __device__ __forceinline__ const SrcArgs& src() const { return MS ? srcm : a.src; }
 
   __device__ __forceinline__ void prologue() {
@@ -427,6 +446,7 @@ struct Rows {
         store_row4(outp(0), gp, i0, g.nx, e2c.x, st_pol);
         store_row4(outp(1), gp, i0, g.nx, e2c.y, st_pol);
         store_row4(outp(2), gp, i0, g.nx, e2c.z, st_pol);
+        if (PS) peer_rows(0, kh, e2c);
       }
       if (QS) {
         const bool nz = own && (nonzero4(e2c.x) | nonzero4(e2c.y) | nonzero4(e2c.z));
@@ -463,6 +483,7 @@ struct Rows {
         store_row4(outp(3), gp, i0, g.nx, h2.x, st_pol);
         store_row4(outp(4), gp, i0, g.nx, h2.y, st_pol);
         store_row4(outp(5), gp, i0, g.nx, h2.z, st_pol);
+        if (PS) peer_rows(3, k4, h2);
       }
       if (QS && j < g.ny) {
         const bool nz = nonzero4(h2.x) | nonzero4(h2.y) | nonzero4(h2.z);
@@ -764,6 +785,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       tb2_edge<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, src, l);
     else
       tb2_rows<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, out, src, w, l, st_pol);
+    if (MODE == 3) __threadfence_system();  // peer stores of this item before the launch's signal
     if (MS) {  // publish: this item's part of sweep sw is in global memory
       consumer_sync();
       if (threadIdx.x == 0) {
@@ -795,10 +817,10 @@ using LimitFn = cudaError_t (*)();
 #define YB_T(m) launch_t<YB_B(m)>
 #define YB_L(m) set_limit_t<YB_B(m)>
 #define YB_8(F, b) F(b), F(b + 1), F(b + 2), F(b + 3), F(b + 4), F(b + 5), F(b + 6), F(b + 7)
-const LaunchFn kLaunch[48] = {YB_8(YB_T, 0),  YB_8(YB_T, 8),  YB_8(YB_T, 16),
-                              YB_8(YB_T, 24), YB_8(YB_T, 32), YB_8(YB_T, 40)};
-const LimitFn kLimit[48] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16),
-                            YB_8(YB_L, 24), YB_8(YB_L, 32), YB_8(YB_L, 40)};
+const LaunchFn kLaunch[64] = {YB_8(YB_T, 0),  YB_8(YB_T, 8),  YB_8(YB_T, 16), YB_8(YB_T, 24),
+                              YB_8(YB_T, 32), YB_8(YB_T, 40), YB_8(YB_T, 48), YB_8(YB_T, 56)};
+const LimitFn kLimit[64] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16), YB_8(YB_L, 24),
+                            YB_8(YB_L, 32), YB_8(YB_L, 40), YB_8(YB_L, 48), YB_8(YB_L, 56)};
 #undef YB_8
 #undef YB_T
 #undef YB_L
@@ -807,7 +829,7 @@ const LimitFn kLimit[48] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16),
 }  // namespace
 
 cudaError_t tb2_set_smem_limits() {
-  for (int m = 0; m < 48; ++m) {
+  for (int m = 0; m < 64; ++m) {
     const cudaError_t e = kLimit[m]();
     if (e != cudaSuccess) return e;
   }
@@ -816,7 +838,7 @@ cudaError_t tb2_set_smem_limits() {
 
 cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, const TMaps& tm_out, int cell_mask, dim3 grid,
                        size_t smem, cudaStream_t st) {
-  const int mode = a.nsweeps > 1 ? 2 : (a.qm.bits ? 1 : 0);
+  const int mode = (a.pdn[0] || a.pup[0]) ? 3 : (a.nsweeps > 1 ? 2 : (a.qm.bits ? 1 : 0));
   return kLaunch[(cell_mask & 15) | (mode << 4)](a, tm, tm_out, grid, smem, st);
 }
 

@@ -128,18 +128,17 @@ class PeerExchange:
         dist.barrier(group=group)
 
 
-def run_steps_peer(sim, nsteps: int, depth: int, overlap: bool = True):
+def run_steps_peer(sim, nsteps: int, depth: int):
     """run_steps for PeerExchange / peer_link'ed slabs: push the current
-    boundary planes, then per exchange: wait for the neighbours, boundary
-    sweep, push the new planes (side stream if overlap), interior sweep."""
+    boundary planes once, then per exchange period yb_peer_step — a device-side
+    wait for the neighbours, then a two-step sweep whose boundary-plane stores
+    also land in the neighbours' ghost planes (compute and exchange in one
+    kernel), then a signal."""
     sim.peer_push(False)
     done = 0
     while done < nsteps:
         n = min(depth, nsteps - done)
-        sim.peer_wait()
-        sim.advance_begin(n)
-        sim.peer_push(overlap)
-        sim.advance_end()
+        sim.peer_step(n)
         done += n
 
 
