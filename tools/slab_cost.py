@@ -74,3 +74,44 @@ def split_x(k):
 
 print("middle slab, split + pack + unpack", round(timed(sl, split_x), 1))
 sl.close()
+
+# three linked slabs in one process: plain sweeps (no exchange) vs yb_peer_step
+# (boundary planes stored straight into the neighbours' ghost planes)
+sims = []
+for i in range(3):
+    s = Y.Simulation(n, n, n, variant=Y.VARIANT_TB2, z_offset=i * n, nz_global=3 * n)
+    s.generate_medium(1, -1)
+    sims.append(s)
+
+
+def plain3(k):
+    for s in sims:
+        s.run(k, sync=False)
+
+
+def peer3(k):
+    for _ in range(k // 2):
+        for s in sims:
+            s.peer_step(2)
+
+
+def timed3(fn):
+    fn(4)
+    for s in sims:
+        s.synchronize()
+    t0 = time.perf_counter()
+    fn(steps)
+    for s in sims:
+        s.synchronize()
+    return 3 * n ** 3 * steps / (time.perf_counter() - t0) / 1e9
+
+
+print("3 slabs, plain sweeps", round(timed3(plain3), 1))
+for lo, hi in zip(sims[:-1], sims[1:]):
+    lo.peer_link(1, hi)
+    hi.peer_link(0, lo)
+for s in sims:
+    s.peer_push(False)
+print("3 slabs, peer_step (fused peer stores)", round(timed3(peer3), 1))
+for s in sims:
+    s.close()
