@@ -215,9 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (jlt) {
         const long long p = gidx(g, i0, j, kh);
-        store_row4(a.out[3], p, i0, g.nx, hx, st_pol);
-        store_row4(a.out[4], p, i0, g.nx, hy, st_pol);
-        store_row4(a.out[5], p, i0, g.nx, hz, st_pol);
+        store_rows3(a.out + 3, p, i0, g.nx, hx, hy, hz, st_pol);
       }
       if (QS && __any_sync(~0u, jlt && (nonzero4(hx) | nonzero4(hy) | nonzero4(hz))) && l == 0)
         qmap_mark(a.qm, tile, kh);
@@ -334,9 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (jlt && k < kz1) {
         const long long p = gidx(g, i0, j, k);
-        store_row4(a.out[0], p, i0, g.nx, exw, st_pol);
-        store_row4(a.out[1], p, i0, g.nx, eyw, st_pol);
-        store_row4(a.out[2], p, i0, g.nx, ezw, st_pol);
+        store_rows3(a.out, p, i0, g.nx, exw, eyw, ezw, st_pol);
       }
       if (QS && k < kz1 &&
           __any_sync(~0u, jlt && (nonzero4(exw) | nonzero4(eyw) | nonzero4(ezw))) && l == 0)

@@ -69,10 +69,24 @@ __device__ __forceinline__ float4 shift_ip(float4 v, int lane, float right) {
 // 128-bit store with an L2 cache-policy hint (evict_first: the next-state
 // arrays are not read again in this launch, so they should not push the
 // halo rows neighbouring CTAs are about to read out of L2).
+#ifndef YB_STG_MODE
+#define YB_STG_MODE 0
+#endif
 __device__ __forceinline__ void stg4_hint(float* ptr, float4 v, uint64_t pol) {
+#if YB_STG_MODE == 0
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x),
                "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
+#elif YB_STG_MODE == 1
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol));
+#elif YB_STG_MODE == 2
+  (void)pol;
+  __stcs(reinterpret_cast<float4*>(ptr), v);
+#else
+  (void)pol;
+  *reinterpret_cast<float4*>(ptr) = v;
+#endif
 }
 
 __device__ __forceinline__ void store_row4(float* base, long long p, int i0, int nx, float4 v,
@@ -83,6 +97,25 @@ __device__ __forceinline__ void store_row4(float* base, long long p, int i0, int
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (i0 + q < nx) base[p + q] = elc(v, q);
+  }
+}
+
+// the three components of one row behind a single ragged-edge branch
+__device__ __forceinline__ void store_rows3(float* const* base, long long p, int i0, int nx, float4 v0,
+                                            float4 v1, float4 v2, uint64_t pol) {
+  float *b0 = base[0], *b1 = base[1], *b2 = base[2];
+  if (i0 + 3 < nx) {
+    stg4_hint(b0 + p, v0, pol);
+    stg4_hint(b1 + p, v1, pol);
+    stg4_hint(b2 + p, v2, pol);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q < nx) {
+        b0[p + q] = elc(v0, q);
+        b1[p + q] = elc(v1, q);
+        b2[p + q] = elc(v2, q);
+      }
   }
 }
 

@@ -306,7 +306,7 @@ struct Rows {
     ze1 = zh1 = 0.f;
   }
 
-  __device__ __forceinline__ float* outp(int q) const { return MS ? outm[q] : a.out[q]; }
+  __device__ __forceinline__ float* const* outs() const { return MS ? outm : a.out; }
 
   // peer-store mode: an owned row of boundary plane k also goes to the neighbour's ghost plane
   __device__ __forceinline__ void peer_rows(int c0, int k, const F4x3& v) {
@@ -322,9 +322,7 @@ struct Rows {
     }
     if (!dst) return;
     const long long gp = gidx(g, i0, j, kp);
-    store_row4(dst[c0], gp, i0, g.nx, v.x, st_pol);
-    store_row4(dst[c0 + 1], gp, i0, g.nx, v.y, st_pol);
-    store_row4(dst[c0 + 2], gp, i0, g.nx, v.z, st_pol);
+    store_rows3(dst + c0, gp, i0, g.nx, v.x, v.y, v.z, st_pol);
   }
   __device__ __forceinline__ const SrcArgs& src() const { return MS ? srcm : a.src; }
 
@@ -443,9 +441,7 @@ struct Rows {
       const bool own = er <= kTB2Rows && j < g.ny && kh < it.kz1;
       if (own) {  // E^{n+2} of the owned rows -> HBM
         const long long gp = gidx(g, i0, j, kh);
-        store_row4(outp(0), gp, i0, g.nx, e2c.x, st_pol);
-        store_row4(outp(1), gp, i0, g.nx, e2c.y, st_pol);
-        store_row4(outp(2), gp, i0, g.nx, e2c.z, st_pol);
+        store_rows3(outs(), gp, i0, g.nx, e2c.x, e2c.y, e2c.z, st_pol);
         if (PS) peer_rows(0, kh, e2c);
       }
       if (QS) {
@@ -480,9 +476,7 @@ struct Rows {
       }
       if (j < g.ny) {
         const long long gp = gidx(g, i0, j, k4);
-        store_row4(outp(3), gp, i0, g.nx, h2.x, st_pol);
-        store_row4(outp(4), gp, i0, g.nx, h2.y, st_pol);
-        store_row4(outp(5), gp, i0, g.nx, h2.z, st_pol);
+        store_rows3(outs() + 3, gp, i0, g.nx, h2.x, h2.y, h2.z, st_pol);
         if (PS) peer_rows(3, k4, h2);
       }
       if (QS && j < g.ny) {
