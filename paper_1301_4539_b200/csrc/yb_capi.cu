@@ -157,6 +157,8 @@ struct yb_sim {
   cudaEvent_t peer_go = nullptr, peer_done = nullptr;
   bool peer_inflight = false;
   bool peer_stores = false;   // the next two-step launch also writes the neighbours' ghost planes
+  bool peer_folded = false;   // ... and did its own wait / signal (set by step_tb2)
+  unsigned pcnt_base[2] = {0u, 0u};
   bool pending_full = false;  // ... whose boundary launch already covered every plane
   bool persist = true;        // multi-sweep two-step launches (YB_TB2_PERSIST=0: off)
   bool qskip = false;         // yb_set_quiescent_skip
@@ -524,6 +526,44 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
       a.pup[c] = s->peer[1].on ? s->peer[1].buf[nxt][c] : nullptr;
     }
     a.pdn_k0 = s->peer[0].nz;
+    // Fold the wait / signal into the launch when only the bottom / top z-chunk
+    // touches the ghost planes (both at least two planes deep); else separate
+    // wait and signal launches around it.
+    const int T = a.ntx * a.nty, nch = a.nitems / T;
+    auto planes = [&](int c, int& k0, int& k1) {
+      if (c < a.nch0) {
+        k0 = a.zb0 + c * a.zchunk;
+        k1 = std::min(k0 + a.zchunk, a.ze0);
+      } else {
+        k0 = a.zb1 + (c - a.nch0) * a.zchunk;
+        k1 = std::min(k0 + a.zchunk, a.ze1);
+      }
+    };
+    int f0, f1, l0, l1;
+    planes(0, f0, f1);
+    planes(nch - 1, l0, l1);
+    s->peer_folded = !s->on_side && f0 == 0 && f1 - f0 >= 2 && l1 == s->g.nz && l1 - l0 >= 2 &&
+                     std::getenv("YB_PEER_NOFOLD") == nullptr;
+    if (s->peer_folded) {
+      if (s->peer_inflight) {  // my own push must have read my planes before they are rewritten
+        YB_CU(cudaStreamWaitEvent(st, s->peer_done, 0));
+        s->peer_inflight = false;
+      }
+      a.pfold = 1;
+      a.pflag = s->pflags;
+      a.pneed = s->push_count;
+      a.psig_val = s->push_count + 1;
+      a.psig[0] = s->peer[0].on ? s->peer[0].flags + 1 : nullptr;
+      a.psig[1] = s->peer[1].on ? s->peer[1].flags + 0 : nullptr;
+      a.pcnt = s->pflags + 4;
+      a.pcnt_base[0] = s->pcnt_base[0];
+      a.pcnt_base[1] = s->pcnt_base[1];
+      a.perr = reinterpret_cast<int*>(s->pflags + 2);
+      if (s->peer[0].on) s->pcnt_base[0] += (unsigned)T;
+      if (s->peer[1].on) s->pcnt_base[1] += (unsigned)T;
+    } else {
+      if (int rc = yb_peer_wait(s)) return rc;
+    }
   }
   if (nsweeps > 1) {  // several sweeps in one launch, items ordered by dependency
     if (s->done_n != a.nitems) {
@@ -1567,8 +1607,8 @@ int yb_halo_unpack(yb_sim* s, int side, const void* src) {
 static int ensure_pflags(yb_sim* s) {
   if (s->pflags) return YB_OK;
   YB_CU(cudaSetDevice(s->device));
-  YB_CU(cudaMalloc(&s->pflags, 4 * sizeof(unsigned)));
-  YB_CU(cudaMemset(s->pflags, 0, 4 * sizeof(unsigned)));
+  YB_CU(cudaMalloc(&s->pflags, 8 * sizeof(unsigned)));  // + [4], [5]: boundary-item counters
+  YB_CU(cudaMemset(s->pflags, 0, 8 * sizeof(unsigned)));
   return YB_OK;
 }
 
@@ -1669,7 +1709,6 @@ int yb_peer_step(yb_sim* s, int64_t nsteps) {
   if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight");
   if (nsteps < 1 || nsteps > halo_depth(s)) return fail(YB_INVALID_ARGUMENT, "peer step: 1 .. halo depth steps");
   YB_CU(cudaSetDevice(s->device));
-  if (int rc = yb_peer_wait(s)) return rc;
   if (nsteps == 2 && s->variant == YB_VARIANT_TB2) {  // the sweep itself stores the halo (MODE 3)
     if (int rc = prepare_fused(s)) return rc;
     s->q_valid = false;  // this launch does not maintain the quiescent map
@@ -1680,10 +1719,13 @@ int yb_peer_step(yb_sim* s, int64_t nsteps) {
     s->step_index += 2;
     s->steps += 2;
     ++s->push_count;
-    YB_CU(yb::launch_peer_signal(s->peer[0].on ? s->peer[0].flags + 1 : nullptr,
-                                 s->peer[1].on ? s->peer[1].flags + 0 : nullptr, s->push_count, s->stream));
+    if (!s->peer_folded)
+      YB_CU(yb::launch_peer_signal(s->peer[0].on ? s->peer[0].flags + 1 : nullptr,
+                                   s->peer[1].on ? s->peer[1].flags + 0 : nullptr, s->push_count, s->stream));
+    s->peer_folded = false;
     return YB_OK;
   }
+  if (int rc = yb_peer_wait(s)) return rc;
   if (int rc = yb_advance_begin(s, nsteps)) return rc;  // one step: split sweep + push
   if (int rc = yb_peer_push(s, 0)) return rc;
   return yb_advance_end(s);

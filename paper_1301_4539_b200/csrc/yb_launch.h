@@ -98,6 +98,19 @@ struct FusedArgs {
   float* pdn[6];                 // slab below (nullptr: none)
   float* pup[6];                 // slab above
   int pdn_k0;                    // the lower slab's depth (its ghost plane for my plane 0)
+  // ... with the exchange's ordering folded in (pfold): the bottom / top z-chunk's
+  // items run first, each waits (bounded) for my flag word pflag[0] / pflag[1] >=
+  // pneed before loading the ghost planes that neighbour writes (and before writing
+  // its), and the last of them to finish publishes psig_val to that neighbour's flag
+  // word psig[0] / psig[1] — no wait or signal launches, and a neighbour can start
+  // its next period's boundary items while this launch is still in its interior.
+  int pfold;
+  const unsigned* pflag;
+  unsigned pneed, psig_val;
+  unsigned* psig[2];
+  unsigned* pcnt;                // per side: boundary items completed (monotonic)
+  unsigned pcnt_base[2];         // their values at this launch's start
+  int* perr;                     // set when a wait timed out
 };
 
 // planes [kz0, kz1) of z-chunk c of a launch

@@ -201,6 +201,20 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
+// MODE 3 (folded exchange): spin, bounded, until a neighbour's flag word reaches need.
+__device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, int* err) {
+  for (long long n = 0;; ++n) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if ((int)(v - need) >= 0) return;
+    if (n > (1ll << 24)) {  // ~2 s: the neighbour never signalled
+      atomicExch(err, 1);
+      return;
+    }
+    __nanosleep(100);
+  }
+}
+
 // Stage layout: fields (12 rows from y0-2), then Ca, Cb (11 rows from y0-1),
 // then Da, Db (10 rows from y0-1), each present only in per-cell mode.
 template <bool CAC, bool CBC, bool DAC, bool DBC>
@@ -632,7 +646,7 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
 template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm,
                                        const __grid_constant__ TMaps tm_o) {
-  constexpr bool QS = MODE == 1, MS = MODE == 2;
+  constexpr bool QS = MODE == 1, MS = MODE == 2, PS = MODE == 3;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
   constexpr uint32_t kBytesF = kBX * kTB2BY * 4, kBytesC = kBX * kTB2RowsCA * 4,
@@ -697,6 +711,14 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         int it = -1, sw = 0;
         if (!MS) {
           it = v < (unsigned long long)a.nitems ? (int)v : -1;
+          if (PS && it >= 0 && a.pfold) {  // bottom chunk, top chunk, then the interior
+            const int nch = a.nitems / T, q = it / T, tile = it - q * T;
+            const int ch = q == 0 ? 0 : (q == 1 ? nch - 1 : q - 1);
+            it = ch * T + tile;
+            if (ch == 0 && a.pdn[0]) peer_flag_wait(a.pflag, a.pneed, a.perr);
+            if (ch == nch - 1 && a.pup[0]) peer_flag_wait(a.pflag + 1, a.pneed, a.perr);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
+          }
         } else if (v < (unsigned long long)a.nitems * a.nsweeps) {
           sw = (int)(v / (unsigned long long)a.nitems);
           it = (int)(v - (unsigned long long)sw * a.nitems);
@@ -779,7 +801,26 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       tb2_edge<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, src, l);
     else
       tb2_rows<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, out, src, w, l, st_pol);
-    if (MODE == 3) __threadfence_system();  // peer stores of this item before the launch's signal
+    if (PS) {  // boundary item: its peer stores before the signal
+      const int ch = item / T, nch = a.nitems / T;
+      const bool bd = ch == 0 && a.pdn[0], bu = ch == nch - 1 && a.pup[0];
+      if (bd || bu) {
+        __threadfence_system();
+        if (a.pfold) {
+          consumer_sync();
+          if (threadIdx.x == 0) {
+            if (bd && atomicAdd(a.pcnt, 1u) - a.pcnt_base[0] == (unsigned)T - 1u) {
+              __threadfence_system();
+              asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.psig[0]), "r"(a.psig_val) : "memory");
+            }
+            if (bu && atomicAdd(a.pcnt + 1, 1u) - a.pcnt_base[1] == (unsigned)T - 1u) {
+              __threadfence_system();
+              asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.psig[1]), "r"(a.psig_val) : "memory");
+            }
+          }
+        }
+      }
+    }
     if (MS) {  // publish: this item's part of sweep sw is in global memory
       consumer_sync();
       if (threadIdx.x == 0) {

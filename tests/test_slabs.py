@@ -430,12 +430,19 @@ def test_peer_errors(yb):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant,nranks,nzg,steps", [(2, 3, 29, 11), (2, 2, 12, 10), (2, 4, 23, 9), (0, 3, 29, 7)])
-def test_gpu_slabs_peer_step(yb, oracle, variant, nranks, nzg, steps):
+@pytest.mark.parametrize("fold", [True, False])
+@pytest.mark.parametrize("variant,nranks,nzg,steps", [(2, 3, 29, 11), (2, 2, 12, 10), (2, 4, 23, 9), (0, 3, 29, 7),
+                                                       (2, 3, 150, 8)])
+def test_gpu_slabs_peer_step(yb, oracle, monkeypatch, fold, variant, nranks, nzg, steps):
     """Exchange fused into the sweep (yb_peer_step): the two-step kernel stores
-    its boundary planes straight into the linked neighbours' ghost planes.
-    One process, one GPU, slabs stepped one after another (every device-side
-    wait already satisfied). Bit-exact against one domain."""
+    its boundary planes straight into the linked neighbours' ghost planes, and
+    (fold) its bottom / top z-chunk items wait for and signal the neighbours
+    themselves. One process, one GPU, all slabs on one stream, stepped one after
+    another (every device-side wait already satisfied when it runs). Bit-exact
+    against one domain."""
+    import torch
+    if not fold:
+        monkeypatch.setenv("YB_PEER_NOFOLD", "1")
     nx, ny = 136, 40
     tab = oracle.gauss_table(steps)
     srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)]
@@ -447,6 +454,9 @@ def test_gpu_slabs_peer_step(yb, oracle, variant, nranks, nzg, steps):
             s.add_source(*q)
         s.fill(8)
         sims.append(s)
+    st = torch.cuda.Stream()
+    for s in sims:
+        s.set_stream(st.cuda_stream)
     for lo, hi in zip(sims[:-1], sims[1:]):
         lo.peer_link(1, hi)
         hi.peer_link(0, lo)
