@@ -173,9 +173,11 @@ def main():
                     help="auto: tb2 (two steps per sweep; z-slabs exchange every two steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 halo transport: NCCL send/recv through torch.distributed, or a direct push "
-                         "into the neighbours' ghost planes over peer memory (CUDA IPC / NVLink)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N>1 halo transport: p2p = the two-step sweep stores its boundary planes straight "
+                         "into the neighbours' ghost planes over peer memory (CUDA IPC / NVLink); nccl = "
+                         "send/recv through torch.distributed; auto = p2p when every rank can map its "
+                         "neighbours' memory, else nccl")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange, then sweep (default: boundary planes first, exchange overlapped "
                          "with the interior sweep)")
@@ -258,8 +260,26 @@ def main():
         dist.barrier()  # the first NCCL op involves every rank (communicator init)
     exch = None
     if world > 1:
-        exch = (PeerExchange(sim, rank, world) if args.exchange == "p2p"
-                else HaloExchange(sim, rank, world, f"cuda:{local}"))
+        exch = None
+        if args.exchange in ("auto", "p2p"):
+            try:
+                exch = PeerExchange(sim, rank, world)
+                why = ""
+            except Exception as e:  # noqa: BLE001 - decided collectively below
+                why = f"{type(e).__name__}: {e}"
+            if args.exchange == "auto":  # every rank must agree on the transport
+                whys = [None] * world
+                dist.all_gather_object(whys, why)
+                bad = [w for w in whys if w]
+                if bad:
+                    exch = None
+                    if rank == 0:
+                        print(f"p2p exchange unavailable ({bad[0]}); using NCCL", file=sys.stderr)
+            elif why:
+                raise RuntimeError(why)
+        args.exchange = "p2p" if exch is not None else "nccl"
+        if exch is None:
+            exch = HaloExchange(sim, rank, world, f"cuda:{local}")
 
     depth = sim.info()["halo_depth"]  # steps per ghost-plane exchange
 

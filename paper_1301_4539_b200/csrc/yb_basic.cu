@@ -238,7 +238,7 @@ __global__ void k_peer_wait(const unsigned* flags, unsigned need0, unsigned need
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(a) : "l"(flags) : "memory");
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(b) : "l"(flags + 1) : "memory");
     if (a >= need0 && b >= need1) return;
-    if (it > (1ll << 24)) {  // ~2 s: the neighbour never signalled
+    if (it > (1ll << 27)) {  // ~15 s: the neighbour never signalled
       atomicExch(err, 1);
       return;
     }

@@ -207,7 +207,7 @@ __device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, in
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
     if ((int)(v - need) >= 0) return;
-    if (n > (1ll << 24)) {  // ~2 s: the neighbour never signalled
+    if (n > (1ll << 27)) {  // ~15 s: the neighbour never signalled
       atomicExch(err, 1);
       return;
     }

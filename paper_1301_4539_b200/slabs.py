@@ -130,10 +130,10 @@ class PeerExchange:
 
 def run_steps_peer(sim, nsteps: int, depth: int):
     """run_steps for PeerExchange / peer_link'ed slabs: push the current
-    boundary planes once, then per exchange period yb_peer_step — a device-side
-    wait for the neighbours, then a two-step sweep whose boundary-plane stores
-    also land in the neighbours' ghost planes (compute and exchange in one
-    kernel), then a signal."""
+    boundary planes once, then per exchange period one yb_peer_step — a
+    two-step sweep whose boundary-plane stores also land in the neighbours'
+    ghost planes, its bottom / top z-chunk items waiting for and signalling the
+    neighbours in-kernel (compute, exchange and ordering in one launch)."""
     sim.peer_push(False)
     done = 0
     while done < nsteps:

@@ -488,3 +488,94 @@ def test_gpu_slabs_peer_step(yb, oracle, monkeypatch, fold, variant, nranks, nzg
         assert bits_equal(out[c], want[c]), c
     for s in sims:
         s.close()
+
+
+def _ipc_worker(rank, world, port, result_path, variant, steps):
+    """One slab per process, all on cuda:0, linked through CUDA IPC
+    (PeerExchange). Ranks take turns — each period rank r steps while the
+    others idle, with a device sync and a gloo barrier between turns — so every
+    device-side wait is already satisfied when it runs and no kernel waits on
+    a concurrently running one."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1301_4539_b200 as Y
+    from oracle import pyoracle as O
+    from paper_1301_4539_b200.slabs import PeerExchange, partition
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    nx, ny, nzg = 136, 40, 37
+    z0, n = partition(nzg, world)[rank]
+    s = Y.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant)
+    s.generate_medium(7, 7)
+    s.add_source(2, nx // 2, ny // 2, nzg // 2, O.gauss_table(steps))
+    s.fill(8)
+    PeerExchange(s, rank, world)
+    depth = s.info()["halo_depth"]
+
+    def turns(fn):
+        for r in range(world):
+            if r == rank:
+                fn()
+                s.synchronize()
+            dist.barrier()
+
+    turns(lambda: s.peer_push(False))
+    done = 0
+    while done < steps:
+        k = min(depth, steps - done)
+        turns(lambda: s.peer_step(k))
+        done += k
+    d = s.download()
+    at_top = z0 + n == nzg
+    mine = [(z0, d[c][:n + (1 if c in (0, 1, 5) and at_top else 0)].copy()) for c in range(6)]
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    if rank == 0:
+        out = O.zeros_state(nx, ny, nzg)
+        for p in parts:
+            for c, (k0, a) in enumerate(p):
+                out[c][k0:k0 + a.shape[0]] = a
+        np.savez(result_path, *out)
+    dist.barrier()
+    s.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,world,steps", [(2, 2, 10), (2, 3, 9), (0, 2, 5)])
+def test_gpu_ipc_peer_exchange(yb, oracle, tmp_path, variant, world, steps):
+    """The cross-process path of --exchange p2p: IPC handles exchanged over
+    gloo, opened with cudaIpcOpenMemHandle, then yb_peer_step per period (the
+    two-step sweep stores its boundary planes into the other process's ghost
+    planes and signals its flag word). Bit-exact against one domain."""
+    path = str(tmp_path / "ipc.npz")
+    mp.spawn(_ipc_worker, args=(world, _free_port(), path, variant, steps), nprocs=world, join=True)
+    got = np.load(path)
+    nx, ny, nzg = 136, 40, 37
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(7, 7)
+        one.add_source(2, nx // 2, ny // 2, nzg // 2, oracle.gauss_table(steps))
+        one.fill(8)
+        one.run(steps)
+        want = one.download()
+    for c in range(6):
+        assert bits_equal(got[f"arr_{c}"], want[c]), c
+
+
+@pytest.mark.gpu
+def test_gpu_peer_wait_times_out(yb):
+    """A neighbour that never publishes: the sweep's in-kernel wait gives up
+    (bounded, ~15 s) and the error surfaces at the next synchronize instead of
+    hanging the device."""
+    a = yb.Simulation(136, 16, 40, z_offset=0, nz_global=80, variant=yb.VARIANT_TB2)
+    b = yb.Simulation(136, 16, 40, z_offset=40, nz_global=80, variant=yb.VARIANT_TB2)
+    a.peer_link(1, b)
+    b.peer_link(0, a)
+    a.peer_push(False)
+    a.peer_step(2)  # b never pushed: a's top-chunk items wait for b's flag
+    with pytest.raises(yb.YeeError):
+        a.synchronize()
+    for s in (a, b):
+        s.close()
