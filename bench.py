@@ -405,6 +405,9 @@ def main():
             s2.download(out=host_out)
             dt = time.perf_counter() - t0
             skipped = s2.info()["skipped_items"]
+            if dist:  # no neighbour may still be storing into this slab's (IPC-mapped) memory
+                torch.cuda.synchronize()
+                dist.barrier()
             s2.close()
             if dist:
                 tt = torch.tensor([dt], device="cuda")
@@ -441,6 +444,9 @@ def main():
         if e2e_skip is not None:
             line["e2e_quiescent_skip"] = e2e_skip
         print(json.dumps(line), flush=True)
+    if dist:
+        torch.cuda.synchronize()
+        dist.barrier()
     sim.close()
     if dist:
         dist.destroy_process_group()
