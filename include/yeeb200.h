@@ -245,19 +245,23 @@ int yb_advance_end(yb_sim* sim);
  * interior sweep); yb_peer_wait makes this handle's stream wait (on the
  * device) until both neighbours have pushed as often as it has. Schedule:
  * push; then per exchange: wait, yb_advance_begin(d), push, yb_advance_end.
- * A wait that never completes gives up after ~2 s and yb_synchronize reports
- * YB_RUNTIME_ERROR. */
+ * A wait that never completes gives up after ~15 s and yb_synchronize reports
+ * YB_RUNTIME_ERROR. Neighbours store into this slab's memory: synchronise
+ * all ranks before yb_destroy. */
 size_t yb_peer_handle_bytes(void);
 int yb_peer_export(yb_sim* sim, void* handles);
 int yb_peer_open(yb_sim* sim, int side, const void* handles, int peer_nz);
 int yb_peer_link(yb_sim* sim, int side, yb_sim* other);
 int yb_peer_push(yb_sim* sim, int overlap);
 int yb_peer_wait(yb_sim* sim);
-/* One exchange period over peer memory: wait for the neighbours, then (TB2,
- * nsteps = 2) a two-step sweep whose boundary-plane stores also land in the
- * neighbours' ghost planes — the exchange fused into the compute kernel —
- * and a signal; for nsteps = 1 a split sweep with a push. Start a run with
- * one yb_peer_push of the current state. */
+/* One exchange period over peer memory. TB2, nsteps = 2: ONE launch — a
+ * two-step sweep whose boundary-plane stores also land in the neighbours'
+ * ghost planes (the exchange fused into the compute kernel); its bottom / top
+ * z-chunk items run first, wait in-kernel for the neighbour's previous period
+ * and the last of them signals this one (separate wait / signal launches
+ * when the grid's first or last z-chunk is under two planes). nsteps = 1:
+ * wait, split sweep, push. Start a run with one yb_peer_push of the current
+ * state. */
 int yb_peer_step(yb_sim* sim, int64_t nsteps);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
