@@ -475,6 +475,7 @@ int step_fused(yb_sim* s, ZPart z, int zchunk, bool flip) {
   unsigned long long& base = s->on_side ? s->sched2_base : s->sched_base;
   a.sched = sc;
   a.sched_base = base;
+  a.no_faces = s->on_side ? 1 : 0;  // the boundary launch of the split sweep does them
   a.store_policy = s->store_policy;
   a.co = coef_args(s);
   for (int c = 0; c < 6; ++c) {
@@ -590,6 +591,7 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
   }
   a.sched = sc;
   a.sched_base = base;
+  a.no_faces = s->on_side ? 1 : 0;  // the boundary launch of the split sweep does them
   a.store_policy = 1;
   a.co = coef_args(s);
   for (int c = 0; c < 6; ++c) {

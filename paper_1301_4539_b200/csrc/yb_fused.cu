@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // through item_q, published by the (release) arrive on the item's first
   // full barrier; -1 (no work left) is published by a plain arrive.
   if (w == kTY + 1) {  // face warp: the upper-face DoFs (face_point)
+    if (a.no_faces) return;
     const long long nf = face_points(g);
     for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL)
       face_point(g, a.in, a.out, co, t);

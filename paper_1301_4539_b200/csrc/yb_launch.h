@@ -106,6 +106,10 @@ struct FusedArgs {
   // its next period's boundary items while this launch is still in its interior.
   int pfold;
   const unsigned* pflag;
+  // the upper-face DoFs are someone else's: the interior launch of a split
+  // sweep runs concurrently with the boundary launch, which applies them
+  // (the two-step update h <- f(f(h)) re-reads its output, so it must run once)
+  int no_faces;
   unsigned pneed, psig_val;
   unsigned* psig[2];
   unsigned* pcnt;                // per side: boundary items completed (monotonic)

@@ -683,6 +683,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   if (w == FACE) {  // upper-face DoFs, two steps per sweep: h <- Da*(Da*h + 0) + 0
     // (no sweep reads them for a valid update, so all sweeps' steps are applied
     // here in order, into the buffer that holds the launch's final state)
+    if (a.no_faces) return;
     const long long nf = face_points(g);
     if (!MS) {
       for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {

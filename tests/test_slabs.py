@@ -374,6 +374,9 @@ def test_gpu_slabs_peer_push(yb, oracle, variant, nranks, nzg):
             s.add_source(*q)
         s.fill(8)
         sims.append(s)
+    st = torch.cuda.Stream()
+    for s in sims:
+        s.set_stream(st.cuda_stream)
     for lo, hi in zip(sims[:-1], sims[1:]):
         lo.peer_link(1, hi)
         hi.peer_link(0, lo)
