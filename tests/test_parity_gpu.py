@@ -153,9 +153,12 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("variant", VARIANTS + ["tb2_one_sweep_per_launch"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_configs_vs_oracle(yb, oracle, name, variant):
+def test_configs_vs_oracle(yb, oracle, name, variant, monkeypatch):
+    if variant == "tb2_one_sweep_per_launch":  # the two-step kernel without multi-sweep launches
+        monkeypatch.setenv("YB_TB2_PERSIST", "0")
+        variant = 2
     nx, ny, nz, steps, es, ss, fs, has_src = CASES[name]
     src = None
     if has_src and nx > 2 and ny > 2 and nz > 2:
@@ -575,8 +578,7 @@ def test_multi_sweep_launches(yb, oracle, name, zchunk, monkeypatch):
         sim.run(steps)
         launches = sim.info()["kernel_launches"]
         got = sim.download()
-    if zchunk > 0:  # a given chunk length forces multi-sweep launches (auto: large grids only)
-        assert launches <= 3 + steps % 2  # the pairs ran in one launch
+    assert launches <= 3 + steps % 2  # the pairs ran in one launch
     want = oracle_run(oracle, nx, ny, nz, f, steps, medium=(es, ss) if es >= 0 or ss >= 0 else None, src=src)
     assert_bits(got, want, name)
 
