@@ -358,14 +358,15 @@ int prepare_fused(yb_sim* s) {
     zc2 = std::min(std::max(zc2, 1), s->g.nz);
     s->zchunk2 = zc2;
     // Multi-sweep launches have no wave tail (the next sweep fills idle SMs),
-    // so they take the longest chunks that still leave >= 2 items per SM in
+    // so they take the longest chunks that still leave ~1.7 items per SM in
     // a sweep; each chunk boundary re-streams ~3 planes, so never shorter than
     // 8 planes. Measured (tools/chunk_sweep.sh, Gcell/s): config 1 (128^3,
     // 16 tiles) chunk 4/6/8/10 -> 91/108/114/105 vs 88 with one launch per
     // sweep; config 2 chunk 16/32/52/64 -> 144/163/170/171; configs 3 / 4
     // chunk 64/128/256 -> 157/162/165 and 179/185/187.
     {
-      const long long T = (long long)tx * ty, need = 2LL * s->num_sms;
+      // (~1.7 items per SM and sweep measured best: config 1 chunk 8 -> 256 items, config 2 chunk 64)
+      const long long T = (long long)tx * ty, need = (17LL * s->num_sms + 9) / 10;
       // (chunks capped at 256 planes: longer ones measured no better)
       const int Zr = (int)std::min<long long>(s->g.nz, std::max<long long>((need + T - 1) / T, (s->g.nz + 255) / 256));
       const int len = (s->g.nz + Zr - 1) / Zr;
