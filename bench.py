@@ -262,21 +262,13 @@ def main():
     if world > 1:
         exch = None
         if args.exchange in ("auto", "p2p"):
-            try:
+            try:  # collective: raises on every rank or on none
                 exch = PeerExchange(sim, rank, world)
-                why = ""
-            except Exception as e:  # noqa: BLE001 - decided collectively below
-                why = f"{type(e).__name__}: {e}"
-            if args.exchange == "auto":  # every rank must agree on the transport
-                whys = [None] * world
-                dist.all_gather_object(whys, why)
-                bad = [w for w in whys if w]
-                if bad:
-                    exch = None
-                    if rank == 0:
-                        print(f"p2p exchange unavailable ({bad[0]}); using NCCL", file=sys.stderr)
-            elif why:
-                raise RuntimeError(why)
+            except RuntimeError as e:
+                if args.exchange == "p2p":
+                    raise
+                if rank == 0:
+                    print(f"{e}; using NCCL", file=sys.stderr)
         args.exchange = "p2p" if exch is not None else "nccl"
         if exch is None:
             exch = HaloExchange(sim, rank, world, f"cuda:{local}")

@@ -113,19 +113,39 @@ class PeerExchange:
     """Direct halo push over peer memory (NVLink P2P, CUDA IPC): each rank
     exports IPC handles of its state buffers, all ranks gather them once
     (torch.distributed object collective), and each slab opens its two
-    neighbours'. Afterwards no collective runs: the library's push kernel
-    writes the boundary planes straight into the neighbours' ghost planes and
-    bumps their flag words; a device-side wait orders the next sweep."""
+    neighbours'. Afterwards no collective runs: yb_peer_step's sweep stores
+    the boundary planes straight into the neighbours' ghost planes and orders
+    the exchange through their flag words (run_steps_peer). Setup is
+    collective: if any rank cannot export or map, every rank raises."""
 
     def __init__(self, sim, rank: int, world: int, group=None):
         self.sim = sim
+        # every step is collective, so a failure on one rank raises on all of
+        # them (callers may then fall back to HaloExchange together)
+        why = ""
+        try:
+            mine = (sim.peer_export(), sim.nz)
+        except Exception as e:  # noqa: BLE001
+            mine, why = None, f"{type(e).__name__}: {e}"
         info = [None] * world
-        dist.all_gather_object(info, (sim.peer_export(), sim.nz), group=group)
-        if rank > 0:
-            sim.peer_open(0, *info[rank - 1])
-        if rank < world - 1:
-            sim.peer_open(1, *info[rank + 1])
-        dist.barrier(group=group)
+        dist.all_gather_object(info, mine, group=group)
+        if not why:
+            try:
+                if rank > 0:
+                    if info[rank - 1] is None:
+                        raise RuntimeError("lower neighbour could not export its memory")
+                    sim.peer_open(0, *info[rank - 1])
+                if rank < world - 1:
+                    if info[rank + 1] is None:
+                        raise RuntimeError("upper neighbour could not export its memory")
+                    sim.peer_open(1, *info[rank + 1])
+            except Exception as e:  # noqa: BLE001
+                why = f"{type(e).__name__}: {e}"
+        whys = [None] * world
+        dist.all_gather_object(whys, why, group=group)
+        bad = [(r, w) for r, w in enumerate(whys) if w]
+        if bad:
+            raise RuntimeError(f"peer-memory exchange unavailable on rank {bad[0][0]}: {bad[0][1]}")
 
 
 def run_steps_peer(sim, nsteps: int, depth: int):

@@ -582,3 +582,55 @@ def test_gpu_peer_wait_times_out(yb):
         a.synchronize()
     for s in (a, b):
         s.close()
+
+
+class _FakePeerSim:
+    """Host-side stand-in for PeerExchange's setup logic (no GPU): rank
+    `fail_rank` cannot map its neighbours' memory."""
+
+    def __init__(self, rank, fail_rank, fail_at):
+        self.rank, self.fail_rank, self.fail_at, self.nz, self.opened = rank, fail_rank, fail_at, 5, []
+
+    def peer_export(self):
+        if self.rank == self.fail_rank and self.fail_at == "export":
+            raise RuntimeError("cudaIpcGetMemHandle failed")
+        return b"h%d" % self.rank
+
+    def peer_open(self, side, handles, nz):
+        if self.rank == self.fail_rank and self.fail_at == "open":
+            raise RuntimeError("cudaIpcOpenMemHandle failed")
+        self.opened.append((side, handles, nz))
+
+
+def _peer_setup_worker(rank, world, port, fail_rank, fail_at, result_path):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1301_4539_b200.slabs import PeerExchange
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sim = _FakePeerSim(rank, fail_rank, fail_at)
+    try:
+        PeerExchange(sim, rank, world)
+        out = "ok " + ",".join(f"{s}:{h.decode()}" for s, h, _ in sim.opened)
+    except RuntimeError as e:
+        out = "raised " + str(e)
+    dist.barrier()  # every rank reached here: no collective was left unmatched
+    with open(f"{result_path}.{rank}", "w") as f:
+        f.write(out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank,fail_at", [(-1, None), (1, "open"), (0, "export"), (2, "open")])
+def test_peer_exchange_setup_is_collective(tmp_path, fail_rank, fail_at):
+    """PeerExchange over gloo (world 3, no GPU): handles reach the right
+    neighbours; when one rank cannot export or map, every rank raises (so
+    bench.py --exchange auto falls back to NCCL on all ranks together)."""
+    world = 3
+    path = str(tmp_path / "setup")
+    mp.spawn(_peer_setup_worker, args=(world, _free_port(), fail_rank, fail_at, path), nprocs=world, join=True)
+    outs = [open(f"{path}.{r}").read() for r in range(world)]
+    if fail_rank < 0:
+        assert outs == ["ok 1:h1", "ok 0:h0,1:h2", "ok 0:h1"]
+    else:
+        assert all(o.startswith("raised peer-memory exchange unavailable") for o in outs), outs
