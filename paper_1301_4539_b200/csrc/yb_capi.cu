@@ -225,7 +225,12 @@ yb::Fields fields_of(const yb_sim* s, int b) {
   return F;
 }
 
-int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY, int box_cols = yb::kBX) {
+// L2 promotion per kernel, measured (Gcell/s, 3 runs each): the one-step kernel's maps gain with
+// 64 B (config 2 96.4 -> 98.6, config 3 87.3 -> 90.6 vs 256 B); the two-step kernel's are best
+// or equal with 256 B (config 4 187.1 vs 184.7 with 64 B).
+constexpr CUtensorMapL2promotion kPromoFused = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY, int box_cols = yb::kBX,
+               CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(YB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   // z coordinate = local plane + kGhost: the allocation starts at ghost plane -kGhost
@@ -234,7 +239,6 @@ int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY
   const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   // YB_L2PROMO=0..3 (tuning knob): none / 64B / 128B / 256B L2 promotion
-  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (const char* e = std::getenv("YB_L2PROMO")) promo = (CUtensorMapL2promotion)std::atoi(e);
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base - yb::kGhost * g.plane, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
@@ -251,10 +255,10 @@ int prepare_fused(yb_sim* s) {
   for (int b = 0; b < 2; ++b) {
     int q = 0;
     for (int c = 0; c < 6; ++c)
-      if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->buf[b][c])) return rc;
+      if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->buf[b][c], yb::kBY, yb::kBX, kPromoFused)) return rc;
     for (int a = 0; a < 4; ++a)
       if (s->cell[a])
-        if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->cell[a])) return rc;
+        if (int rc = encode_map(&s->tm[b].m[q++], s->g, s->cell[a], yb::kBY, yb::kBX, kPromoFused)) return rc;
   }
   const size_t avail = 227 * 1024;
   // Ring depth: measured best at 4 stages (<= 7 arrays) / 3 (more), i.e.
