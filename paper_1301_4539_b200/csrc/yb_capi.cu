@@ -567,8 +567,8 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
       a.pcnt_base[0] = s->pcnt_base[0];
       a.pcnt_base[1] = s->pcnt_base[1];
       a.perr = reinterpret_cast<int*>(s->pflags + 2);
-      if (s->peer[0].on) s->pcnt_base[0] += (unsigned)T;
-      if (s->peer[1].on) s->pcnt_base[1] += (unsigned)T;
+      if (s->peer[0].on) s->pcnt_base[0] += (unsigned)T * yb::kTB2RowWarps;  // every row warp counts
+      if (s->peer[1].on) s->pcnt_base[1] += (unsigned)T * yb::kTB2RowWarps;
     } else {
       if (int rc = yb_peer_wait(s)) return rc;
     }

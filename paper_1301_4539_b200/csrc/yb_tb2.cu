@@ -181,7 +181,8 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   const int c_lo = max(kz0 - 3, 0) / a.zchunk, c_hi = min((kz1 + 2) / a.zchunk, a.nch0 - 1);
   const int y_lo = max(ty - 1, 0), y_hi = min(ty + 1, a.nty - 1);
   const int x_lo = max(tx - 1, 0), x_hi = min(tx + 1, a.ntx - 1);
-  const unsigned need = a.epoch + (unsigned)sw;
+  // every row warp of an item counts itself in done[item] once per sweep
+  const unsigned need = (a.epoch + (unsigned)sw) * (unsigned)RW;
   for (long long n = 0;; ++n) {  // one pass of independent relaxed loads, then acquire
     bool ok = true;
     for (int cc = c_lo; cc <= c_hi; ++cc)
@@ -291,6 +292,7 @@ struct Rows {
   const SrcArgs& srcm;  // this sweep's sources (MS)
   const int er, l, j, c, i0;
   const bool xedge;
+  const bool pitem;  // MODE 3: this item owns boundary planes a neighbour mirrors
   const uint64_t st_pol;
   float* const e1o;  // E1 buffer 0, comp 0, row er, column c
   float* const h1o;  // H1 buffer 0, comp 0, row er, column c
@@ -306,7 +308,8 @@ struct Rows {
   __device__ __forceinline__ Rows(const FusedArgs& a_, const Item& it_, const Bufs& B_, Cursor& cur_,
                                   float* const* out_, const SrcArgs& src_, int er_, int l_, uint64_t pol)
       : a(a_), it(it_), B(B_), cur(cur_), outm(out_), srcm(src_), er(er_), l(l_), j(it_.y0 - 1 + er_), c(4 + 4 * l_),
-        i0(it_.x0 + 4 * l_), xedge(i0 == 0 || i0 + 4 > a_.g.nx), st_pol(pol),
+        i0(it_.x0 + 4 * l_), xedge(i0 == 0 || i0 + 4 > a_.g.nx),
+        pitem(PS && ((it_.kz0 < 2 && a_.pdn[0]) || (it_.kz1 > a_.g.nz - 2 && a_.pup[0]))), st_pol(pol),
         e1o(B_.e1b + er_ * BX + c), h1o(B_.h1b + er_ * BX + c), e2o(B_.e2b + (er_ - 1) * BX + c) {
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     cdy_e = a.co.cdy_e[max(j, 0)];
@@ -456,7 +459,7 @@ struct Rows {
       if (own) {  // E^{n+2} of the owned rows -> HBM
         const long long gp = gidx(g, i0, j, kh);
         store_rows3(outs(), gp, i0, g.nx, e2c.x, e2c.y, e2c.z, st_pol);
-        if (PS) peer_rows(0, kh, e2c);
+        if (PS && pitem) peer_rows(0, kh, e2c);
       }
       if (QS) {
         const bool nz = own && (nonzero4(e2c.x) | nonzero4(e2c.y) | nonzero4(e2c.z));
@@ -491,7 +494,7 @@ struct Rows {
       if (j < g.ny) {
         const long long gp = gidx(g, i0, j, k4);
         store_rows3(outs() + 3, gp, i0, g.nx, h2.x, h2.y, h2.z, st_pol);
-        if (PS) peer_rows(3, k4, h2);
+        if (PS && pitem) peer_rows(3, k4, h2);
       }
       if (QS && j < g.ny) {
         const bool nz = nonzero4(h2.x) | nonzero4(h2.y) | nonzero4(h2.z);
@@ -806,15 +809,21 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       const int ch = item / T, nch = a.nitems / T;
       const bool bd = ch == 0 && a.pdn[0], bu = ch == nch - 1 && a.pup[0];
       if (bd || bu) {
-        __threadfence_system();
-        if (a.pfold) {
-          consumer_sync();
-          if (threadIdx.x == 0) {
-            if (bd && atomicAdd(a.pcnt, 1u) - a.pcnt_base[0] == (unsigned)T - 1u) {
+        if (!a.pfold) {
+          __threadfence_system();  // before the separate signal launch
+        } else if (w < RW) {
+          // each row warp counts itself once its stores are visible system-wide
+          // (its peer stores; every stage it consumed — the ghost planes read —
+          // had landed); the last of the T * RW row warps of the side signals
+          __syncwarp();
+          if (l == 0) {
+            __threadfence_system();
+            const unsigned last = (unsigned)T * RW - 1u;
+            if (bd && atomicAdd(a.pcnt, 1u) - a.pcnt_base[0] == last) {
               __threadfence_system();
               asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.psig[0]), "r"(a.psig_val) : "memory");
             }
-            if (bu && atomicAdd(a.pcnt + 1, 1u) - a.pcnt_base[1] == (unsigned)T - 1u) {
+            if (bu && atomicAdd(a.pcnt + 1, 1u) - a.pcnt_base[1] == last) {
               __threadfence_system();
               asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.psig[1]), "r"(a.psig_val) : "memory");
             }
@@ -822,11 +831,11 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         }
       }
     }
-    if (MS) {  // publish: this item's part of sweep sw is in global memory
-      consumer_sync();
-      if (threadIdx.x == 0) {
+    if (MS && w < RW) {  // publish: this row warp's part of sweep sw is in global memory
+      __syncwarp();
+      if (l == 0) {
         __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done + item), "r"(a.epoch + sw + 1) : "memory");
+        atomicAdd(a.done + item, 1u);
       }
     }
   }
