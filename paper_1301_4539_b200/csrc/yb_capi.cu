@@ -557,7 +557,7 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
         YB_CU(cudaStreamWaitEvent(st, s->peer_done, 0));
         s->peer_inflight = false;
       }
-      a.pfold = 1;
+      a.pfold = std::getenv("YB_PEER_NOREMAP") ? 2 : 1;
       a.pflag = s->pflags;
       a.pneed = s->push_count;
       a.psig_val = s->push_count + 1;

@@ -717,11 +717,12 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
           it = v < (unsigned long long)a.nitems ? (int)v : -1;
           if (PS && it >= 0 && a.pfold) {  // bottom chunk, top chunk, then the interior
             const int nch = a.nitems / T, q = it / T, tile = it - q * T;
-            const int ch = q == 0 ? 0 : (q == 1 ? nch - 1 : q - 1);
+            const int ch = a.pfold == 2 ? q : (q == 0 ? 0 : (q == 1 ? nch - 1 : q - 1));
             it = ch * T + tile;
-            if (ch == 0 && a.pdn[0]) peer_flag_wait(a.pflag, a.pneed, a.perr);
-            if (ch == nch - 1 && a.pup[0]) peer_flag_wait(a.pflag + 1, a.pneed, a.perr);
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
+            const bool wd = ch == 0 && a.pdn[0], wu = ch == nch - 1 && a.pup[0];
+            if (wd) peer_flag_wait(a.pflag, a.pneed, a.perr);
+            if (wu) peer_flag_wait(a.pflag + 1, a.pneed, a.perr);
+            if (wd || wu) asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
           }
         } else if (v < (unsigned long long)a.nitems * a.nsweeps) {
           sw = (int)(v / (unsigned long long)a.nitems);
