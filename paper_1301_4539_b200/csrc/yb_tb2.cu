@@ -21,6 +21,14 @@
 // arrivals on its "empty" mbarrier). Chunk boundaries re-stream two planes below and one
 // above (the wavefront's z-halo). Arithmetic: yee_upd, bit-identical to two
 // single steps.
+//
+// Kernel modes (template MODE): 0 one sweep per launch; 1 + quiescent-item
+// skip; 2 several sweeps per launch — items sweep-major, each waits for the
+// sweep-(s-1) completion counts of its 3x3-tile x adjacent-chunk neighbourhood
+// (every row warp adds 1 to done[item] after a fence; no item-end barrier);
+// 3 z-slab peer stores — boundary planes also stored into the neighbours'
+// ghost planes, boundary chunks handed out first, in-kernel wait on the
+// neighbours' flags and a per-side row-warp count whose last member signals.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
