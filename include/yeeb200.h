@@ -136,6 +136,12 @@ int yb_host_medium_slab(int nx, int ny, int nz_global, int z_offset, int nplanes
 /* FieldSet readout/writeback (fields.hpp:21-67). Dense reference layout. */
 int yb_upload_field(yb_sim* sim, int comp, const float* dense);
 int yb_download_field(yb_sim* sim, int comp, float* dense);
+/* All six components (Ex, Ey, Ez, Hx, Hy, Hz) in one call: the host<->device
+ * copies run back to back while the dense<->padded layout conversion of the
+ * previous component overlaps them; one synchronisation at the end (the host
+ * buffers may be reused when the call returns). */
+int yb_upload_fields(yb_sim* sim, const float* const* dense6);
+int yb_download_fields(yb_sim* sim, float* const* dense6);
 /* FieldSet::zero() (fields.hpp:60-63) and seeded init (yeeb200_inputs.h). */
 int yb_zero_fields(yb_sim* sim);
 int yb_fill_fields(yb_sim* sim, uint64_t seed);

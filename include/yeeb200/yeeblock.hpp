@@ -498,13 +498,17 @@ class Simulation {
   }
   void sync_mirror() {
     if (have_mirror_) return;
-    for (Comp c : kAllComps) detail::check(yb_download_field(h_, comp_index(c), mirror_.field(c).data()));
+    float* d6[6];
+    for (Comp c : kAllComps) d6[comp_index(c)] = mirror_.field(c).data();
+    detail::check(yb_download_fields(h_, d6));
     mirror_.step_index = step_;
     have_mirror_ = true;
   }
   void push_if_dirty() {
     if (!dirty_) return;
-    for (Comp c : kAllComps) detail::check(yb_upload_field(h_, comp_index(c), mirror_.field(c).data()));
+    const float* u6[6];
+    for (Comp c : kAllComps) u6[comp_index(c)] = mirror_.field(c).data();
+    detail::check(yb_upload_fields(h_, u6));
     step_ = mirror_.step_index;
     detail::check(yb_set_step_index(h_, step_));
     dirty_ = false;
@@ -580,10 +584,18 @@ void step_standard(const GridSpec<Real>& g, FieldSet<Real>& f, const Coefficient
     ~Guard() { yb_destroy(h); }
   } guard{h};
   detail::check(yb_set_axis_coeffs(h, c.cdx.data(), c.cdy.data(), c.cdz.data()));
-  for (Comp q : kAllComps) detail::check(yb_upload_field(h, comp_index(q), f.field(q).data()));
+  {
+    const float* u6[6];
+    for (Comp q : kAllComps) u6[comp_index(q)] = f.field(q).data();
+    detail::check(yb_upload_fields(h, u6));
+  }
   detail::check(yb_set_step_index(h, f.step_index));
   detail::check(yb_advance(h, 1));
-  for (Comp q : kAllComps) detail::check(yb_download_field(h, comp_index(q), f.field(q).data()));
+  {
+    float* d6[6];
+    for (Comp q : kAllComps) d6[comp_index(q)] = f.field(q).data();
+    detail::check(yb_download_fields(h, d6));
+  }
   f.step_index += 1;
 }
 

@@ -34,7 +34,7 @@ S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt
 ABI_SYMBOLS = (
     "yb_last_error", "yb_abi_version", "yb_create", "yb_destroy", "yb_set_axis_coeffs",
     "yb_set_cell_coeffs", "yb_generate_medium", "yb_upload_field", "yb_download_field",
-    "yb_zero_fields", "yb_fill_fields", "yb_set_step_index", "yb_get_step_index",
+    "yb_upload_fields", "yb_download_fields", "yb_zero_fields", "yb_fill_fields", "yb_set_step_index", "yb_get_step_index",
     "yb_add_source", "yb_clear_sources", "yb_advance", "yb_synchronize", "yb_advance_timed",
     "yb_apply_ampere_range", "yb_apply_faraday_range", "yb_apply_pec_boundary",
     "yb_field_digest", "yb_set_stream", "yb_set_kernel_timing", "yb_get_info",
@@ -101,6 +101,8 @@ def lib():
         L.yb_set_cell_coeffs.argtypes = [vp, C.c_int, _f32p, C.c_float]
         L.yb_generate_medium.argtypes = [vp, C.c_int64, C.c_int64]
         L.yb_upload_field.argtypes = [vp, C.c_int, _f32p]
+        L.yb_upload_fields.argtypes = [vp, C.POINTER(vp)]
+        L.yb_download_fields.argtypes = [vp, C.POINTER(vp)]
         L.yb_download_field.argtypes = [vp, C.c_int, _f32p]
         L.yb_zero_fields.argtypes = [vp]
         L.yb_fill_fields.argtypes = [vp, C.c_uint64]
@@ -232,10 +234,13 @@ class Simulation:
 
     # fields -----------------------------------------------------------------
     def upload(self, fields):
+        arrs = []
         for c in range(6):
             a = _f32c(fields[c])
             assert a.shape == comp_extents(self.nx, self.ny, self.nz, c)[::-1], (c, a.shape)
-            _check(lib().yb_upload_field(self._h, c, _fp(a)))
+            arrs.append(a)
+        ptrs = (C.c_void_p * 6)(*[a.ctypes.data for a in arrs])  # arrs keeps the buffers alive
+        _check(lib().yb_upload_fields(self._h, ptrs))
 
     def download(self, out=None):
         """Dense host copies of the six components (into `out` if given, e.g.
@@ -245,8 +250,9 @@ class Simulation:
             shape = comp_extents(self.nx, self.ny, self.nz, c)[::-1]
             a = np.empty(shape, np.float32) if out is None else out[c]
             assert a.shape == shape and a.dtype == np.float32 and a.flags.c_contiguous
-            _check(lib().yb_download_field(self._h, c, _fp(a)))
             res.append(a)
+        ptrs = (C.c_void_p * 6)(*[a.ctypes.data for a in res])
+        _check(lib().yb_download_fields(self._h, ptrs))
         return res
 
     def zero(self):

@@ -146,6 +146,8 @@ struct yb_sim {
   // split sweeps: the interior launch runs on a side stream with its own
   // work counter, concurrently with the boundary launch and the exchange
   cudaStream_t side = nullptr;
+  cudaStream_t xfer = nullptr;  // layout conversion of yb_upload_fields / yb_download_fields
+  cudaEvent_t xev[7] = {};
   cudaEvent_t ev_pre = nullptr, ev_int = nullptr;
   unsigned long long* sched2 = nullptr;
   unsigned long long sched2_base = 0;
@@ -871,6 +873,9 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->sched);
   cudaFree(s->sched2);
   if (s->side) cudaStreamDestroy(s->side);
+  if (s->xfer) cudaStreamDestroy(s->xfer);
+  for (cudaEvent_t e : s->xev)
+    if (e) cudaEventDestroy(e);
   if (s->ev_pre) cudaEventDestroy(s->ev_pre);
   if (s->ev_int) cudaEventDestroy(s->ev_int);
   cudaFree(s->probe_dev);
@@ -1125,6 +1130,61 @@ int yb_download_field(yb_sim* s, int comp, float* dense) {
   if (int rc = check_comp(comp)) return rc;
   YB_CU(cudaSetDevice(s->device));
   return copy_dense(s, comp, s->buf[s->cur][comp], nullptr, dense);
+}
+
+static int ensure_xfer(yb_sim* s) {
+  if (s->xfer) return YB_OK;
+  YB_CU(cudaStreamCreateWithFlags(&s->xfer, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : s->xev) YB_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return YB_OK;
+}
+
+int yb_upload_fields(yb_sim* s, const float* const* d) {
+  if (!s || !d) return fail(YB_INVALID_ARGUMENT, "null argument");
+  for (int c = 0; c < 6; ++c)
+    if (!d[c]) return fail(YB_INVALID_ARGUMENT, "null component %d", c);
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
+  YB_CU(cudaSetDevice(s->device));
+  if (int rc = ensure_xfer(s)) return rc;
+  s->q_valid = false;
+  for (int c = 0; c < 6; ++c) {  // copies on the handle's stream, back to back
+    int e[3];
+    comp_ext(s->g, c, e);
+    float* stage = s->buf[s->cur ^ 1][c];
+    YB_CU(cudaMemcpyAsync(stage, d[c], (size_t)e[0] * e[1] * e[2] * 4, cudaMemcpyHostToDevice, s->stream));
+    YB_CU(cudaEventRecord(s->xev[c], s->stream));
+    YB_CU(cudaStreamWaitEvent(s->xfer, s->xev[c], 0));  // its scatter overlaps the next copy
+    YB_CU(yb::launch_scatter_dense(s->g, e, stage, s->buf[s->cur][c], s->xfer));
+    YB_CU(cudaMemsetAsync(stage - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->xfer));
+  }
+  YB_CU(cudaEventRecord(s->xev[6], s->xfer));
+  YB_CU(cudaStreamWaitEvent(s->stream, s->xev[6], 0));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_download_fields(yb_sim* s, float* const* d) {
+  if (!s || !d) return fail(YB_INVALID_ARGUMENT, "null argument");
+  for (int c = 0; c < 6; ++c)
+    if (!d[c]) return fail(YB_INVALID_ARGUMENT, "null component %d", c);
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
+  YB_CU(cudaSetDevice(s->device));
+  if (int rc = ensure_xfer(s)) return rc;
+  YB_CU(cudaEventRecord(s->xev[6], s->stream));  // the state is final
+  YB_CU(cudaStreamWaitEvent(s->xfer, s->xev[6], 0));
+  for (int c = 0; c < 6; ++c) {  // gathers on the side stream, each copy starts as its gather ends
+    int e[3];
+    comp_ext(s->g, c, e);
+    float* stage = s->buf[s->cur ^ 1][c];
+    YB_CU(yb::launch_gather_dense(s->g, e, s->buf[s->cur][c], stage, s->xfer));
+    YB_CU(cudaEventRecord(s->xev[c], s->xfer));
+    YB_CU(cudaStreamWaitEvent(s->stream, s->xev[c], 0));
+    YB_CU(cudaMemcpyAsync(d[c], stage, (size_t)e[0] * e[1] * e[2] * 4, cudaMemcpyDeviceToHost, s->stream));
+  }
+  for (int c = 0; c < 6; ++c)
+    YB_CU(cudaMemsetAsync(s->buf[s->cur ^ 1][c] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
 }
 
 int yb_zero_fields(yb_sim* s) {
