@@ -821,6 +821,12 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(YB_CUDA_ERROR, "stream create failed"));
   s->stream = s->own_stream;
+  // the transfer side stream exists from the start (not created inside a timed upload)
+  if (cudaStreamCreateWithFlags(&s->xfer, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(YB_CUDA_ERROR, "stream create failed"));
+  for (cudaEvent_t& e : s->xev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(YB_CUDA_ERROR, "event create failed"));
   const size_t bytes = (size_t)g.total * sizeof(float);
   for (int b = 0; b < 2; ++b)
     for (int c = 0; c < 6; ++c) {
