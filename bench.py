@@ -144,7 +144,8 @@ def cpu_reference_rate(nx, ny, nz, budget_s=10.0, max_steps=None):
 
 def load_traffic(cfg, variant):
     """ncu DRAM bytes per cell-update of this config's sweep kernel (profiles/ncu_traffic.json,
-    written by tools/ncu_summary.py from one --set full capture), or None."""
+    written by tools/ncu_summary.py from one --set full capture, or from an ncu --metrics
+    dram__bytes pass over the config's launches — see each entry's "source"), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
