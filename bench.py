@@ -142,6 +142,25 @@ def cpu_reference_rate(nx, ny, nz, budget_s=10.0, max_steps=None):
             "sample": f"C oracle port (OpenMP {cores} threads) {nx}x{ny}x{nz}, {steps} steps"}
 
 
+def gpu_local_cpus(device):
+    """CPUs on the GPU's NUMA node (sysfs local_cpulist of its PCI device), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(device)).busId
+        bus = bus.decode() if isinstance(bus, bytes) else bus
+        dom, rest = bus.lower().split(":", 1)
+        path = f"/sys/bus/pci/devices/{dom[-4:]}:{rest}/local_cpulist"
+        cpus = set()
+        for part in open(path).read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
 def load_traffic(cfg, variant):
     """ncu DRAM bytes per cell-update of this config's sweep kernel (profiles/ncu_traffic.json,
     written by tools/ncu_summary.py from one --set full capture, or from an ncu --metrics
@@ -353,6 +372,13 @@ def main():
     # step count (with halo exchanges), fields downloaded.
     e2e = e2e_skip = None
     if not args.no_e2e:
+        # pinned host buffers on the GPU's NUMA node (first touch by a local CPU),
+        # so the copies do not cross the socket interconnect; restored afterwards
+        affinity = os.sched_getaffinity(0)
+        local_cpus = gpu_local_cpus(local)
+        if local_cpus:
+            os.sched_setaffinity(0, local_cpus)
+
         def pin(shape):
             return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
         shapes = [Y.comp_extents(nx, ny, nz, c)[::-1] for c in range(6)]
@@ -386,8 +412,8 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            for q, a_ in cell_arrays.items():
-                s2.set_cell_coeffs(q, a_)
+            if cell_arrays:
+                s2.set_cell_coeffs_many(cell_arrays)
             s2.upload(host_f)
             if ex2 is None:
                 s2.run(e_steps)
@@ -423,6 +449,8 @@ def main():
                         "note": "same e2e run with yb_set_quiescent_skip(1) (RunOptions::quiescent_skip, "
                                 "runner.hpp:60-73): all-zero work items skipped, results bit-identical; "
                                 "informational, not the headline"}
+        os.sched_setaffinity(0, affinity)
+        e2e["host_cpus"] = f"{len(local_cpus)} CPUs of the GPU NUMA node" if local_cpus else "all (GPU NUMA node unknown)"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

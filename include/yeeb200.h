@@ -141,6 +141,11 @@ int yb_download_field(yb_sim* sim, int comp, float* dense);
  * previous component overlaps them; one synchronisation at the end (the host
  * buffers may be reused when the call returns). */
 int yb_upload_fields(yb_sim* sim, const float* const* dense6);
+/* Several per-cell coefficient arrays in one call (which[i] in CA..DB, each
+ * at most once, cells[i] non-null): the copies run back to back with one
+ * synchronisation for their uniformity checks; otherwise as n calls of
+ * yb_set_cell_coeffs(which[i], cells[i], 0). */
+int yb_set_cell_coeffs_n(yb_sim* sim, int n, const int* which, const float* const* cells);
 int yb_download_fields(yb_sim* sim, float* const* dense6);
 /* FieldSet::zero() (fields.hpp:60-63) and seeded init (yeeb200_inputs.h). */
 int yb_zero_fields(yb_sim* sim);

@@ -33,7 +33,7 @@ S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt
 # C-ABI exported symbols (include/yeeb200.h) — checked by tests.
 ABI_SYMBOLS = (
     "yb_last_error", "yb_abi_version", "yb_create", "yb_destroy", "yb_set_axis_coeffs",
-    "yb_set_cell_coeffs", "yb_generate_medium", "yb_upload_field", "yb_download_field",
+    "yb_set_cell_coeffs", "yb_set_cell_coeffs_n", "yb_generate_medium", "yb_upload_field", "yb_download_field",
     "yb_upload_fields", "yb_download_fields", "yb_zero_fields", "yb_fill_fields", "yb_set_step_index", "yb_get_step_index",
     "yb_add_source", "yb_clear_sources", "yb_advance", "yb_synchronize", "yb_advance_timed",
     "yb_apply_ampere_range", "yb_apply_faraday_range", "yb_apply_pec_boundary",
@@ -99,6 +99,7 @@ def lib():
         L.yb_destroy.argtypes = [vp]
         L.yb_set_axis_coeffs.argtypes = [vp, _f32p, _f32p, _f32p]
         L.yb_set_cell_coeffs.argtypes = [vp, C.c_int, _f32p, C.c_float]
+        L.yb_set_cell_coeffs_n.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(vp)]
         L.yb_generate_medium.argtypes = [vp, C.c_int64, C.c_int64]
         L.yb_upload_field.argtypes = [vp, C.c_int, _f32p]
         L.yb_upload_fields.argtypes = [vp, C.POINTER(vp)]
@@ -228,6 +229,17 @@ class Simulation:
             slab = self.nz_global != self.nz  # z-slab: nz + 4 cell planes from z_offset - 2
             assert cells.size == self.nx * self.ny * (self.nz + (4 if slab else 0))
             _check(lib().yb_set_cell_coeffs(self._h, which, _fp(cells), uniform))
+
+    def set_cell_coeffs_many(self, arrays):
+        """{which: cells} for several coefficient arrays in one call
+        (yb_set_cell_coeffs_n: the copies run back to back)."""
+        slab = self.nz_global != self.nz
+        items = [(w, _f32c(a)) for w, a in arrays.items()]
+        for _, a in items:
+            assert a.size == self.nx * self.ny * (self.nz + (4 if slab else 0))
+        which = (C.c_int * len(items))(*[w for w, _ in items])
+        ptrs = (C.c_void_p * len(items))(*[a.ctypes.data for _, a in items])
+        _check(lib().yb_set_cell_coeffs_n(self._h, len(items), which, ptrs))
 
     def generate_medium(self, eps_seed=-1, sigma_seed=-1):
         _check(lib().yb_generate_medium(self._h, eps_seed, sigma_seed))

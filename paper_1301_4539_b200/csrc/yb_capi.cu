@@ -154,6 +154,7 @@ struct yb_sim {
   bool on_side = false;
   PeerSide peer[2];           // direct halo push targets (0: below, 1: above)
   unsigned* pflags = nullptr; // my flag words [0] from below, [1] from above, [2] error
+  int* cflags = nullptr;      // uniformity flags of yb_set_cell_coeffs_n
   unsigned push_count = 0;
   cudaStream_t peer_stream = nullptr;
   cudaEvent_t peer_go = nullptr, peer_done = nullptr;
@@ -880,6 +881,7 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->sched2);
   if (s->side) cudaStreamDestroy(s->side);
   if (s->xfer) cudaStreamDestroy(s->xfer);
+  if (s->cflags) cudaFree(s->cflags);
   for (cudaEvent_t e : s->xev)
     if (e) cudaEventDestroy(e);
   if (s->ev_pre) cudaEventDestroy(s->ev_pre);
@@ -916,34 +918,28 @@ int yb_set_axis_coeffs(yb_sim* s, const float* cdx, const float* cdy, const floa
   return upload_axis(s);
 }
 
-int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) {
-  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
-  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
-  if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
-  YB_CU(cudaSetDevice(s->device));
+// Per-cell coefficient upload, part 1: the host array into a staging buffer
+// and a device check of uniformity (bit patterns) into *flag; no sync.
+static int cell_stage(yb_sim* s, const float* cells, long long n, float* stage, int* flag) {
+  YB_CU(cudaMemcpyAsync(stage, cells, (size_t)n * 4, cudaMemcpyHostToDevice, s->stream));
+  const int one = 1;
+  YB_CU(cudaMemcpyAsync(flag, &one, 4, cudaMemcpyHostToDevice, s->stream));
+  YB_CU(yb::launch_all_equal(stage, n, flag, s->num_sms, s->stream));
+  return YB_OK;
+}
+
+static long long cell_count(const yb_sim* s) {
   // single domain: nz cell planes. z-slab mode: nz + 2*kGhost planes, the
   // global cell planes z_offset-kGhost .. z_offset+nz+kGhost-1 (entries of
   // planes outside the global grid are ignored)
+  const int nzc = s->g.nzg != s->g.nz ? s->g.nz + 2 * yb::kGhost : s->g.nz;
+  return (long long)s->g.nx * s->g.ny * nzc;
+}
+
+// Part 2: store array `which` from the staged copy (or as a uniform value).
+static int cell_finish(yb_sim* s, int which, const float* cells, bool all_equal, float v, float* stage) {
   const bool slab = s->g.nzg != s->g.nz;
   const int nzc = slab ? s->g.nz + 2 * yb::kGhost : s->g.nz;
-  const long long n = (long long)s->g.nx * s->g.ny * nzc;
-  bool all_equal = false;
-  float v = uniform;
-  // staging: the spare state buffer from its allocation start (see copy_dense)
-  float* stage = s->buf[s->cur ^ 1][0] - yb::kGhost * s->g.plane;
-  if (cells) {
-    // linear upload, then a device check of uniformity (bit patterns)
-    YB_CU(cudaMemcpyAsync(stage, cells, (size_t)n * 4, cudaMemcpyHostToDevice, s->stream));
-    int* flag = reinterpret_cast<int*>(s->sched) + 2;  // scratch word next to the work counter
-    const int one = 1;
-    YB_CU(cudaMemcpyAsync(flag, &one, 4, cudaMemcpyHostToDevice, s->stream));
-    YB_CU(yb::launch_all_equal(stage, n, flag, s->num_sms, s->stream));
-    int same = 0;
-    YB_CU(cudaMemcpyAsync(&same, flag, 4, cudaMemcpyDeviceToHost, s->stream));
-    YB_CU(cudaStreamSynchronize(s->stream));
-    all_equal = same != 0;
-    v = cells[0];
-  }
   s->tm_valid = false;
   if ((which == YB_CA || which == YB_DA) && (!cells || all_equal) && v != 1.0f) {
     // a uniform Ca / Da other than 1 is stored as a full array: the sweep
@@ -997,6 +993,52 @@ int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) 
                               slab ? s->g.nz + 1 : nzc - 1, s->stream));
   YB_CU(cudaMemsetAsync(stage, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
+  return YB_OK;
+}
+
+int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) {
+  if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
+  if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
+  YB_CU(cudaSetDevice(s->device));
+  bool all_equal = false;
+  float v = uniform;
+  // staging: the spare state buffer from its allocation start (see copy_dense)
+  float* stage = s->buf[s->cur ^ 1][0] - yb::kGhost * s->g.plane;
+  if (cells) {
+    int* flag = reinterpret_cast<int*>(s->sched) + 2;  // scratch word next to the work counter
+    if (int rc = cell_stage(s, cells, cell_count(s), stage, flag)) return rc;
+    int same = 0;
+    YB_CU(cudaMemcpyAsync(&same, flag, 4, cudaMemcpyDeviceToHost, s->stream));
+    YB_CU(cudaStreamSynchronize(s->stream));
+    all_equal = same != 0;
+    v = cells[0];
+  }
+  return cell_finish(s, which, cells, all_equal, v, stage);
+}
+
+int yb_set_cell_coeffs_n(yb_sim* s, int n, const int* which, const float* const* cells) {
+  if (!s || (n > 0 && (!which || !cells))) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (n < 0 || n > 4) return fail(YB_INVALID_ARGUMENT, "1 .. 4 arrays");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
+  for (int i = 0; i < n; ++i) {
+    if (which[i] < 0 || which[i] > 3 || !cells[i]) return fail(YB_INVALID_ARGUMENT, "bad array %d", i);
+    for (int k = 0; k < i; ++k)
+      if (which[k] == which[i]) return fail(YB_INVALID_ARGUMENT, "coefficient %d given twice", which[i]);
+  }
+  YB_CU(cudaSetDevice(s->device));
+  if (!s->cflags) YB_CU(cudaMalloc(&s->cflags, 4 * sizeof(int)));
+  // all copies back to back (one spare state buffer each), then one sync
+  float* stage[4];
+  for (int i = 0; i < n; ++i) {
+    stage[i] = s->buf[s->cur ^ 1][i] - yb::kGhost * s->g.plane;
+    if (int rc = cell_stage(s, cells[i], cell_count(s), stage[i], s->cflags + i)) return rc;
+  }
+  int same[4] = {0, 0, 0, 0};
+  if (n > 0) YB_CU(cudaMemcpyAsync(same, s->cflags, n * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  for (int i = 0; i < n; ++i)
+    if (int rc = cell_finish(s, which[i], cells[i], same[i] != 0, cells[i][0], stage[i])) return rc;
   return YB_OK;
 }
 

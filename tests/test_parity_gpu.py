@@ -600,3 +600,36 @@ def test_uniform_non_unit_ca_da(yb, oracle, variant):
     want = [a.copy() for a in f]
     oracle.run(nx, ny, nz, want, co, steps)
     assert_bits(got, want, "uniform Ca/Da != 1")
+
+
+def test_cell_coeffs_batched_equals_single(yb, oracle):
+    """yb_set_cell_coeffs_n (back-to-back copies, one sync) stores exactly what
+    four yb_set_cell_coeffs calls store — including a uniform array (kept as
+    the compressed uniform form) and a uniform Da != 1 (a full array)."""
+    nx, ny, nz, steps = 44, 30, 20, 6
+    ca, cb, da, db = oracle.cell_coeffs(nx, ny, nz, 5, 6)
+    cb_u = np.full((nz, ny, nx), cb.flat[0], np.float32)
+    da_u = np.full((nz, ny, nx), 0.5, np.float32)
+    f = oracle.fill_fields(nx, ny, nz, 9)
+    outs = []
+    for batched in (False, True):
+        with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2) as sim:
+            arrays = {yb.CA: ca, yb.CB: cb_u, yb.DA: da_u, yb.DB: db}
+            if batched:
+                sim.set_cell_coeffs_many(arrays)
+            else:
+                for w, a in arrays.items():
+                    sim.set_cell_coeffs(w, a)
+            info = sim.info()
+            sim.upload(f)
+            sim.run(steps)
+            outs.append((info["n_cell_arrays"], sim.download()))
+    assert outs[0][0] == outs[1][0]
+    assert_bits(outs[1][1], outs[0][1], "batched coefficients")
+    co = oracle.Coeffs(nx, ny, nz, ca=ca, cb=cb_u, da=da_u, db=db)
+    want = [a.copy() for a in f]
+    oracle.run(nx, ny, nz, want, co, steps)
+    assert_bits(outs[1][1], want, "batched vs oracle")
+    with yb.Simulation(nx, ny, nz) as sim:
+        with pytest.raises(yb.YeeInvalidArgument):
+            sim.set_cell_coeffs_many({yb.CA: ca, 7: cb})
