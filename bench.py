@@ -1,12 +1,15 @@
 #!/usr/bin/env python3
 """bench.py — Gcell-updates/s of the fp32 Yee E+H leapfrog step on B200.
 
-Default workload = BASELINE config 2 (configs[1]): 256^3 heterogeneous
-dielectric (eps_r ~ U[1,4] seed 1 -> per-cell Cb, Ca = Da = 1, Db = S), PEC,
-Gaussian Ez point source at the centre. One "step" = one full leapfrog time
-step (Ampere, PEC, source, Faraday) over the whole grid. Fields (6 x 67 MB)
-plus the Cb array exceed the 126 MB L2, so no L2 flush is needed between
-steps (stated in config).
+Default workload = BASELINE config 4 (configs[3]), the largest configuration
+that fits one GPU and the one the metric's 1/2/4/8-GPU scaling is quoted on:
+1024 x 1024 x 512 cells, heterogeneous dielectric (eps_r ~ U[1,4] seed 4 ->
+per-cell Cb, Ca = Da = 1, Db = S), PEC, Gaussian Ez point source at the
+centre. One "step" = one full leapfrog time step (Ampere, PEC, source,
+Faraday) over the whole grid. Fields (6 x 2.15 GB) plus the Cb array exceed
+the 126 MB L2 many times over, so no L2 flush is needed between steps
+(stated in config). Under torchrun the fixed grid is split into z-slabs
+(strong scaling); every other config scales weakly.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
                   [--impl ours|reference] [--variant auto|tb2|fused|tb4|naive]
@@ -109,48 +112,88 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(nx, ny, nz, budget_s=10.0, max_steps=None):
-    """The reference's own CPU path (oracle/_ref: yeeblock Simulation<float>,
-    Tiled split 1x16x16, all host cores, quiescent skip off) on the same grid.
-    The reference has no per-cell coefficients, so it runs the vacuum
-    coefficient set on that grid. Falls back to the C oracle port."""
+def _ref_rate(O, nx, ny, nz, f, variant, split, workers, budget_s, max_steps=None):
+    """The reference's own Simulation<float>::run (oracle/_ref) on the grid:
+    one calibration step, then about budget_s of steps; RunStats.total_seconds."""
+    s0, _ = O.ref_simulation(nx, ny, nz, f, 1, variant=variant, split=split, workers=workers)
+    steps = max(1, int(budget_s / max(s0, 1e-6)))
+    if max_steps is not None:
+        steps = min(steps, max_steps)
+    secs, _ = O.ref_simulation(nx, ny, nz, f, steps, variant=variant, split=split, workers=workers)
+    return nx * ny * nz * steps / secs / 1e9, steps
+
+
+def cpu_baselines(nx, ny, nz, es, ss, budget_s=10.0, max_steps=None, like_for_like=True):
+    """CPU paths timed on this host's cores (BASELINE.md CPU-baseline plan),
+    each over a bounded number of steps of the same grid (rates extrapolate
+    linearly in steps; setup excluded, as RunStats.total_seconds):
+
+      reference_tiled   the reference's fastest CPU path: yeeblock
+                        Simulation<float> Tiled, split 1x16x16, all cores,
+                        quiescent skip off (oracle/_ref, unmodified headers).
+                        The reference has no per-cell coefficients, so it
+                        runs the vacuum coefficient set on that grid. This is
+                        the headline value (kind "reference").
+      reference_standard the exact oracle order: Standard, 1 thread.
+      port_materials    the C restatement (oracle/yee_oracle.c, OpenMP, all
+                        cores) on the config's own per-cell medium: the
+                        like-for-like workload (kind "port").
+    """
     from oracle import pyoracle as O
     cores = os.cpu_count() or 1
     f = O.fill_fields(nx, ny, nz, 1, threads=cores)
+    paths = {}
+    head = None
     if O.have_ref():
         split = (1, min(16, ny), min(16, nz))
-        s0, _ = O.ref_simulation(nx, ny, nz, f, 2, variant="tiled", split=split, workers=cores)
-        steps = max(1, int(budget_s * 2 / max(s0, 1e-6)))  # one call of ~budget_s
+        v, n = _ref_rate(O, nx, ny, nz, f, "tiled", split, cores, budget_s, max_steps)
+        head = paths["reference_tiled"] = {
+            "value": v, "unit": UNIT, "cores": cores, "kind": "reference", "same_config": False,
+            "sample": f"yeeblock Simulation<float> Tiled split 1x{split[1]}x{split[2]}, {cores} workers, "
+                      f"{nx}x{ny}x{nz} grid, {n} steps, vacuum coefficients (the reference has no per-cell "
+                      f"Ca/Cb), random fields, quiescent skip off; RunStats.total_seconds"}
+        if like_for_like:
+            v, n = _ref_rate(O, nx, ny, nz, f, "standard", (1, 1, 1), 1, budget_s, max_steps)
+            paths["reference_standard"] = {
+                "value": v, "unit": UNIT, "cores": 1, "kind": "reference", "same_config": False,
+                "sample": f"yeeblock Simulation<float> Standard (the oracle order), 1 thread, {nx}x{ny}x{nz} "
+                          f"grid, {n} steps, vacuum coefficients, random fields; RunStats.total_seconds"}
+    if like_for_like or head is None:
+        if es >= 0:
+            ca, cb, da, db = O.cell_coeffs(nx, ny, nz, es, ss, threads=cores)
+            # the arrays the B200 path streams: Cb only when sigma = 0 (Ca = Da = 1, Db = S exactly)
+            co = (O.Coeffs(nx, ny, nz, cb=cb) if ss < 0 else O.Coeffs(nx, ny, nz, ca=ca, cb=cb, da=da, db=db))
+            med = f"per-cell medium of the config (eps seed {es}, sigma seed {ss})"
+        else:
+            co, med = O.Coeffs(nx, ny, nz), "vacuum (the config's medium)"
+        t = time.perf_counter()
+        O.run(nx, ny, nz, f, co, 1, threads=cores)
+        steps = max(1, int(budget_s / max(time.perf_counter() - t, 1e-6)))
         if max_steps is not None:
             steps = min(steps, max_steps)
-        secs, _ = O.ref_simulation(nx, ny, nz, f, steps, variant="tiled", split=split, workers=cores)
-        return {"value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores,
-                "kind": "reference",
-                "sample": f"yeeblock Simulation<float> Tiled split 1x{split[1]}x{split[2]}, {cores} workers, "
-                          f"{nx}x{ny}x{nz} grid, {steps} steps, vacuum coefficients (the reference has "
-                          f"no per-cell Ca/Cb), quiescent skip off; time from RunStats.total_seconds"}
-    co = O.Coeffs(nx, ny, nz)
-    t = time.perf_counter()
-    O.run(nx, ny, nz, f, co, 2, threads=cores)
-    steps = max(1, int(budget_s * 2 / max(time.perf_counter() - t, 1e-6)))
-    if max_steps is not None:
-        steps = min(steps, max_steps)
-    t = time.perf_counter()
-    O.run(nx, ny, nz, f, co, steps, threads=cores)
-    secs = time.perf_counter() - t
-    return {"value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"C oracle port (OpenMP {cores} threads) {nx}x{ny}x{nz}, {steps} steps"}
+        t = time.perf_counter()
+        O.run(nx, ny, nz, f, co, steps, threads=cores)
+        secs = time.perf_counter() - t
+        paths["port_materials"] = {
+            "value": nx * ny * nz * steps / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "same_config": True,
+            "sample": f"C restatement of the reference step (oracle/yee_oracle.c, OpenMP {cores} threads), "
+                      f"{nx}x{ny}x{nz} grid, {med}, {steps} steps"}
+        if head is None:
+            head = paths["port_materials"]
+    out = dict(head)
+    out["paths"] = paths
+    return out
 
 
 def gpu_local_cpus(device):
-    """CPUs on the GPU's NUMA node (sysfs local_cpulist of its PCI device), or None."""
+    """CPUs on the GPU's NUMA node (sysfs local_cpulist of its PCI device), or None.
+    The device is resolved through CUDA's own PCI ids (they follow
+    CUDA_VISIBLE_DEVICES / CUDA_DEVICE_ORDER; NVML's indices do not)."""
     try:
-        import pynvml
-        pynvml.nvmlInit()
-        bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(device)).busId
-        bus = bus.decode() if isinstance(bus, bytes) else bus
-        dom, rest = bus.lower().split(":", 1)
-        path = f"/sys/bus/pci/devices/{dom[-4:]}:{rest}/local_cpulist"
+        import torch
+        p = torch.cuda.get_device_properties(device)
+        path = f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0/local_cpulist"
         cpus = set()
         for part in open(path).read().strip().split(","):
             lo, _, hi = part.partition("-")
@@ -187,7 +230,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "fused", "naive", "tb2", "tb4"],
                     help="auto: tb2 (two steps per sweep; z-slabs exchange every two steps)")
@@ -216,7 +259,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        ref = cpu_reference_rate(nx, ny, nz, budget_s=60.0, max_steps=max(1, args.steps))
+        ref = cpu_baselines(nx, ny, nz, es, ss, budget_s=20.0, max_steps=max(1, args.steps))
         line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -346,8 +389,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_bytes_per_cell_update": traffic_bpc,
-                "kernel": {0: "k_fused (one E+H sweep per step)", 1: "naive step (4 kernels)",
-                           2: "k_tb2 (two steps per sweep)", 3: "k_tb4 (four steps per sweep)"}[variant],
+                "kernel": {2: "k_fused (one E+H sweep per step)", 1: "naive step (4 kernels)",
+                           0: "k_tb2 (two steps per sweep)", 3: "k_tb4 (four steps per sweep)"}[variant],
                 "kernel_ms_avg": kern_ms, "algorithmic_bytes_per_cell_update": bpc,
                 "peak_source": peak_src, "per_gpu": world > 1,
                 "one_sweep_bytes_per_cell_update": 48.0 + 4.0 * info1["n_cell_arrays"],
@@ -376,85 +419,87 @@ def main():
         # so the copies do not cross the socket interconnect; restored afterwards
         affinity = os.sched_getaffinity(0)
         local_cpus = gpu_local_cpus(local)
-        if local_cpus:
-            os.sched_setaffinity(0, local_cpus)
+        try:
+            if local_cpus:
+                os.sched_setaffinity(0, local_cpus)
 
-        def pin(shape):
-            return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
-        shapes = [Y.comp_extents(nx, ny, nz, c)[::-1] for c in range(6)]
-        host_f = [pin(sh) for sh in shapes]
-        host_out = [pin(sh) for sh in shapes]
-        if fs is not None:
-            Y.host_fields_slab(nx, ny, nz_global, z0, nz, fs, out=host_f)
-        else:
-            for a_ in host_f:
-                a_[...] = 0.0
-        cell_arrays = {}
-        if es >= 0:
-            want = (Y.CB,) if ss < 0 else (Y.CA, Y.CB, Y.DA, Y.DB)
-            # single domain: nz cell planes; z-slab: planes z0-2 .. z0+nz+1 (yb_set_cell_coeffs)
-            zc0, nzc = (z0 - 2, nz + 4) if world > 1 else (0, nz)
-            med = Y.host_medium_slab(nx, ny, nz_global, zc0, nzc, es, ss,
-                                     [pin((nzc, ny, nx)) if q in want else None for q in range(4)])
-            cell_arrays = {q: med[q] for q in want}
-        e_steps = cfg_steps
-
-        def run_e2e(qskip):
-            s2 = make_sim()
-            if table is not None:
-                s2.add_source(*src, table)
-            s2.set_quiescent_skip(qskip)
-            ex2 = None
-            if world > 1:
-                ex2 = (PeerExchange(s2, rank, world) if args.exchange == "p2p"
-                       else HaloExchange(s2, rank, world, f"cuda:{local}"))
-            if dist:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            if cell_arrays:
-                s2.set_cell_coeffs_many(cell_arrays)
-            s2.upload(host_f)
-            if ex2 is None:
-                s2.run(e_steps)
-            elif args.exchange == "p2p":
-                run_steps_peer(s2, e_steps, depth)
+            def pin(shape):
+                return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+            shapes = [Y.comp_extents(nx, ny, nz, c)[::-1] for c in range(6)]
+            host_f = [pin(sh) for sh in shapes]
+            host_out = [pin(sh) for sh in shapes]
+            if fs is not None:
+                Y.host_fields_slab(nx, ny, nz_global, z0, nz, fs, out=host_f)
             else:
-                run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
-            s2.download(out=host_out)
-            dt = time.perf_counter() - t0
-            skipped = s2.info()["skipped_items"]
-            if dist:  # no neighbour may still be storing into this slab's (IPC-mapped) memory
-                torch.cuda.synchronize()
-                dist.barrier()
-            s2.close()
-            if dist:
-                tt = torch.tensor([dt], device="cuda")
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                dt = float(tt.item())
-            return dt, skipped
+                for a_ in host_f:
+                    a_[...] = 0.0
+            cell_arrays = {}
+            if es >= 0:
+                want = (Y.CB,) if ss < 0 else (Y.CA, Y.CB, Y.DA, Y.DB)
+                # single domain: nz cell planes; z-slab: planes z0-2 .. z0+nz+1 (yb_set_cell_coeffs)
+                zc0, nzc = (z0 - 2, nz + 4) if world > 1 else (0, nz)
+                med = Y.host_medium_slab(nx, ny, nz_global, zc0, nzc, es, ss,
+                                         [pin((nzc, ny, nx)) if q in want else None for q in range(4)])
+                cell_arrays = {q: med[q] for q in want}
+            e_steps = cfg_steps
 
-        dt, _ = run_e2e(False)
-        h2d = sum(a_.nbytes for a_ in host_f) + sum(a_.nbytes for a_ in cell_arrays.values())
-        d2h = sum(a_.nbytes for a_ in host_out)
-        e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
-               "steps": e_steps, "wall_s": dt, "per_gpu_bytes": True,
-               "path": "Simulation: set_cell_coeffs + upload (pinned host) -> run(config steps) -> "
-                       "download (pinned host)"}
-        if fs is None:  # zero initial fields + point source: the reference's quiescent skip applies
-            dq, skipped = run_e2e(True)
-            e2e_skip = {"value": cells_total * e_steps / dq / 1e9, "unit": UNIT, "wall_s": dq,
-                        "skipped_items": skipped,
-                        "note": "same e2e run with yb_set_quiescent_skip(1) (RunOptions::quiescent_skip, "
-                                "runner.hpp:60-73): all-zero work items skipped, results bit-identical; "
-                                "informational, not the headline"}
-        os.sched_setaffinity(0, affinity)
+            def run_e2e(qskip):
+                s2 = make_sim()
+                if table is not None:
+                    s2.add_source(*src, table)
+                s2.set_quiescent_skip(qskip)
+                ex2 = None
+                if world > 1:
+                    ex2 = (PeerExchange(s2, rank, world) if args.exchange == "p2p"
+                           else HaloExchange(s2, rank, world, f"cuda:{local}"))
+                if dist:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                if cell_arrays:
+                    s2.set_cell_coeffs_many(cell_arrays)
+                s2.upload(host_f)
+                if ex2 is None:
+                    s2.run(e_steps)
+                elif args.exchange == "p2p":
+                    run_steps_peer(s2, e_steps, depth)
+                else:
+                    run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
+                s2.download(out=host_out)
+                dt = time.perf_counter() - t0
+                skipped = s2.info()["skipped_items"]
+                if dist:  # no neighbour may still be storing into this slab's (IPC-mapped) memory
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                s2.close()
+                if dist:
+                    tt = torch.tensor([dt], device="cuda")
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    dt = float(tt.item())
+                return dt, skipped
+
+            dt, _ = run_e2e(False)
+            h2d = sum(a_.nbytes for a_ in host_f) + sum(a_.nbytes for a_ in cell_arrays.values())
+            d2h = sum(a_.nbytes for a_ in host_out)
+            e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
+                   "steps": e_steps, "wall_s": dt, "per_gpu_bytes": True,
+                   "path": "Simulation: set_cell_coeffs + upload (pinned host) -> run(config steps) -> "
+                           "download (pinned host)"}
+            if fs is None:  # zero initial fields + point source: the reference's quiescent skip applies
+                dq, skipped = run_e2e(True)
+                e2e_skip = {"value": cells_total * e_steps / dq / 1e9, "unit": UNIT, "wall_s": dq,
+                            "skipped_items": skipped,
+                            "note": "same e2e run with yb_set_quiescent_skip(1) (RunOptions::quiescent_skip, "
+                                    "runner.hpp:60-73): all-zero work items skipped, results bit-identical; "
+                                    "informational, not the headline"}
+        finally:
+            os.sched_setaffinity(0, affinity)
         e2e["host_cpus"] = f"{len(local_cpus)} CPUs of the GPU NUMA node" if local_cpus else "all (GPU NUMA node unknown)"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_rate(nx, ny, nz, budget_s=10.0)
+        cpu = cpu_baselines(nx, ny, nz, es, ss, budget_s=8.0)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

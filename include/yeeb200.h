@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define YB_ABI_VERSION 2
+#define YB_ABI_VERSION 3
 
 /* Status codes. The shim maps INVALID_ARGUMENT -> std::invalid_argument,
  * OUT_OF_RANGE -> std::out_of_range, the rest -> std::runtime_error. */
@@ -48,11 +48,12 @@ enum { YB_EX = 0, YB_EY, YB_EZ, YB_HX, YB_HY, YB_HZ };
 /* Per-cell coefficient selectors (extension; the reference has none). */
 enum { YB_CA = 0, YB_CB = 1, YB_DA = 2, YB_DB = 3 };
 
-/* Step implementations. */
+/* Step implementations. A zero-initialised yb_desc selects YB_VARIANT_TB2,
+ * the fastest path (ABI 3; ABI 2 had FUSED = 0 and TB2 = 2). */
 enum {
-  YB_VARIANT_FUSED = 0, /* one z-march sweep per step: TMA-staged planes, E+H fused */
+  YB_VARIANT_TB2 = 0,   /* temporal blocking: two full steps per sweep (odd remainder: FUSED) */
   YB_VARIANT_NAIVE = 1, /* one thread per DoF, separate E/PEC/source/H launches */
-  YB_VARIANT_TB2 = 2,   /* temporal blocking: two full steps per sweep (odd remainder: FUSED) */
+  YB_VARIANT_FUSED = 2, /* one z-march sweep per step: TMA-staged planes, E+H fused */
   YB_VARIANT_TB4 = 3    /* temporal blocking: four full steps per sweep (remainder: TB2 / FUSED);
                            single domain; the depth-8 point of the temporal-depth sweep */
 };
@@ -62,7 +63,7 @@ typedef struct yb_sim yb_sim;
 typedef struct {
   int nx, ny, nz; /* cells per axis (GridSpec, grid.hpp:17-43); nz = this slab's depth */
   int device;     /* CUDA device ordinal */
-  int variant;    /* YB_VARIANT_* */
+  int variant;    /* YB_VARIANT_* (0 = TB2, the default) */
   int zchunk;     /* fused: z planes per work item; 0 = auto */
   int z_offset;   /* z-slab mode: global index of local cell plane 0 (0 otherwise) */
   int nz_global;  /* z-slab mode: global cell count along z (0 = nz, single domain) */

@@ -350,7 +350,7 @@ struct RunOptions {
   std::vector<ProbeSpec> probes;
   bool quiescent_skip = true;  // skip all-zero work items (runner.hpp:60-73); results unchanged
   int device = 0;
-  int variant = YB_VARIANT_FUSED;
+  int variant = YB_VARIANT_TB2;
   std::function<void(const FieldSet<Real>&, long long)> after_step;
 };
 

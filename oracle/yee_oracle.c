@@ -51,9 +51,10 @@ static geo make_geo(const yo_state* s) {
 }
 
 #define AT(c, i, j, k) (((int64_t)(k) * g.e[c][1] + (j)) * g.e[c][0] + (i))
-#define CELL(i, j, k)                                                       \
-  (((int64_t)clampi(k, 0, g.nz - 1) * g.ny + clampi(j, 0, g.ny - 1)) * g.nx + \
-   clampi(i, 0, g.nx - 1))
+/* Per-cell coefficient index of DoF (i,j,k): the cell clamped into the grid.
+ * CROW is its (j,k) part, hoisted out of the i loops. */
+#define CROW(j, k) (((int64_t)clampi(k, 0, g.nz - 1) * g.ny + clampi(j, 0, g.ny - 1)) * g.nx)
+#define CELL(i, j, k) (CROW(j, k) + ((i) < g.nx ? (i) : g.nx - 1))
 
 /* kernels.hpp:18-20 / :27-44, over curl_updatable_box (staggering.hpp:70-77). */
 void yo_ampere(yo_state* s, const yo_coeffs* c, int nthreads) {
@@ -63,9 +64,10 @@ void yo_ampere(yo_state* s, const yo_coeffs* c, int nthreads) {
   /* ex: i in [0,nx), j in [1,ny), k in [1,nz) */
   OMP_FOR
   for (int k = 1; k < g.nz; ++k)
-    for (int j = 1; j < g.ny; ++j)
+    for (int j = 1; j < g.ny; ++j) {
+      const int64_t crow = CROW(j, k);
       for (int i = 0; i < g.nx; ++i) {
-        const int64_t cl = CELL(i, j, k);
+        const int64_t cl = crow + (i < g.nx ? i : g.nx - 1);
         const float A = c->ca ? c->ca[cl] : c->ca_s;
         const float C1 = c->cb ? c->cb[cl] : c->cdy[j];
         const float C2 = c->cb ? c->cb[cl] : c->cdz[k];
@@ -77,12 +79,14 @@ void yo_ampere(yo_state* s, const yo_coeffs* c, int nthreads) {
         const float inc = t1 - t2;
         ex[p] = A * ex[p] + inc;
       }
+    }
   /* ey: i in [1,nx), j in [0,ny), k in [1,nz) */
   OMP_FOR
   for (int k = 1; k < g.nz; ++k)
-    for (int j = 0; j < g.ny; ++j)
+    for (int j = 0; j < g.ny; ++j) {
+      const int64_t crow = CROW(j, k);
       for (int i = 1; i < g.nx; ++i) {
-        const int64_t cl = CELL(i, j, k);
+        const int64_t cl = crow + (i < g.nx ? i : g.nx - 1);
         const float A = c->ca ? c->ca[cl] : c->ca_s;
         const float C1 = c->cb ? c->cb[cl] : c->cdz[k];
         const float C2 = c->cb ? c->cb[cl] : c->cdx[i];
@@ -94,12 +98,14 @@ void yo_ampere(yo_state* s, const yo_coeffs* c, int nthreads) {
         const float inc = t1 - t2;
         ey[p] = A * ey[p] + inc;
       }
+    }
   /* ez: i in [1,nx), j in [1,ny), k in [0,nz) */
   OMP_FOR
   for (int k = 0; k < g.nz; ++k)
-    for (int j = 1; j < g.ny; ++j)
+    for (int j = 1; j < g.ny; ++j) {
+      const int64_t crow = CROW(j, k);
       for (int i = 1; i < g.nx; ++i) {
-        const int64_t cl = CELL(i, j, k);
+        const int64_t cl = crow + (i < g.nx ? i : g.nx - 1);
         const float A = c->ca ? c->ca[cl] : c->ca_s;
         const float C1 = c->cb ? c->cb[cl] : c->cdx[i];
         const float C2 = c->cb ? c->cb[cl] : c->cdy[j];
@@ -111,23 +117,31 @@ void yo_ampere(yo_state* s, const yo_coeffs* c, int nthreads) {
         const float inc = t1 - t2;
         ez[p] = A * ez[p] + inc;
       }
+    }
 }
 
-/* pec_boxes (staggering.hpp:81-86): every E DoF outside curl_updatable_box. */
+/* pec_boxes (staggering.hpp:81-86): every E DoF outside curl_updatable_box,
+ * i.e. the node planes idx[ax] == 0 and idx[ax] == n[ax] of each axis ax
+ * tangential to the component (the six outer faces; edges are visited
+ * twice, writing the same +0). */
 void yo_pec(yo_state* s) {
   const geo g = make_geo(s);
   const int n[3] = {g.nx, g.ny, g.nz};
   for (int c = 0; c < 3; ++c) {
     float* a = s->f[c];
-    for (int k = 0; k < g.e[c][2]; ++k)
-      for (int j = 0; j < g.e[c][1]; ++j)
-        for (int i = 0; i < g.e[c][0]; ++i) {
-          const int idx[3] = {i, j, k};
-          int inside = 1;
-          for (int ax = 0; ax < 3; ++ax)
-            if (ax != c && (idx[ax] == 0 || idx[ax] == n[ax])) inside = 0;
-          if (!inside) a[AT(c, i, j, k)] = 0.0f;
-        }
+    const int* e = g.e[c];
+    for (int ax = 0; ax < 3; ++ax) {
+      if (ax == c) continue;
+      for (int side = 0; side < 2; ++side) {
+        const int v = side ? n[ax] : 0;
+        int lo[3] = {0, 0, 0}, hi[3] = {e[0], e[1], e[2]};
+        lo[ax] = v;
+        hi[ax] = v + 1;
+        for (int k = lo[2]; k < hi[2]; ++k)
+          for (int j = lo[1]; j < hi[1]; ++j)
+            for (int i = lo[0]; i < hi[0]; ++i) a[AT(c, i, j, k)] = 0.0f;
+      }
+    }
   }
 }
 
@@ -139,9 +153,10 @@ void yo_faraday(yo_state* s, const yo_coeffs* c, int nthreads) {
   /* hx: (nx+1) x ny x nz */
   OMP_FOR
   for (int k = 0; k < g.nz; ++k)
-    for (int j = 0; j < g.ny; ++j)
+    for (int j = 0; j < g.ny; ++j) {
+      const int64_t crow = CROW(j, k);
       for (int i = 0; i <= g.nx; ++i) {
-        const int64_t cl = CELL(i, j, k);
+        const int64_t cl = crow + (i < g.nx ? i : g.nx - 1);
         const float A = c->da ? c->da[cl] : c->da_s;
         const float C1 = c->db ? c->db[cl] : c->cdz[k];
         const float C2 = c->db ? c->db[cl] : c->cdy[j];
@@ -153,12 +168,14 @@ void yo_faraday(yo_state* s, const yo_coeffs* c, int nthreads) {
         const float inc = t1 - t2;
         hx[p] = A * hx[p] + inc;
       }
+    }
   /* hy: nx x (ny+1) x nz */
   OMP_FOR
   for (int k = 0; k < g.nz; ++k)
-    for (int j = 0; j <= g.ny; ++j)
+    for (int j = 0; j <= g.ny; ++j) {
+      const int64_t crow = CROW(j, k);
       for (int i = 0; i < g.nx; ++i) {
-        const int64_t cl = CELL(i, j, k);
+        const int64_t cl = crow + (i < g.nx ? i : g.nx - 1);
         const float A = c->da ? c->da[cl] : c->da_s;
         const float C1 = c->db ? c->db[cl] : c->cdx[i];
         const float C2 = c->db ? c->db[cl] : c->cdz[k];
@@ -170,12 +187,14 @@ void yo_faraday(yo_state* s, const yo_coeffs* c, int nthreads) {
         const float inc = t1 - t2;
         hy[p] = A * hy[p] + inc;
       }
+    }
   /* hz: nx x ny x (nz+1) */
   OMP_FOR
   for (int k = 0; k <= g.nz; ++k)
-    for (int j = 0; j < g.ny; ++j)
+    for (int j = 0; j < g.ny; ++j) {
+      const int64_t crow = CROW(j, k);
       for (int i = 0; i < g.nx; ++i) {
-        const int64_t cl = CELL(i, j, k);
+        const int64_t cl = crow + (i < g.nx ? i : g.nx - 1);
         const float A = c->da ? c->da[cl] : c->da_s;
         const float C1 = c->db ? c->db[cl] : c->cdy[j];
         const float C2 = c->db ? c->db[cl] : c->cdx[i];
@@ -187,6 +206,7 @@ void yo_faraday(yo_state* s, const yo_coeffs* c, int nthreads) {
         const float inc = t1 - t2;
         hz[p] = A * hz[p] + inc;
       }
+    }
 }
 
 /* plan_standard (schedule.hpp:171-210); inject_current (source.hpp:61-68). */

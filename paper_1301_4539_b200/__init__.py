@@ -26,7 +26,8 @@ CSRC = os.path.join(HERE, "csrc")
 EX, EY, EZ, HX, HY, HZ = range(6)
 COMP_NAMES = ("ex", "ey", "ez", "hx", "hy", "hz")
 CA, CB, DA, DB = range(4)
-VARIANT_FUSED, VARIANT_NAIVE, VARIANT_TB2, VARIANT_TB4 = 0, 1, 2, 3
+ABI_VERSION = 3  # YB_ABI_VERSION of include/yeeb200.h
+VARIANT_TB2, VARIANT_NAIVE, VARIANT_FUSED, VARIANT_TB4 = 0, 1, 2, 3  # YB_VARIANT_* (TB2 = 0: the default)
 S_BITS = 0x3F1252DB
 S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt(3))
 
@@ -144,6 +145,8 @@ def lib():
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
         L.yb_halo_unpack.argtypes = [vp, C.c_int, vp]
+        if L.yb_abi_version() != ABI_VERSION:
+            raise YeeError(f"{LIB_PATH}: ABI {L.yb_abi_version()}, this module needs {ABI_VERSION} (rebuild)")
         _lib = L
     return _lib
 
@@ -183,7 +186,7 @@ class Simulation:
     (make_uniform_grid<float>(n, 1, 1, 0.99) + build_coefficients).
     """
 
-    def __init__(self, nx, ny, nz, device=0, variant=VARIANT_FUSED, zchunk=0, cdx=None, cdy=None,
+    def __init__(self, nx, ny, nz, device=0, variant=VARIANT_TB2, zchunk=0, cdx=None, cdy=None,
                  cdz=None, z_offset=0, nz_global=0):
         """nz_global > 0: this handle is the z-slab [z_offset, z_offset+nz) of a grid with
         nz_global cell planes (halo exchange: halo_pack / halo_unpack, see slabs.py)."""
@@ -454,7 +457,7 @@ def host_medium_slab(nx, ny, nz_global, z_offset, nplanes, eps_seed, sigma_seed,
 
 
 def run_simulation(nx, ny, nz, fields, nsteps, step0=0, sources=(), medium=None, cells=None,
-                   variant=VARIANT_FUSED, device=0):
+                   variant=VARIANT_TB2, device=0):
     """run_simulation (runner.hpp:349-362) mirror: copy the host state in, advance, copy out.
 
     medium=(eps_seed, sigma_seed) generates the pinned medium on the device;

@@ -14,6 +14,7 @@
 #include "../../include/yeeb200_inputs.h"
 #include "yb_device.cuh"
 #include "yb_launch.h"
+#include "yb_ptx.cuh"
 
 namespace yb {
 
@@ -232,17 +233,20 @@ __global__ void k_peer_signal(unsigned* f0, unsigned* f1, unsigned epoch) {
   if (f1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f1), "r"(epoch) : "memory");
 }
 
-__global__ void k_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err) {
-  for (long long it = 0;; ++it) {
+__global__ void k_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err,
+                            unsigned long long wait_ns) {
+  const unsigned long long t0 = globaltimer_ns();
+  for (;;) {
     unsigned a, b;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(a) : "l"(flags) : "memory");
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(b) : "l"(flags + 1) : "memory");
     if (a >= need0 && b >= need1) return;
-    if (it > (1ll << 27)) {  // ~15 s: the neighbour never signalled
-      atomicExch(err, 1);
+    if (globaltimer_ns() - t0 > wait_ns) {  // the neighbour never signalled: report, do not hang
+      const bool lo = a < need0;
+      wait_timed_out(err, WAIT_PEER, -1, lo ? 0 : 1, lo ? a : b, lo ? need0 : need1);
       return;
     }
-    __nanosleep(100);
+    __nanosleep(256);
   }
 }
 
@@ -402,8 +406,9 @@ cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned 
   return cudaGetLastError();
 }
 
-cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err, cudaStream_t st) {
-  k_peer_wait<<<1, 1, 0, st>>>(flags, need0, need1, err);
+cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err,
+                             unsigned long long wait_ns, cudaStream_t st) {
+  k_peer_wait<<<1, 1, 0, st>>>(flags, need0, need1, err, wait_ns);
   return cudaGetLastError();
 }
 

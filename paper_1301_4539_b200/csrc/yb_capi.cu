@@ -169,6 +169,8 @@ struct yb_sim {
   unsigned* qbits = nullptr;  // quiescent map (tiles x words)
   int qwords = 0, qtiles = 0;
   unsigned long long* qskipped = nullptr;  // device counter of skipped items
+  int* werr = nullptr;        // wait-error record of the bounded spin waits (yb::WaitErr, 8 ints)
+  unsigned long long wait_ns = 20000000000ull;  // their deadline (YB_WAIT_TIMEOUT_MS, default 20 s)
 };
 
 namespace {
@@ -530,7 +532,8 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
   unsigned long long* sc = s->on_side ? s->sched2 : s->sched;
   unsigned long long& base = s->on_side ? s->sched2_base : s->sched_base;
   a.nsweeps = nsweeps;
-  a.err = reinterpret_cast<int*>(s->sched) + 6;
+  a.err = s->werr;
+  a.wait_ns = s->wait_ns;
   if (s->peer_stores) {  // MODE 3: boundary planes straight into the neighbours' (same-parity) buffers
     for (int c = 0; c < 6; ++c) {
       a.pdn[c] = s->peer[0].on ? s->peer[0].buf[nxt][c] : nullptr;
@@ -569,7 +572,7 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
       a.pcnt = s->pflags + 4;
       a.pcnt_base[0] = s->pcnt_base[0];
       a.pcnt_base[1] = s->pcnt_base[1];
-      a.perr = reinterpret_cast<int*>(s->pflags + 2);
+      a.perr = s->werr;
       if (s->peer[0].on) s->pcnt_base[0] += (unsigned)T * yb::kTB2RowWarps;  // every row warp counts
       if (s->peer[1].on) s->pcnt_base[1] += (unsigned)T * yb::kTB2RowWarps;
     } else {
@@ -853,6 +856,13 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (cudaMalloc(&s->sched, 4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemsetAsync(s->sched, 0, 4 * sizeof(unsigned long long), s->stream) != cudaSuccess)
     return bail(fail(YB_CUDA_ERROR, "scheduler counter alloc failed"));
+  if (cudaMalloc(&s->werr, 8 * sizeof(int)) != cudaSuccess ||
+      cudaMemsetAsync(s->werr, 0, 8 * sizeof(int), s->stream) != cudaSuccess)
+    return bail(fail(YB_CUDA_ERROR, "wait-error record alloc failed"));
+  if (const char* w = std::getenv("YB_WAIT_TIMEOUT_MS")) {
+    const long long ms = std::atoll(w);
+    if (ms > 0) s->wait_ns = (unsigned long long)ms * 1000000ull;
+  }
   if (int rc = upload_axis(s)) return bail(rc);
   static bool limits_set = false;
   if (!limits_set) {
@@ -879,6 +889,7 @@ int yb_destroy(yb_sim* s) {
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
   cudaFree(s->sched2);
+  cudaFree(s->werr);
   if (s->side) cudaStreamDestroy(s->side);
   if (s->xfer) cudaStreamDestroy(s->xfer);
   if (s->cflags) cudaFree(s->cflags);
@@ -998,28 +1009,16 @@ static int cell_finish(yb_sim* s, int which, const float* cells, bool all_equal,
 
 int yb_set_cell_coeffs(yb_sim* s, int which, const float* cells, float uniform) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
-  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   if (which < 0 || which > 3) return fail(YB_INVALID_ARGUMENT, "coefficient selector %d", which);
+  if (cells) return yb_set_cell_coeffs_n(s, 1, &which, &cells);
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   YB_CU(cudaSetDevice(s->device));
-  bool all_equal = false;
-  float v = uniform;
-  // staging: the spare state buffer from its allocation start (see copy_dense)
-  float* stage = s->buf[s->cur ^ 1][0] - yb::kGhost * s->g.plane;
-  if (cells) {
-    int* flag = reinterpret_cast<int*>(s->sched) + 2;  // scratch word next to the work counter
-    if (int rc = cell_stage(s, cells, cell_count(s), stage, flag)) return rc;
-    int same = 0;
-    YB_CU(cudaMemcpyAsync(&same, flag, 4, cudaMemcpyDeviceToHost, s->stream));
-    YB_CU(cudaStreamSynchronize(s->stream));
-    all_equal = same != 0;
-    v = cells[0];
-  }
-  return cell_finish(s, which, cells, all_equal, v, stage);
+  return cell_finish(s, which, nullptr, false, uniform, nullptr);
 }
 
 int yb_set_cell_coeffs_n(yb_sim* s, int n, const int* which, const float* const* cells) {
-  if (!s || (n > 0 && (!which || !cells))) return fail(YB_INVALID_ARGUMENT, "null argument");
-  if (n < 0 || n > 4) return fail(YB_INVALID_ARGUMENT, "1 .. 4 arrays");
+  if (!s || !which || !cells) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (n < 1 || n > 4) return fail(YB_INVALID_ARGUMENT, "1 .. 4 arrays (got %d)", n);
   if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
   for (int i = 0; i < n; ++i) {
     if (which[i] < 0 || which[i] > 3 || !cells[i]) return fail(YB_INVALID_ARGUMENT, "bad array %d", i);
@@ -1028,18 +1027,40 @@ int yb_set_cell_coeffs_n(yb_sim* s, int n, const int* which, const float* const*
   }
   YB_CU(cudaSetDevice(s->device));
   if (!s->cflags) YB_CU(cudaMalloc(&s->cflags, 4 * sizeof(int)));
-  // all copies back to back (one spare state buffer each), then one sync
-  float* stage[4];
+  // Staging: the spare state buffers from their allocation start (see
+  // copy_dense; re-zeroed after use). With peer links the neighbours may be
+  // storing into this handle's spare buffer's ghost planes, so each array
+  // goes through a scratch allocation instead.
+  const bool scratch = s->peer[0].on || s->peer[1].on;
+  float* stage[4] = {};
+  auto cleanup = [&](int rc) {
+    for (int i = 0; i < n; ++i) {
+      if (!stage[i]) continue;
+      if (scratch)
+        cudaFree(stage[i]);
+      else if (rc != YB_OK)  // an error left staged data behind: restore the +0 invariant
+        cudaMemsetAsync(stage[i], 0, (size_t)s->g.total * 4, s->stream);
+    }
+    if (rc != YB_OK || scratch) cudaStreamSynchronize(s->stream);
+    return rc;
+  };
+  // all copies back to back, then one sync for the uniformity checks
   for (int i = 0; i < n; ++i) {
-    stage[i] = s->buf[s->cur ^ 1][i] - yb::kGhost * s->g.plane;
-    if (int rc = cell_stage(s, cells[i], cell_count(s), stage[i], s->cflags + i)) return rc;
+    if (scratch) {
+      if (cudaMalloc(&stage[i], (size_t)s->g.total * 4) != cudaSuccess)
+        return cleanup(fail(YB_CUDA_ERROR, "coefficient staging buffer: cudaMalloc failed"));
+    } else {
+      stage[i] = s->buf[s->cur ^ 1][i] - yb::kGhost * s->g.plane;
+    }
+    if (int rc = cell_stage(s, cells[i], cell_count(s), stage[i], s->cflags + i)) return cleanup(rc);
   }
   int same[4] = {0, 0, 0, 0};
-  if (n > 0) YB_CU(cudaMemcpyAsync(same, s->cflags, n * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-  YB_CU(cudaStreamSynchronize(s->stream));
+  if (cudaMemcpyAsync(same, s->cflags, n * sizeof(int), cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+      cudaStreamSynchronize(s->stream) != cudaSuccess)
+    return cleanup(fail(YB_CUDA_ERROR, "coefficient uniformity check failed"));
   for (int i = 0; i < n; ++i)
-    if (int rc = cell_finish(s, which[i], cells[i], same[i] != 0, cells[i][0], stage[i])) return rc;
-  return YB_OK;
+    if (int rc = cell_finish(s, which[i], cells[i], same[i] != 0, cells[i][0], stage[i])) return cleanup(rc);
+  return cleanup(YB_OK);
 }
 
 int yb_generate_medium(yb_sim* s, int64_t eps_seed, int64_t sigma_seed) {
@@ -1533,21 +1554,37 @@ int yb_read_probes(yb_sim* s, int64_t* steps, int* probe, float* values, int64_t
   return YB_OK;
 }
 
+// Reports (and clears) the record of a spin wait that passed its deadline.
+static int check_wait_error(yb_sim* s) {
+  int r[8] = {};
+  YB_CU(cudaMemcpy(r, s->werr, sizeof r, cudaMemcpyDeviceToHost));
+  if (r[0] == 0) return YB_OK;
+  YB_CU(cudaMemset(s->werr, 0, sizeof r));
+  const double ms = (double)s->wait_ns * 1e-6;
+  if (r[0] == yb::WAIT_DEP) {
+    const int T = s->ntx * s->nty, ch = r[1] / T, tile = r[1] % T;
+    return fail(YB_RUNTIME_ERROR,
+                "multi-sweep launch: work item %d (tile x=%d y=%d, z-chunk %d) of sweep %d waited more than "
+                "%.0f ms for its neighbourhood (completion count %u, needed %u)",
+                r[1], tile % s->ntx, tile / s->ntx, ch, r[2], ms, (unsigned)r[3], (unsigned)r[4]);
+  }
+  const char* side = r[2] == 0 ? "below" : "above";
+  if (r[0] == yb::WAIT_PEER_KERNEL)
+    return fail(YB_RUNTIME_ERROR,
+                "peer-store sweep: boundary work item %d waited more than %.0f ms for the slab %s "
+                "(flag %u, needed %u: that neighbour never signalled)",
+                r[1], ms, side, (unsigned)r[3], (unsigned)r[4]);
+  return fail(YB_RUNTIME_ERROR,
+              "peer halo wait: more than %.0f ms for the slab %s (flag %u, needed %u: that neighbour never signalled)",
+              ms, side, (unsigned)r[3], (unsigned)r[4]);
+}
+
 int yb_synchronize(yb_sim* s) {
   if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
   YB_CU(cudaSetDevice(s->device));
   YB_CU(cudaStreamSynchronize(s->stream));
   if (s->peer_stream) YB_CU(cudaStreamSynchronize(s->peer_stream));
-  if (s->pflags) {
-    int err = 0;
-    YB_CU(cudaMemcpy(&err, s->pflags + 2, sizeof err, cudaMemcpyDeviceToHost));
-    if (err) return fail(YB_RUNTIME_ERROR, "peer halo wait timed out (a neighbour never signalled)");
-  }
-  {
-    int err = 0;
-    YB_CU(cudaMemcpy(&err, reinterpret_cast<int*>(s->sched) + 6, sizeof err, cudaMemcpyDeviceToHost));
-    if (err) return fail(YB_RUNTIME_ERROR, "a multi-sweep launch timed out waiting for a dependency");
-  }
+  if (int rc = check_wait_error(s)) return rc;
   return collect_timers(s);
 }
 
@@ -1857,7 +1894,15 @@ int yb_peer_wait(yb_sim* s) {
     s->peer_inflight = false;
   }
   YB_CU(yb::launch_peer_wait(s->pflags, s->peer[0].on ? s->push_count : 0u, s->peer[1].on ? s->push_count : 0u,
-                             reinterpret_cast<int*>(s->pflags + 2), s->stream));
+                             s->werr, s->wait_ns, s->stream));
+  if (s->qskip && s->q_valid) {  // the neighbours stored my ghost planes: mark their nonzero tile-planes
+    const int d = halo_depth(s);  // (yb_halo_unpack does the same for the NCCL transport)
+    if (s->peer[0].on)
+      YB_CU(yb::launch_qscan(s->g, fields_of(s, 0), fields_of(s, 1), qmap_of(s), -d, -1, s->stream));
+    if (s->peer[1].on)
+      YB_CU(yb::launch_qscan(s->g, fields_of(s, 0), fields_of(s, 1), qmap_of(s), s->g.nz, s->g.nz + d - 1,
+                             s->stream));
+  }
   return YB_OK;
 }
 

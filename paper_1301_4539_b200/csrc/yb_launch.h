@@ -90,7 +90,8 @@ struct FusedArgs {
   unsigned* done;                // per-item completion epochs
   unsigned epoch;
   const SrcArgs* srcs;           // per-sweep sources (nsweeps > 1)
-  int* err;                      // set when a dependency wait timed out
+  int* err;                      // wait-error record (WaitErr) of a timed-out dependency wait
+  unsigned long long wait_ns;    // deadline of every spin wait of this launch (ns of globaltimer)
   // Peer-store mode (two-step kernel MODE 3, z-slabs over peer memory): the
   // boundary planes 0,1 / nz-2,nz-1 this launch writes also go straight into
   // the neighbours' ghost planes pdn_k0 + {0,1} / {-2,-1} of the same-parity
@@ -114,8 +115,15 @@ struct FusedArgs {
   unsigned* psig[2];
   unsigned* pcnt;                // per side: boundary items completed (monotonic)
   unsigned pcnt_base[2];         // their values at this launch's start
-  int* perr;                     // set when a wait timed out
+  int* perr;                     // wait-error record of a timed-out neighbour wait
 };
+
+// Wait-error record, 8 ints per handle: [0] code (0 none; WAIT_DEP: a
+// multi-sweep item waited for its neighbourhood; WAIT_PEER_KERNEL: the
+// folded peer wait of a boundary item; WAIT_PEER: the separate peer-wait
+// launch), [1] item (-1 if none), [2] sweep / side, [3] counter value seen,
+// [4] value needed.
+enum { WAIT_DEP = 1, WAIT_PEER_KERNEL = 2, WAIT_PEER = 3 };
 
 // planes [kz0, kz1) of z-chunk c of a launch
 __device__ __forceinline__ void chunk_planes(const FusedArgs& a, int c, int& kz0, int& kz1) {
@@ -190,9 +198,10 @@ struct PeerCopy {
 };
 cudaError_t launch_peer_copy(const Geo& g, const PeerCopy& down, const PeerCopy& up, cudaStream_t st);
 cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned epoch, cudaStream_t st);
-// Spins (bounded, ~seconds) until flags[0] >= need0 and flags[1] >= need1;
-// on timeout sets *err = 1.
-cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err, cudaStream_t st);
+// Spins until flags[0] >= need0 and flags[1] >= need1, at most wait_ns of
+// device time; on timeout fills the wait-error record `err` (WAIT_PEER).
+cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err,
+                             unsigned long long wait_ns, cudaStream_t st);
 // Halo planes <-> a contiguous exchange buffer: plane q of the list is
 // src[q] (or dst[q]) = one padded plane (PX*PY floats); ext holds them in order.
 struct HaloList {

@@ -127,5 +127,26 @@ namespace {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+
+// Device wall clock (ns) for the deadlines of the bounded spin waits.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// A spin wait passed its deadline: the first one to time out fills the
+// handle's wait-error record (WaitErr in yb_launch.h); the host reports it.
+__device__ __forceinline__ void wait_timed_out(int* rec, int code, int item, int sweep, unsigned seen,
+                                               unsigned need) {
+  if (atomicCAS(rec, 0, -1) == 0) {
+    rec[1] = item;
+    rec[2] = sweep;
+    rec[3] = (int)seen;
+    rec[4] = (int)need;
+    __threadfence();
+    atomicExch(rec, code);
+  }
+}
 }  // namespace
 }  // namespace yb

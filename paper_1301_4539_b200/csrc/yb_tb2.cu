@@ -191,18 +191,22 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   const int x_lo = max(tx - 1, 0), x_hi = min(tx + 1, a.ntx - 1);
   // every row warp of an item counts itself in done[item] once per sweep
   const unsigned need = (a.epoch + (unsigned)sw) * (unsigned)RW;
+  unsigned long long t0 = 0;
   for (long long n = 0;; ++n) {  // one pass of independent relaxed loads, then acquire
     bool ok = true;
+    unsigned low = need;  // the smallest count seen (for the error record)
     for (int cc = c_lo; cc <= c_hi; ++cc)
       for (int yy = y_lo; yy <= y_hi; ++yy)
         for (int xx = x_lo; xx <= x_hi; ++xx) {
           unsigned v;
           asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.done + (cc * T + yy * a.ntx + xx)));
           ok &= (int)(v - need) >= 0;
+          if ((int)(v - low) < 0) low = v;
         }
     if (ok) break;
-    if (n > (1ll << 22)) {  // ~1 s: report instead of hanging
-      atomicExch(a.err, 1);
+    if (n == 0) t0 = globaltimer_ns();
+    else if (globaltimer_ns() - t0 > a.wait_ns) {  // report the stuck item instead of hanging
+      wait_timed_out(a.err, WAIT_DEP, item, sw, low, need);
       break;
     }
     __nanosleep(128);
@@ -210,14 +214,18 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-// MODE 3 (folded exchange): spin, bounded, until a neighbour's flag word reaches need.
-__device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, int* err) {
+// MODE 3 (folded exchange): spin, bounded by the launch's deadline, until a
+// neighbour's flag word reaches need.
+__device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, int* err, unsigned long long wait_ns,
+                                            int item, int side) {
+  unsigned long long t0 = 0;
   for (long long n = 0;; ++n) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
     if ((int)(v - need) >= 0) return;
-    if (n > (1ll << 27)) {  // ~15 s: the neighbour never signalled
-      atomicExch(err, 1);
+    if (n == 0) t0 = globaltimer_ns();
+    else if (globaltimer_ns() - t0 > wait_ns) {  // the neighbour never signalled
+      wait_timed_out(err, WAIT_PEER_KERNEL, item, side, v, need);
       return;
     }
     __nanosleep(100);
@@ -728,8 +736,8 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
             const int ch = a.pfold == 2 ? q : (q == 0 ? 0 : (q == 1 ? nch - 1 : q - 1));
             it = ch * T + tile;
             const bool wd = ch == 0 && a.pdn[0], wu = ch == nch - 1 && a.pup[0];
-            if (wd) peer_flag_wait(a.pflag, a.pneed, a.perr);
-            if (wu) peer_flag_wait(a.pflag + 1, a.pneed, a.perr);
+            if (wd) peer_flag_wait(a.pflag, a.pneed, a.perr, a.wait_ns, it, 0);
+            if (wu) peer_flag_wait(a.pflag + 1, a.pneed, a.perr, a.wait_ns, it, 1);
             if (wd || wu) asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
           }
         } else if (v < (unsigned long long)a.nitems * a.nsweeps) {

@@ -32,7 +32,8 @@ def assert_bits(a, b, what=""):
                                  f"{y[tuple(v[0] for v in bad)]}"
 
 
-VARIANTS = [0, 1, 2]  # fused, naive, two-step temporal blocking
+TB2, NAIVE, FUSED, TB4 = 0, 1, 2, 3  # include/yeeb200.h YB_VARIANT_* (ABI 3)
+VARIANTS = [FUSED, NAIVE, TB2]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -158,7 +159,7 @@ CASES = {
 def test_configs_vs_oracle(yb, oracle, name, variant, monkeypatch):
     if variant == "tb2_one_sweep_per_launch":  # the two-step kernel without multi-sweep launches
         monkeypatch.setenv("YB_TB2_PERSIST", "0")
-        variant = 2
+        variant = yb.VARIANT_TB2
     nx, ny, nz, steps, es, ss, fs, has_src = CASES[name]
     src = None
     if has_src and nx > 2 and ny > 2 and nz > 2:
@@ -179,7 +180,7 @@ def test_configs_vs_oracle(yb, oracle, name, variant, monkeypatch):
     assert_bits(got, want, name)
 
 
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [FUSED, TB2])
 @pytest.mark.parametrize("shape,zchunk", [((40, 24, 30), 1), ((40, 24, 30), 3), ((40, 24, 30), 7),
                                           ((40, 24, 30), 64), ((200, 64, 40), 2), ((130, 40, 33), 1),
                                           ((256, 96, 21), 4)])
@@ -422,7 +423,7 @@ def test_energy_slabs_sum(yb, oracle):
     assert abs(want - oracle.total_energy(nx, ny, nzg, f, prev[3:], dz=dz)) <= 1e-12 * abs(want)
 
 
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [FUSED, TB2])
 @pytest.mark.parametrize("shape,zchunk,medium", [((136, 72, 40), 4, (4, -1)), ((200, 40, 33), 0, (-1, -1)),
                                                  ((64, 48, 40), 3, (2, 2)), ((37, 29, 23), 0, (7, 7))])
 def test_quiescent_skip_bit_exact(yb, oracle, variant, shape, zchunk, medium):
@@ -451,7 +452,7 @@ def test_quiescent_skip_bit_exact(yb, oracle, variant, shape, zchunk, medium):
     assert_bits(outs[1], want, "skip vs oracle")
 
 
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [FUSED, TB2])
 def test_quiescent_skip_stale_buffers(yb, oracle, variant):
     """After a run leaves nonzero state in both buffers, an upload of a mostly
     zero state must rebuild the quiescent map (both buffers are scanned): the
@@ -481,7 +482,7 @@ def test_quiescent_skip_slabs(yb, oracle):
     nx, ny, nzg, steps = 136, 40, 29, 11
     tab = oracle.gauss_table(steps, t0=3.0, w=2.0)
     src = (2, 60, 20, 13, tab)
-    for variant in (0, 2):
+    for variant in (FUSED, TB2):
         sims = []
         for z0, n in partition(nzg, 3):
             s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant)
@@ -583,7 +584,7 @@ def test_multi_sweep_launches(yb, oracle, name, zchunk, monkeypatch):
     assert_bits(got, want, name)
 
 
-@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("variant", [FUSED, TB2, TB4])
 def test_uniform_non_unit_ca_da(yb, oracle, variant):
     """A uniform Ca / Da other than 1 (yb_set_cell_coeffs(which, NULL, v)):
     stored as a full array (the sweep kernels treat 'no array' as exactly 1)."""

@@ -26,6 +26,7 @@ def test_partition():
         partition(3, 4)
 
 
+TB2, FUSED = 0, 2  # include/yeeb200.h YB_VARIANT_* (ABI 3)
 CASE = dict(nx=13, ny=11, nzg=17, steps=9, medium=(7, 7), fseed=8)
 
 
@@ -163,7 +164,7 @@ class _DeviceExchange:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [FUSED, TB2])
 @pytest.mark.parametrize("nranks,medium,fseed,src,upload", [(2, (7, 7), 8, True, False),
                                                             (3, (4, -1), None, True, False),
                                                             (4, (-1, -1), 5, False, False),
@@ -192,7 +193,7 @@ def test_gpu_slabs_bit_exact(yb, oracle, nranks, medium, fseed, src, variant, up
         sims.append(s)
     ex = _DeviceExchange(sims)
     depth = sims[0].info()["halo_depth"]
-    assert depth == (2 if variant == 2 else 1)
+    assert depth == (2 if variant == yb.VARIANT_TB2 else 1)
     done = 0
     while done < steps:
         n = min(depth, steps - done)
@@ -223,7 +224,7 @@ def test_gpu_slabs_bit_exact(yb, oracle, nranks, medium, fseed, src, variant, up
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [FUSED, TB2])
 def test_gpu_slabs_stream_ordered(yb, oracle, variant):
     """Slabs on a shared caller stream: halo pack/unpack are stream-ordered
     (no host synchronisation between sweeps and exchanges) — same result."""
@@ -287,7 +288,7 @@ class _DeviceExchangeSplit(_DeviceExchange):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant,nranks,nzg", [(0, 3, 29), (2, 3, 29), (2, 2, 12), (2, 4, 23), (0, 2, 5)])
+@pytest.mark.parametrize("variant,nranks,nzg", [(FUSED, 3, 29), (TB2, 3, 29), (TB2, 2, 12), (TB2, 4, 23), (FUSED, 2, 5)])
 def test_gpu_slabs_split_sweeps(yb, oracle, variant, nranks, nzg):
     """Split sweeps (yb_advance_begin / yb_advance_end: boundary planes first,
     exchange, interior) give the single-domain result bit for bit, including
@@ -338,7 +339,7 @@ def test_gpu_slabs_split_sweeps(yb, oracle, variant, nranks, nzg):
 
 @pytest.mark.gpu
 def test_split_sweep_errors(yb):
-    with yb.Simulation(40, 16, 10, z_offset=0, nz_global=20, variant=0) as s:
+    with yb.Simulation(40, 16, 10, z_offset=0, nz_global=20, variant=yb.VARIANT_FUSED) as s:
         with pytest.raises(yb.YeeInvalidArgument):
             s.advance_begin(2)  # the one-step kernel: depth 1
         with pytest.raises(yb.YeeInvalidArgument):
@@ -357,7 +358,7 @@ def test_split_sweep_errors(yb):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant,nranks,nzg", [(2, 3, 29), (0, 3, 29), (2, 2, 12), (2, 4, 23)])
+@pytest.mark.parametrize("variant,nranks,nzg", [(TB2, 3, 29), (FUSED, 3, 29), (TB2, 2, 12), (TB2, 4, 23)])
 def test_gpu_slabs_peer_push(yb, oracle, variant, nranks, nzg):
     """Direct peer-memory halo push (yb_peer_link within one process, one GPU):
     push / wait / split sweeps enqueued slab after slab on one stream, so every
@@ -416,6 +417,66 @@ def test_gpu_slabs_peer_push(yb, oracle, variant, nranks, nzg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("variant", [FUSED, TB2])
+def test_gpu_slabs_peer_quiescent_skip(yb, oracle, variant):
+    """Peer-memory exchange with the quiescent skip on: the neighbours' stores
+    into a slab's ghost planes must reach its quiescent map (yb_peer_wait
+    rescans them), else a boundary item whose only nonzero input came from
+    the neighbour is skipped and the wave never enters the slab. Zero fields
+    and one point source in the bottom slab: every other slab starts all-zero
+    and only the exchange can wake it. Bit-exact against one domain."""
+    nx, ny, nzg, nranks, steps = 136, 40, 30, 3, 24
+    tab = oracle.gauss_table(steps)
+    src = (2, nx // 2, ny // 2, 6, tab)
+    sims = []
+    for z0, n in partition(nzg, nranks):
+        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, variant=variant, zchunk=3)
+        s.generate_medium(7, -1)
+        s.add_source(*src)
+        s.set_quiescent_skip(True)
+        sims.append(s)
+    st = torch.cuda.Stream()
+    for s in sims:
+        s.set_stream(st.cuda_stream)
+    for lo, hi in zip(sims[:-1], sims[1:]):
+        lo.peer_link(1, hi)
+        hi.peer_link(0, lo)
+    depth = sims[0].info()["halo_depth"]
+    for s in sims:
+        s.peer_push(False)
+    done = 0
+    while done < steps:
+        n = min(depth, steps - done)
+        for s in sims:
+            s.peer_wait()
+            s.advance_begin(n)
+        for s in sims:
+            s.peer_push(False)
+        for s in sims:
+            s.advance_end()
+        done += n
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in sims:
+        s.synchronize()
+        d = s.download()
+        at_top = s.z_offset + s.nz == nzg
+        for c in range(6):
+            k = s.nz + (1 if c in (0, 1, 5) and at_top else 0)
+            out[c][s.z_offset:s.z_offset + k] = d[c][:k]
+    assert sims[0].info()["skipped_items"] > 0  # the skip was active
+    for s in sims:
+        s.close()
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(7, -1)
+        one.add_source(*src)
+        one.run(steps)
+        want = one.download()
+    assert any(np.any(out[c][20:] != 0) for c in range(6))  # the wave reached the top slab
+    for c in range(6):
+        assert bits_equal(out[c], want[c]), c
+
+
+@pytest.mark.gpu
 def test_peer_errors(yb):
     with yb.Simulation(40, 16, 10) as one:
         with pytest.raises(yb.YeeInvalidArgument):
@@ -434,7 +495,7 @@ def test_peer_errors(yb):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("fold", [True, False])
-@pytest.mark.parametrize("variant,nranks,nzg,steps", [(2, 3, 29, 11), (2, 2, 12, 10), (2, 4, 23, 9), (0, 3, 29, 7),
+@pytest.mark.parametrize("variant,nranks,nzg,steps", [(TB2, 3, 29, 11), (TB2, 2, 12, 10), (TB2, 4, 23, 9), (FUSED, 3, 29, 7),
                                                        (2, 3, 150, 8)])
 def test_gpu_slabs_peer_step(yb, oracle, monkeypatch, fold, variant, nranks, nzg, steps):
     """Exchange fused into the sweep (yb_peer_step): the two-step kernel stores
@@ -547,7 +608,7 @@ def _ipc_worker(rank, world, port, result_path, variant, steps):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant,world,steps", [(2, 2, 10), (2, 3, 9), (0, 2, 5)])
+@pytest.mark.parametrize("variant,world,steps", [(TB2, 2, 10), (TB2, 3, 9), (FUSED, 2, 5)])
 def test_gpu_ipc_peer_exchange(yb, oracle, tmp_path, variant, world, steps):
     """The cross-process path of --exchange p2p: IPC handles exchanged over
     gloo, opened with cudaIpcOpenMemHandle, then yb_peer_step per period (the

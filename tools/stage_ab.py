@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) > 1:
     import paper_1301_4539_b200 as yb
     n = int(sys.argv[1])
-    with yb.Simulation(n, n, n, variant=2) as s:
+    with yb.Simulation(n, n, n, variant=yb.VARIANT_TB2) as s:
         s.fill(3)
         s.run(8)
         s.synchronize()
