@@ -278,6 +278,36 @@ int yb_peer_step(yb_sim* sim, int64_t nsteps);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
 
+/* Per-box operations on a caller's FieldSet<Real> held in HOST memory: the
+ * reference's free functions, for either precision (the reference is
+ * templated on Real; its own unit tests run in double). The components the
+ * operation reads are copied to device `device`, it runs as per-DoF kernels
+ * in the reference's operand order (bit-identical in fp32 and fp64), and the
+ * components it writes are copied back. No handle; synchronous. For the
+ * device-resident fp32 time loop use a yb_sim handle instead.
+ *   dense6: Ex..Hz arrays (dense Array3 layout, element type dtype)
+ *   cd3:    Coefficients cdx[nx], cdy[ny], cdz[nz] (dtype; unused by ZERO / PEC)
+ *   box:    {xlo,xhi,ylo,yhi,zlo,zhi} (IndexBox; unused by PEC)
+ *   op:     YB_OP_UPDATE_E  update_e_box(f, c, comp, box)   kernels.hpp:78-88
+ *           YB_OP_UPDATE_H  update_h_box(f, c, comp, box)   kernels.hpp:92-101
+ *           YB_OP_ZERO      zero_box(f, comp, box)          kernels.hpp:104-111
+ *           YB_OP_AMPERE    apply_ampere_range(f, c, box)   kernels.hpp:129-135
+ *           YB_OP_FARADAY   apply_faraday_range(f, c, box)  kernels.hpp:138-144
+ *           YB_OP_PEC       apply_pec_boundary(f)           kernels.hpp:147-155
+ * Boxes outside the ranges the reference accepts -> YB_OUT_OF_RANGE with the
+ * reference's message. */
+enum { YB_F32 = 0, YB_F64 = 1 };
+enum { YB_OP_UPDATE_E = 0, YB_OP_UPDATE_H, YB_OP_ZERO, YB_OP_AMPERE, YB_OP_FARADAY, YB_OP_PEC };
+int yb_fs_apply(int device, int dtype, int nx, int ny, int nz, void* const* dense6, const void* const* cd3, int op,
+                int comp, const int* box);
+/* total_energy(g, f, prev_h) (fields.hpp:116-146) of a host FieldSet and
+ * HSnapshot (prev_h3 = Hx, Hy, Hz), spacings dx/dy/dz (NULL = 1), double
+ * accumulation on the device (deterministic; summation order differs from
+ * the reference's serial loop). */
+int yb_fs_total_energy(int device, int dtype, int nx, int ny, int nz, const void* const* dense6,
+                       const void* const* prev_h3, const double* dx, const double* dy, const double* dz,
+                       double* energy);
+
 /* Work on a caller-owned stream (e.g. torch.cuda.current_stream()); NULL
  * restores the handle's own stream. */
 int yb_set_stream(yb_sim* sim, void* cuda_stream);

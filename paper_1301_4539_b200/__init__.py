@@ -43,6 +43,7 @@ ABI_SYMBOLS = (
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
     "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
     "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait", "yb_peer_step",
+    "yb_fs_apply", "yb_fs_total_energy",
 )
 
 
@@ -145,6 +146,9 @@ def lib():
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
         L.yb_halo_unpack.argtypes = [vp, C.c_int, vp]
+        L.yb_fs_apply.argtypes = [C.c_int] * 5 + [C.POINTER(vp), C.POINTER(vp), C.c_int, C.c_int,
+                                                   C.POINTER(C.c_int)]
+        L.yb_fs_total_energy.argtypes = [C.c_int] * 5 + [C.POINTER(vp)] * 2 + [C.POINTER(C.c_double)] * 4
         if L.yb_abi_version() != ABI_VERSION:
             raise YeeError(f"{LIB_PATH}: ABI {L.yb_abi_version()}, this module needs {ABI_VERSION} (rebuild)")
         _lib = L
@@ -418,6 +422,40 @@ class Simulation:
         i = Info()
         _check(lib().yb_get_info(self._h, C.byref(i)))
         return i.as_dict()
+
+
+OP_UPDATE_E, OP_UPDATE_H, OP_ZERO, OP_AMPERE, OP_FARADAY, OP_PEC = range(6)
+
+
+def fs_apply(fields, cd, op, comp=0, box=None, device=0):
+    """A per-box operation on a host FieldSet (six dense float32 or float64
+    arrays, updated in place): the reference's free functions
+    update_e_box / update_h_box / zero_box / apply_ampere_range /
+    apply_faraday_range / apply_pec_boundary (kernels.hpp:78-155) run on the
+    device. cd = (cdx, cdy, cdz) in the same dtype."""
+    dt = fields[0].dtype
+    assert dt in (np.float32, np.float64) and all(a.dtype == dt and a.flags.c_contiguous for a in fields)
+    nz, ny, nx = fields[0].shape[0] - 1, fields[0].shape[1] - 1, fields[0].shape[2]  # ex: nx x (ny+1) x (nz+1)
+    cds = [np.ascontiguousarray(a, dt) for a in cd] if cd is not None else None
+    f6 = (C.c_void_p * 6)(*[a.ctypes.data for a in fields])
+    c3 = (C.c_void_p * 3)(*[a.ctypes.data for a in cds]) if cds is not None else None
+    b = (C.c_int * 6)(*box) if box is not None else None
+    _check(lib().yb_fs_apply(device, 0 if dt == np.float32 else 1, nx, ny, nz, f6, c3, op, comp, b))
+    return fields
+
+
+def fs_total_energy(fields, prev_h, dx=None, dy=None, dz=None, device=0):
+    """total_energy (fields.hpp:116-146) of a host FieldSet and an H snapshot, on the device."""
+    dt = fields[0].dtype
+    nz, ny, nx = fields[0].shape[0] - 1, fields[0].shape[1] - 1, fields[0].shape[2]
+    f6 = (C.c_void_p * 6)(*[a.ctypes.data for a in fields])
+    p3 = (C.c_void_p * 3)(*[a.ctypes.data for a in prev_h])
+    ds = [None if d is None else np.ascontiguousarray(d, np.float64) for d in (dx, dy, dz)]
+    ptr = [None if d is None else d.ctypes.data_as(C.POINTER(C.c_double)) for d in ds]
+    out = C.c_double()
+    _check(lib().yb_fs_total_energy(device, 0 if dt == np.float32 else 1, nx, ny, nz, f6, p3, *ptr,
+                                    C.byref(out)))
+    return out.value
 
 
 def host_medium(nx, ny, nz, eps_seed, sigma_seed, out=None):

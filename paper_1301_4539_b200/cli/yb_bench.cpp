@@ -108,7 +108,7 @@ CaseResult run_case(const Config& cfg, int variant) {
   opts.sources = {default_source(cfg.size, static_cast<double>(grid.dt), cfg)};
   opts.probes = default_probes(cfg.size, cfg.probe_stride);
   opts.quiescent_skip = cfg.quiescent_skip;
-  opts.variant = variant;
+  opts.kernel = variant;
   Simulation<float> sim(grid, opts);
   yb_set_kernel_timing(sim.handle(), 1);
   const auto records = sim.run(cfg.steps);
@@ -235,7 +235,7 @@ int mode_energy(const Config& cfg) {  // measure_energy_drift (bench.hpp:273-303
   const GridSpec<float> grid = make_uniform_grid<float>(cfg.size, 1.0f, static_cast<float>(kVacuumLightSpeed), cfg.safety);
   RunOptions<float> opts;
   opts.sources = {default_source(cfg.size, static_cast<double>(grid.dt), cfg)};
-  opts.variant = variant_id(cfg.variants.front());
+  opts.kernel = variant_id(cfg.variants.front());
   Simulation<float> sim(grid, opts);
   double reference = 0.0, max_drift = 0.0;
   bool have = false;

@@ -1973,3 +1973,257 @@ int yb_get_info(yb_sim* s, yb_info* info) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------- per-box ops on host FieldSets
+namespace {
+
+struct IBox {
+  int lo[3], hi[3];
+  bool empty() const { return hi[0] <= lo[0] || hi[1] <= lo[1] || hi[2] <= lo[2]; }
+};
+
+IBox ibox(const int* b) { return {{b[0], b[2], b[4]}, {b[1], b[3], b[5]}}; }
+
+// contains (array3.hpp:47-52): an empty inner box is contained in anything
+bool box_contains(const IBox& outer, const IBox& inner) {
+  if (inner.empty()) return true;
+  for (int a = 0; a < 3; ++a)
+    if (inner.lo[a] < outer.lo[a] || inner.hi[a] > outer.hi[a]) return false;
+  return true;
+}
+
+IBox box_intersect(const IBox& p, const IBox& q) {
+  IBox r;
+  for (int a = 0; a < 3; ++a) {
+    r.lo[a] = std::max(p.lo[a], q.lo[a]);
+    r.hi[a] = std::min(p.hi[a], q.hi[a]);
+  }
+  return r;
+}
+
+// comp_extents / curl_updatable_box (staggering.hpp:59-77)
+IBox extents_box(const int n[3], int c) {
+  IBox b;
+  const int axis = c % 3;
+  for (int a = 0; a < 3; ++a) {
+    const bool node = c < 3 ? (a != axis) : (a == axis);
+    b.lo[a] = 0;
+    b.hi[a] = n[a] + (node ? 1 : 0);
+  }
+  return b;
+}
+
+IBox updatable_box(const int n[3], int c) {
+  IBox b = extents_box(n, c);
+  if (c < 3)
+    for (int a = 0; a < 3; ++a)
+      if (a != c % 3) b.lo[a] = 1, b.hi[a] = n[a];
+  return b;
+}
+
+struct SubOp {
+  int op, comp;
+  IBox box;
+};
+
+// The component-boxes an operation updates, with the reference's range checks.
+int plan_fs_op(const int n[3], int op, int comp, const int* box, std::vector<SubOp>& out) {
+  const IBox node = {{0, 0, 0}, {n[0] + 1, n[1] + 1, n[2] + 1}};  // detail::node_box, kernels.hpp:113-116
+  switch (op) {
+    case YB_OP_UPDATE_E: {  // update_e_box, kernels.hpp:78-88
+      if (comp < 0 || comp > 2) return fail(YB_INVALID_ARGUMENT, "update_e_box: component %d is not electric", comp);
+      const IBox b = ibox(box);
+      if (b.empty()) return YB_OK;
+      if (!box_contains(updatable_box(n, comp), b))
+        return fail(YB_OUT_OF_RANGE, "update_e_box: box outside updatable range");
+      out.push_back({0, comp, b});
+      return YB_OK;
+    }
+    case YB_OP_UPDATE_H: {  // update_h_box, kernels.hpp:92-101
+      if (comp < 3 || comp > 5) return fail(YB_INVALID_ARGUMENT, "update_h_box: component %d is not magnetic", comp);
+      const IBox b = ibox(box);
+      if (b.empty()) return YB_OK;
+      if (!box_contains(extents_box(n, comp), b))
+        return fail(YB_OUT_OF_RANGE, "update_h_box: box outside component extents");
+      out.push_back({1, comp, b});
+      return YB_OK;
+    }
+    case YB_OP_ZERO: {  // zero_box, kernels.hpp:104-111
+      if (comp < 0 || comp > 5) return fail(YB_INVALID_ARGUMENT, "zero_box: component %d", comp);
+      const IBox b = ibox(box);
+      if (b.empty()) return YB_OK;
+      if (!box_contains(extents_box(n, comp), b))
+        return fail(YB_OUT_OF_RANGE, "zero_box: box outside component extents");
+      out.push_back({2, comp, b});
+      return YB_OK;
+    }
+    case YB_OP_AMPERE:
+    case YB_OP_FARADAY: {  // apply_ampere_range / apply_faraday_range, kernels.hpp:129-144
+      const IBox b = ibox(box);
+      const bool amp = op == YB_OP_AMPERE;
+      if (!box_contains(node, b))  // detail::check_range, kernels.hpp:118-122
+        return fail(YB_OUT_OF_RANGE, "%s: range out of bounds", amp ? "apply_ampere_range" : "apply_faraday_range");
+      for (int c = amp ? 0 : 3; c < (amp ? 3 : 6); ++c) {
+        const IBox r = box_intersect(b, amp ? updatable_box(n, c) : extents_box(n, c));
+        if (!r.empty()) out.push_back({amp ? 0 : 1, c, r});
+      }
+      return YB_OK;
+    }
+    case YB_OP_PEC:  // apply_pec_boundary, kernels.hpp:147-155: the tangential node planes of each face
+      for (int c = 0; c < 3; ++c) {
+        const IBox ext = extents_box(n, c);
+        for (int a = 0; a < 3; ++a) {
+          if (a == c) continue;
+          for (int side = 0; side < 2; ++side) {
+            IBox r = ext;
+            r.lo[a] = side ? n[a] : 0;
+            r.hi[a] = r.lo[a] + 1;
+            out.push_back({2, c, r});
+          }
+        }
+      }
+      return YB_OK;
+    default:
+      return fail(YB_INVALID_ARGUMENT, "unknown operation %d", op);
+  }
+}
+
+// components an update of `comp` reads (kernels.hpp:18-25)
+int stencil_mask(int op, int comp) {
+  if (op == 2) return 1 << comp;
+  static const int reads[6] = {(1 << 5) | (1 << 4), (1 << 3) | (1 << 5), (1 << 4) | (1 << 3),
+                               (1 << 1) | (1 << 2), (1 << 2) | (1 << 0), (1 << 0) | (1 << 1)};
+  return (1 << comp) | reads[comp];
+}
+
+template <class T>
+int fs_apply_t(int device, const int n[3], void* const* dense6, const void* const* cd3,
+               const std::vector<SubOp>& ops) {
+  yb::HostExt x{};
+  for (int c = 0; c < 6; ++c) {
+    const IBox e = extents_box(n, c);
+    for (int a = 0; a < 3; ++a) x.e[c][a] = e.hi[a];
+  }
+  int rd = 0, wr = 0;
+  bool need_cd = false;
+  for (const SubOp& o : ops) {
+    rd |= stencil_mask(o.op, o.comp);
+    wr |= 1 << o.comp;
+    need_cd |= o.op != 2;
+  }
+  for (int c = 0; c < 6; ++c)
+    if (((rd | wr) >> c & 1) && !dense6[c]) return fail(YB_INVALID_ARGUMENT, "component %d array is null", c);
+  if (need_cd && (!cd3 || !cd3[0] || !cd3[1] || !cd3[2]))
+    return fail(YB_INVALID_ARGUMENT, "coefficient arrays are null");
+  YB_CU(cudaSetDevice(device));
+  yb::HostFields<T> f{};
+  void* mem[9] = {};
+  auto release = [&](int rc) {
+    for (void* p : mem) cudaFree(p);
+    return rc;
+  };
+  for (int c = 0; c < 6; ++c) {
+    if (!((rd | wr) >> c & 1)) continue;
+    const size_t bytes = (size_t)x.e[c][0] * x.e[c][1] * x.e[c][2] * sizeof(T);
+    if (cudaMalloc(&mem[c], bytes) != cudaSuccess ||
+        cudaMemcpy(mem[c], dense6[c], bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      return release(fail(YB_CUDA_ERROR, "host FieldSet: copy of component %d to the device failed", c));
+    f.f[c] = static_cast<T*>(mem[c]);
+  }
+  if (need_cd)
+    for (int a = 0; a < 3; ++a) {
+      const size_t bytes = (size_t)n[a] * sizeof(T);
+      if (cudaMalloc(&mem[6 + a], bytes) != cudaSuccess ||
+          cudaMemcpy(mem[6 + a], cd3[a], bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        return release(fail(YB_CUDA_ERROR, "coefficient copy failed"));
+      f.cd[a] = static_cast<const T*>(mem[6 + a]);
+    }
+  // in the reference's order: components one after another (stream-ordered)
+  for (const SubOp& o : ops) {
+    const yb::HostBox b{o.box.lo[0], o.box.hi[0], o.box.lo[1], o.box.hi[1], o.box.lo[2], o.box.hi[2]};
+    if (yb::launch_host_box<T>(f, x, o.op, o.comp, b, 0) != cudaSuccess)
+      return release(fail(YB_CUDA_ERROR, "per-box kernel launch failed"));
+  }
+  for (int c = 0; c < 6; ++c) {
+    if (!(wr >> c & 1)) continue;
+    const size_t bytes = (size_t)x.e[c][0] * x.e[c][1] * x.e[c][2] * sizeof(T);
+    if (cudaMemcpy(dense6[c], mem[c], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return release(fail(YB_CUDA_ERROR, "host FieldSet: copy of component %d back failed", c));
+  }
+  return release(YB_OK);
+}
+
+template <class T>
+int fs_energy_t(int device, const int n[3], const void* const* dense6, const void* const* prev3,
+                const double* const* d3, double* energy) {
+  yb::HostExt x{};
+  for (int c = 0; c < 6; ++c) {
+    const IBox e = extents_box(n, c);
+    for (int a = 0; a < 3; ++a) x.e[c][a] = e.hi[a];
+  }
+  YB_CU(cudaSetDevice(device));
+  void* mem[10] = {};
+  auto release = [&](int rc) {
+    for (void* p : mem) cudaFree(p);
+    return rc;
+  };
+  yb::HostFields<T> f{};
+  const T* prev[3] = {};
+  for (int q = 0; q < 9; ++q) {
+    const int c = q < 6 ? q : q - 3;
+    const size_t bytes = (size_t)x.e[c][0] * x.e[c][1] * x.e[c][2] * sizeof(T);
+    const void* src = q < 6 ? dense6[q] : prev3[q - 6];
+    if (cudaMalloc(&mem[q], bytes) != cudaSuccess || cudaMemcpy(mem[q], src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      return release(fail(YB_CUDA_ERROR, "total_energy: copy to the device failed"));
+    if (q < 6)
+      f.f[q] = static_cast<T*>(mem[q]);
+    else
+      prev[q - 6] = static_cast<const T*>(mem[q]);
+  }
+  std::vector<double> dxyz;
+  for (int a = 0; a < 3; ++a)
+    for (int i = 0; i < n[a]; ++i) dxyz.push_back(d3[a] ? d3[a][i] : 1.0);
+  const size_t scratch = (size_t)yb::host_energy_scratch_doubles();
+  if (cudaMalloc(&mem[9], (dxyz.size() + scratch) * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(mem[9], dxyz.data(), dxyz.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    return release(fail(YB_CUDA_ERROR, "total_energy: spacing copy failed"));
+  double* d = static_cast<double*>(mem[9]);
+  if (yb::launch_host_energy<T>(f, prev, x, d, n[0], n[1], n[2], d + dxyz.size(), 0) != cudaSuccess ||
+      cudaMemcpy(energy, d + dxyz.size() + scratch - 1, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return release(fail(YB_CUDA_ERROR, "total_energy kernel failed"));
+  return release(YB_OK);
+}
+
+}  // namespace
+
+extern "C" {
+
+int yb_fs_apply(int device, int dtype, int nx, int ny, int nz, void* const* dense6, const void* const* cd3, int op,
+                int comp, const int* box) {
+  if (!dense6) return fail(YB_INVALID_ARGUMENT, "null field arrays");
+  if (dtype != YB_F32 && dtype != YB_F64) return fail(YB_INVALID_ARGUMENT, "unknown element type %d", dtype);
+  if (nx < 1 || ny < 1 || nz < 1) return fail(YB_INVALID_ARGUMENT, "cell counts must be positive");
+  if (op != YB_OP_PEC && !box) return fail(YB_INVALID_ARGUMENT, "null box");
+  const int n[3] = {nx, ny, nz};
+  std::vector<SubOp> ops;
+  if (int rc = plan_fs_op(n, op, comp, box, ops)) return rc;
+  if (ops.empty()) return YB_OK;
+  return dtype == YB_F32 ? fs_apply_t<float>(device, n, dense6, cd3, ops)
+                         : fs_apply_t<double>(device, n, dense6, cd3, ops);
+}
+
+int yb_fs_total_energy(int device, int dtype, int nx, int ny, int nz, const void* const* dense6,
+                       const void* const* prev_h3, const double* dx, const double* dy, const double* dz,
+                       double* energy) {
+  if (!dense6 || !prev_h3 || !energy) return fail(YB_INVALID_ARGUMENT, "null argument");
+  for (int c = 0; c < 6; ++c)
+    if (!dense6[c] || (c < 3 && !prev_h3[c])) return fail(YB_INVALID_ARGUMENT, "null array");
+  if (dtype != YB_F32 && dtype != YB_F64) return fail(YB_INVALID_ARGUMENT, "unknown element type %d", dtype);
+  if (nx < 1 || ny < 1 || nz < 1) return fail(YB_INVALID_ARGUMENT, "cell counts must be positive");
+  const int n[3] = {nx, ny, nz};
+  const double* d3[3] = {dx, dy, dz};
+  return dtype == YB_F32 ? fs_energy_t<float>(device, n, dense6, prev_h3, d3, energy)
+                         : fs_energy_t<double>(device, n, dense6, prev_h3, d3, energy);
+}
+
+}  // extern "C"

@@ -202,6 +202,29 @@ cudaError_t launch_peer_signal(unsigned* flag_down, unsigned* flag_up, unsigned 
 // device time; on timeout fills the wait-error record `err` (WAIT_PEER).
 cudaError_t launch_peer_wait(const unsigned* flags, unsigned need0, unsigned need1, int* err,
                              unsigned long long wait_ns, cudaStream_t st);
+// Per-box operations on dense Array3 arrays (yb_hostops.cu): the caller's
+// host FieldSet copied to the device as is (element type T = float or double).
+struct HostExt {
+  int e[6][3];  // extents per component (staggering.hpp:34-39)
+};
+struct HostBox {
+  int xlo, xhi, ylo, yhi, zlo, zhi;
+};
+template <class T>
+struct HostFields {
+  T* f[6];         // ex..hz (nullptr where the op does not touch it)
+  const T* cd[3];  // Coefficients cdx, cdy, cdz
+};
+// op 0: update_e_box, 1: update_h_box, 2: zero_box of component `comp`.
+template <class T>
+cudaError_t launch_host_box(const HostFields<T>& f, const HostExt& x, int op, int comp, const HostBox& b,
+                            cudaStream_t st);
+// total_energy into scratch[host_energy_scratch_doubles() - 1]; dxyz = dx | dy | dz (double).
+template <class T>
+cudaError_t launch_host_energy(const HostFields<T>& f, const T* const* prev_h, const HostExt& x,
+                               const double* dxyz, int nx, int ny, int nz, double* scratch, cudaStream_t st);
+int host_energy_scratch_doubles();
+
 // Halo planes <-> a contiguous exchange buffer: plane q of the list is
 // src[q] (or dst[q]) = one padded plane (PX*PY floats); ext holds them in order.
 struct HaloList {
