@@ -1811,6 +1811,19 @@ int yb_peer_link(yb_sim* s, int side, yb_sim* other) {
   if (int rc = check_peer_args(s, side, other->g.nz)) return rc;
   if (int rc = ensure_pflags(other)) return rc;
   if (other->g.nx != s->g.nx || other->g.ny != s->g.ny) return fail(YB_INVALID_ARGUMENT, "peer x/y extents differ");
+  if (other->device != s->device) {  // slabs on two GPUs of one process: my kernels store into its memory
+    int can = 0;
+    YB_CU(cudaDeviceCanAccessPeer(&can, s->device, other->device));
+    if (!can)
+      return fail(YB_INVALID_ARGUMENT, "device %d cannot access device %d's memory (no P2P path)", s->device,
+                  other->device);
+    YB_CU(cudaSetDevice(s->device));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(other->device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      (void)cudaGetLastError();  // clear the sticky-free "already enabled" status
+    else
+      YB_CU(e);
+  }
   PeerSide& ps = s->peer[side];
   for (int b = 0; b < 2; ++b)
     for (int c = 0; c < 6; ++c) ps.buf[b][c] = other->buf[b][c];
