@@ -225,6 +225,26 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def shim_pageable_e2e(cfg, variant, device):
+    """The same config end to end through the C++ drop-in (yb_e2e over
+    include/yeeb200/yeeblock.hpp) from the reference's own pageable host
+    storage (FieldSet<float> = std::vector). Informational next to `e2e`."""
+    exe = os.path.join(ROOT, "paper_1301_4539_b200", "yb_e2e")
+    if not os.path.exists(exe):
+        return {"unavailable": "paper_1301_4539_b200/yb_e2e not built"}
+    kernel = "fused" if variant == "fused" else "tb2"
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(device)))
+    r = subprocess.run([exe, "--config", cfg, "--kernel", kernel, "--reps", "2"], capture_output=True, text=True,
+                       timeout=600, env=env)
+    if r.returncode != 0:
+        return {"unavailable": (r.stderr or r.stdout).strip().splitlines()[-1:] or ["yb_e2e failed"]}
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    out["path"] = ("C++ drop-in: Simulation<float>(grid, layout, Variant, RunOptions) -> set_cell_coefficients "
+                   "(std::vector) -> run(config steps) (uploads the host FieldSet) -> fields() read back; "
+                   "pageable host memory")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -413,7 +433,7 @@ def main():
     # e2e through the public API with pinned host buffers (run_simulation
     # semantics): per-cell coefficients + fields uploaded, the config's full
     # step count (with halo exchanges), fields downloaded.
-    e2e = e2e_skip = None
+    e2e = e2e_skip = e2e_shim = None
     if not args.no_e2e:
         # pinned host buffers on the GPU's NUMA node (first touch by a local CPU),
         # so the copies do not cross the socket interconnect; restored afterwards
@@ -496,6 +516,8 @@ def main():
         finally:
             os.sched_setaffinity(0, affinity)
         e2e["host_cpus"] = f"{len(local_cpus)} CPUs of the GPU NUMA node" if local_cpus else "all (GPU NUMA node unknown)"
+        if rank == 0 and world == 1:
+            e2e_shim = shim_pageable_e2e(args.config, args.variant, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -509,6 +531,8 @@ def main():
                 "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         if e2e_skip is not None:
             line["e2e_quiescent_skip"] = e2e_skip
+        if e2e_shim is not None:
+            line["e2e_shim_pageable"] = e2e_shim
         print(json.dumps(line), flush=True)
     if dist:
         torch.cuda.synchronize()
