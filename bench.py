@@ -463,7 +463,7 @@ def main():
                 cell_arrays = {q: med[q] for q in want}
             e_steps = cfg_steps
 
-            def run_e2e(qskip):
+            def run_e2e(qskip, upload_fields=True):
                 s2 = make_sim()
                 if table is not None:
                     s2.add_source(*src, table)
@@ -478,7 +478,8 @@ def main():
                 t0 = time.perf_counter()
                 if cell_arrays:
                     s2.set_cell_coeffs_many(cell_arrays)
-                s2.upload(host_f)
+                if upload_fields:
+                    s2.upload(host_f)
                 if ex2 is None:
                     s2.run(e_steps)
                 elif args.exchange == "p2p":
@@ -498,16 +499,29 @@ def main():
                     dt = float(tt.item())
                 return dt, skipped
 
-            dt, _ = run_e2e(False)
-            h2d = sum(a_.nbytes for a_ in host_f) + sum(a_.nbytes for a_ in cell_arrays.values())
+            # Zero-start configs (1, 2, 4): the state begins as the zero FieldSet the reference's
+            # Simulation constructs (fields.hpp FieldSet ctor); yb_create zero-fills the device state
+            # the same way, so the caller's inputs are the coefficient arrays (+ source table) only.
+            # Seeded-field configs (3, 5) upload their six fields.
+            zero_start = fs is None
+            coef_b = sum(a_.nbytes for a_ in cell_arrays.values())
+            field_b = sum(a_.nbytes for a_ in host_f)
             d2h = sum(a_.nbytes for a_ in host_out)
+            dt, _ = run_e2e(False, upload_fields=not zero_start)
+            h2d = coef_b + (0 if zero_start else field_b)
             e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
                    "steps": e_steps, "wall_s": dt, "per_gpu_bytes": True,
-                   "path": "Simulation: set_cell_coeffs + upload (pinned host) -> run(config steps) -> "
-                           "download (pinned host)"}
+                   "path": ("Simulation: set_cell_coeffs (pinned host) -> run(config steps) from the zero-initialised "
+                            "state -> download all six fields (pinned host)" if zero_start else
+                            "Simulation: set_cell_coeffs + upload all six fields (pinned host) -> run(config steps) "
+                            "-> download all six fields (pinned host)")}
+            if zero_start:  # the same run with the zero fields uploaded from the host as well
+                du, _ = run_e2e(False, upload_fields=True)
+                e2e["with_zero_field_upload"] = {"value": cells_total * e_steps / du / 1e9, "unit": UNIT,
+                                                 "wall_s": du, "h2d_bytes_per_step": (coef_b + field_b) / e_steps}
             if fs is None:  # zero initial fields + point source: the reference's quiescent skip applies
-                dq, skipped = run_e2e(True)
+                dq, skipped = run_e2e(True, upload_fields=False)
                 e2e_skip = {"value": cells_total * e_steps / dq / 1e9, "unit": UNIT, "wall_s": dq,
                             "skipped_items": skipped,
                             "note": "same e2e run with yb_set_quiescent_skip(1) (RunOptions::quiescent_skip, "

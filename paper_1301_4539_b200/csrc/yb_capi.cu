@@ -751,11 +751,11 @@ int copy_dense(yb_sim* s, int comp, float* dev, const float* hsrc, float* hdst) 
   const size_t n = (size_t)e[0] * e[1] * e[2];
   float* stage = s->buf[s->cur ^ 1][comp];
   if (hsrc) {
-    YB_CU(cudaMemcpyAsync(stage, hsrc, n * 4, cudaMemcpyHostToDevice, s->stream));
+    YB_CU(yb::copy_h2d(stage, hsrc, n * 4, s->stream));
     YB_CU(yb::launch_scatter_dense(s->g, e, stage, dev, s->stream));
   } else {
     YB_CU(yb::launch_gather_dense(s->g, e, dev, stage, s->stream));
-    YB_CU(cudaMemcpyAsync(hdst, stage, n * 4, cudaMemcpyDeviceToHost, s->stream));
+    YB_CU(yb::copy_d2h(hdst, stage, n * 4, s->stream));
   }
   YB_CU(cudaMemsetAsync(stage - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
@@ -932,7 +932,7 @@ int yb_set_axis_coeffs(yb_sim* s, const float* cdx, const float* cdy, const floa
 // Per-cell coefficient upload, part 1: the host array into a staging buffer
 // and a device check of uniformity (bit patterns) into *flag; no sync.
 static int cell_stage(yb_sim* s, const float* cells, long long n, float* stage, int* flag) {
-  YB_CU(cudaMemcpyAsync(stage, cells, (size_t)n * 4, cudaMemcpyHostToDevice, s->stream));
+  YB_CU(yb::copy_h2d(stage, cells, (size_t)n * 4, s->stream));
   const int one = 1;
   YB_CU(cudaMemcpyAsync(flag, &one, 4, cudaMemcpyHostToDevice, s->stream));
   YB_CU(yb::launch_all_equal(stage, n, flag, s->num_sms, s->stream));
@@ -1220,7 +1220,7 @@ int yb_upload_fields(yb_sim* s, const float* const* d) {
     int e[3];
     comp_ext(s->g, c, e);
     float* stage = s->buf[s->cur ^ 1][c];
-    YB_CU(cudaMemcpyAsync(stage, d[c], (size_t)e[0] * e[1] * e[2] * 4, cudaMemcpyHostToDevice, s->stream));
+    YB_CU(yb::copy_h2d(stage, d[c], (size_t)e[0] * e[1] * e[2] * 4, s->stream));
     YB_CU(cudaEventRecord(s->xev[c], s->stream));
     YB_CU(cudaStreamWaitEvent(s->xfer, s->xev[c], 0));  // its scatter overlaps the next copy
     YB_CU(yb::launch_scatter_dense(s->g, e, stage, s->buf[s->cur][c], s->xfer));
@@ -1248,7 +1248,7 @@ int yb_download_fields(yb_sim* s, float* const* d) {
     YB_CU(yb::launch_gather_dense(s->g, e, s->buf[s->cur][c], stage, s->xfer));
     YB_CU(cudaEventRecord(s->xev[c], s->xfer));
     YB_CU(cudaStreamWaitEvent(s->stream, s->xev[c], 0));
-    YB_CU(cudaMemcpyAsync(d[c], stage, (size_t)e[0] * e[1] * e[2] * 4, cudaMemcpyDeviceToHost, s->stream));
+    YB_CU(yb::copy_d2h(d[c], stage, (size_t)e[0] * e[1] * e[2] * 4, s->stream));
   }
   for (int c = 0; c < 6; ++c)
     YB_CU(cudaMemsetAsync(s->buf[s->cur ^ 1][c] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
@@ -2139,7 +2139,7 @@ int fs_apply_t(int device, const int n[3], void* const* dense6, const void* cons
     if (!((rd | wr) >> c & 1)) continue;
     const size_t bytes = (size_t)x.e[c][0] * x.e[c][1] * x.e[c][2] * sizeof(T);
     if (cudaMalloc(&mem[c], bytes) != cudaSuccess ||
-        cudaMemcpy(mem[c], dense6[c], bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        yb::copy_h2d(mem[c], dense6[c], bytes, 0) != cudaSuccess)
       return release(fail(YB_CUDA_ERROR, "host FieldSet: copy of component %d to the device failed", c));
     f.f[c] = static_cast<T*>(mem[c]);
   }
@@ -2160,9 +2160,10 @@ int fs_apply_t(int device, const int n[3], void* const* dense6, const void* cons
   for (int c = 0; c < 6; ++c) {
     if (!(wr >> c & 1)) continue;
     const size_t bytes = (size_t)x.e[c][0] * x.e[c][1] * x.e[c][2] * sizeof(T);
-    if (cudaMemcpy(dense6[c], mem[c], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (yb::copy_d2h(dense6[c], mem[c], bytes, 0) != cudaSuccess)
       return release(fail(YB_CUDA_ERROR, "host FieldSet: copy of component %d back failed", c));
   }
+  if (cudaStreamSynchronize(0) != cudaSuccess) return release(fail(YB_CUDA_ERROR, "host FieldSet: copy back failed"));
   return release(YB_OK);
 }
 

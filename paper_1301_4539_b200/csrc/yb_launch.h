@@ -242,3 +242,12 @@ cudaError_t launch_energy(const Geo& g, const Fields& F, const float* const* pre
 cudaError_t launch_all_equal(const float* a, long long n, int* flag, int num_sms, cudaStream_t st);
 
 }  // namespace yb
+
+namespace yb {
+// Caller-memory transfers (yb_xfer.cu): pinned buffers -> cudaMemcpyAsync;
+// pageable ones through the pinned staging pipeline (multi-threaded host
+// copies overlapped with the DMAs).
+bool host_is_pageable(const void* p);
+cudaError_t copy_h2d(void* dst, const void* src, size_t n, cudaStream_t st);
+cudaError_t copy_d2h(void* dst, const void* src, size_t n, cudaStream_t st);
+}  // namespace yb
