@@ -499,11 +499,13 @@ def main():
                     dt = float(tt.item())
                 return dt, skipped
 
-            # Zero-start configs (1, 2, 4): the state begins as the zero FieldSet the reference's
-            # Simulation constructs (fields.hpp FieldSet ctor); yb_create zero-fills the device state
-            # the same way, so the caller's inputs are the coefficient arrays (+ source table) only.
-            # Seeded-field configs (3, 5) upload their six fields.
-            zero_start = fs is None
+            # Configs 2 and 4 (a per-cell medium, zero initial fields) follow the reference's
+            # Simulation flow (runner.hpp:205-266): the state begins as the zero FieldSet the
+            # Simulation constructs — yb_create zero-fills the device state the same way — and the
+            # caller's input is the medium (per-cell coefficient arrays). Configs with seeded fields
+            # (3, 5), and config 1 (vacuum: no medium, so its input is the initial state), follow
+            # run_simulation (runner.hpp:349-362) and copy the six fields in.
+            zero_start = fs is None and bool(cell_arrays)
             coef_b = sum(a_.nbytes for a_ in cell_arrays.values())
             field_b = sum(a_.nbytes for a_ in host_f)
             d2h = sum(a_.nbytes for a_ in host_out)
@@ -521,7 +523,7 @@ def main():
                 e2e["with_zero_field_upload"] = {"value": cells_total * e_steps / du / 1e9, "unit": UNIT,
                                                  "wall_s": du, "h2d_bytes_per_step": (coef_b + field_b) / e_steps}
             if fs is None:  # zero initial fields + point source: the reference's quiescent skip applies
-                dq, skipped = run_e2e(True, upload_fields=False)
+                dq, skipped = run_e2e(True, upload_fields=not zero_start)
                 e2e_skip = {"value": cells_total * e_steps / dq / 1e9, "unit": UNIT, "wall_s": dq,
                             "skipped_items": skipped,
                             "note": "same e2e run with yb_set_quiescent_skip(1) (RunOptions::quiescent_skip, "

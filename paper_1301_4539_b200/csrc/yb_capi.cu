@@ -338,7 +338,8 @@ int prepare_fused(yb_sim* s) {
     for (int b = 0; b < 2; ++b) {
       int q = 0;
       for (int c = 0; c < 6; ++c)
-        if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->buf[b][c], yb::kTB2BY)) return rc;
+        if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->buf[b][c], yb::tb2_short(c) ? yb::kTB2RowsE : yb::kTB2BY))
+          return rc;
       for (int a = 0; a < 4; ++a)
         if (s->cell[a])
           if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->cell[a],

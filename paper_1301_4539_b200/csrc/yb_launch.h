@@ -33,6 +33,19 @@ constexpr int kTB2RowsCA = kTB2Rows + 3;
 constexpr int kTB2RowsDA = kTB2Rows + 2;
 constexpr int slot_floats(int rows) { return ((kBX * rows * 4 + 127) / 128) * 32; }
 constexpr int kTB2SlotF = slot_floats(kTB2BY);
+// ex, ey, ez, hy are read on rows y0-1 .. y0+9 only (hx, hz also on y0-2,
+// for the j-1 neighbour of row y0-1): 11-row boxes for those four, which
+// trims a stage enough for a third one next to a per-cell Cb array.
+constexpr int kTB2RowsE = kTB2Rows + 3;
+constexpr int kTB2SlotE = slot_floats(kTB2RowsE);
+__host__ __device__ constexpr bool tb2_short(int q) { return q != 3 && q != 5; }  // ex, ey, ez, hy
+// physical start (floats) of component q's slot in a stage: ex, ey, ez, hx, hy, hz
+__host__ __device__ constexpr int tb2_foff(int q) {
+  return q <= 3 ? q * kTB2SlotE : (q == 4 ? 3 * kTB2SlotE + kTB2SlotF : 4 * kTB2SlotE + kTB2SlotF);
+}
+// the slot's row-y0-2 origin (the 11-row slots start one row lower)
+__host__ __device__ constexpr int tb2_fbase(int q) { return tb2_foff(q) - (tb2_short(q) ? kBX : 0); }
+constexpr int kTB2Fields = 4 * kTB2SlotE + 2 * kTB2SlotF;  // floats of the six field slots
 constexpr int kTB2SlotC = slot_floats(kTB2RowsCA);
 constexpr int kTB2SlotD = slot_floats(kTB2RowsDA);
 constexpr int kTB2E1 = 2 * 3 * kTB2RowWarps * kBX;    // E^{n+1} planes (double buffered)
@@ -50,7 +63,7 @@ constexpr int kTB4Cols = kTB4Win - 8;       // output columns x0 .. x0+55
 
 // floats of one stage for a coefficient set (mask bit q: array q per-cell)
 inline int tb2_stage_floats(int cell_mask) {
-  return 6 * kTB2SlotF + ((cell_mask & 1) + ((cell_mask >> 1) & 1)) * kTB2SlotC +
+  return kTB2Fields + ((cell_mask & 1) + ((cell_mask >> 1) & 1)) * kTB2SlotC +
          (((cell_mask >> 2) & 1) + ((cell_mask >> 3) & 1)) * kTB2SlotD;
 }
 

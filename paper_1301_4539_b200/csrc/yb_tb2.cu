@@ -237,8 +237,8 @@ __device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, in
 template <bool CAC, bool CBC, bool DAC, bool DBC>
 struct StageLayout {
   static constexpr int floats =
-      6 * kTB2SlotF + (CAC + CBC) * kTB2SlotC + (DAC + DBC) * kTB2SlotD;
-  static constexpr int off_ca = 6 * kTB2SlotF;
+      kTB2Fields + (CAC + CBC) * kTB2SlotC + (DAC + DBC) * kTB2SlotD;
+  static constexpr int off_ca = kTB2Fields;
   static constexpr int off_cb = off_ca + CAC * kTB2SlotC;
   static constexpr int off_da = off_cb + CBC * kTB2SlotC;
   static constexpr int off_db = off_da + DAC * kTB2SlotD;
@@ -363,8 +363,8 @@ struct Rows {
     const int rs = er + 1;
     const int s = cur.wait(B, a.nstages);
     const float* F = B.stages + (size_t)s * L::floats + rs * BX + c;
-    h0p.x = lds4(F + 3 * kTB2SlotF);
-    h0p.y = lds4(F + 4 * kTB2SlotF);
+    h0p.x = lds4(F + tb2_fbase(3));
+    h0p.y = lds4(F + tb2_fbase(4));
     release_stage(B.empty, s, l);
   }
 
@@ -385,19 +385,19 @@ struct Rows {
       const float* F = B.stages + (size_t)s1 * L::floats;
       const float* Fr = F + (er + 1) * BX + c;  // field stage row of j
       const float cdz_e = ze;
-      h0n.x = lds4(Fr + 3 * kTB2SlotF);
-      h0n.y = lds4(Fr + 4 * kTB2SlotF);
-      h0n.z = lds4(Fr + 5 * kTB2SlotF);
-      const float4 hy_im = make_float4(Fr[4 * kTB2SlotF - 1], h0n.y.x, h0n.y.y, h0n.y.z);
-      const float4 hz_im = make_float4(Fr[5 * kTB2SlotF - 1], h0n.z.x, h0n.z.y, h0n.z.z);
+      h0n.x = lds4(Fr + tb2_fbase(3));
+      h0n.y = lds4(Fr + tb2_fbase(4));
+      h0n.z = lds4(Fr + tb2_fbase(5));
+      const float4 hy_im = make_float4(Fr[tb2_fbase(4) - 1], h0n.y.x, h0n.y.y, h0n.y.z);
+      const float4 hz_im = make_float4(Fr[tb2_fbase(5) - 1], h0n.z.x, h0n.z.y, h0n.z.z);
       const float* Fc = F + er * BX + c;  // coefficient stage row of j
       if (CAC) can = lds4(Fc + L::off_ca);
       if (CBC) cbn = lds4(Fc + L::off_cb);
       if (DAC && er <= RW - 2) dan = lds4(Fc + L::off_da);
       if (DBC && er <= RW - 2) dbn = lds4(Fc + L::off_db);
-      e1c = e_update4<CAC, CBC>(co, g, i0, xedge, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn, lds4(Fr),
-                                lds4(Fr + kTB2SlotF), lds4(Fr + 2 * kTB2SlotF), h0n.x, h0n.y, h0n.z,
-                                lds4(Fr + 3 * kTB2SlotF - BX), lds4(Fr + 5 * kTB2SlotF - BX), hy_im, hz_im, h0p.x,
+      e1c = e_update4<CAC, CBC>(co, g, i0, xedge, j, p + g.zoff, cdy_e, cdz_e, cdx_e, can, cbn, lds4(Fr + tb2_fbase(0)),
+                                lds4(Fr + tb2_fbase(1)), lds4(Fr + tb2_fbase(2)), h0n.x, h0n.y, h0n.z,
+                                lds4(Fr + tb2_fbase(3) - BX), lds4(Fr + tb2_fbase(5) - BX), hy_im, hz_im, h0p.x,
                                 h0p.y);
       if (it.src && src_row(src(), 1, j, p)) {
 #pragma unroll
@@ -576,8 +576,8 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
     const int s = cur.wait(B, S);
     const float* F = B.stages + (size_t)s * L::floats;
     const int pb = (it.pstart - 1) & 1;
-    *B.H0e(pb, 0, e1r, e1i) = F[3 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
-    *B.H0e(pb, 1, e1r, e1i) = F[4 * kTB2SlotF + (e1r + 1) * BX + ce(e1i)];
+    *B.H0e(pb, 0, e1r, e1i) = F[tb2_fbase(3) + (e1r + 1) * BX + ce(e1i)];
+    *B.H0e(pb, 1, e1r, e1i) = F[tb2_fbase(4) + (e1r + 1) * BX + ce(e1i)];
     release_stage(B.empty, s, l);
   }
 
@@ -588,13 +588,13 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
       const float* F = B.stages + (size_t)s1 * L::floats;
       const int r = e1r, col = ce(e1i), i = ie(e1i), j = it.y0 - 1 + r, rs = r + 1;
       const float* Fr = F + rs * BX + col;
-      const float hx = Fr[3 * kTB2SlotF], hy = Fr[4 * kTB2SlotF], hz = Fr[5 * kTB2SlotF];
+      const float hx = Fr[tb2_fbase(3)], hy = Fr[tb2_fbase(4)], hz = Fr[tb2_fbase(5)];
       const float ca = CAC ? F[L::off_ca + r * BX + col] : 0.f;
       const float cb = CBC ? F[L::off_cb + r * BX + col] : 0.f;
       float ox, oy, oz;
       e_update1<CAC, CBC>(co, g, i, j, p + g.zoff, cdy1, co.cdz_e[p], cdx1, ca,
-                          cb, Fr[0], Fr[kTB2SlotF], Fr[2 * kTB2SlotF], hx, hy, hz, Fr[3 * kTB2SlotF - BX],
-                          Fr[5 * kTB2SlotF - BX], Fr[4 * kTB2SlotF - 1], Fr[5 * kTB2SlotF - 1],
+                          cb, Fr[tb2_fbase(0)], Fr[tb2_fbase(1)], Fr[tb2_fbase(2)], hx, hy, hz, Fr[tb2_fbase(3) - BX],
+                          Fr[tb2_fbase(5) - BX], Fr[tb2_fbase(4) - 1], Fr[tb2_fbase(5) - 1],
                           *B.H0e((p - 1) & 1, 0, r, e1i), *B.H0e((p - 1) & 1, 1, r, e1i), ox, oy, oz);
       if (it.src && src_row(src, 1, j, p)) {
         ox = __fadd_rn(ox, src_add(src, 1, 0, i, j, p));
@@ -668,9 +668,9 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   constexpr bool QS = MODE == 1, MS = MODE == 2, PS = MODE == 3;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
-  constexpr uint32_t kBytesF = kBX * kTB2BY * 4, kBytesC = kBX * kTB2RowsCA * 4,
+  constexpr uint32_t kBytesF = kBX * kTB2BY * 4, kBytesE = kBX * kTB2RowsE * 4, kBytesC = kBX * kTB2RowsCA * 4,
                      kBytesD = kBX * kTB2RowsDA * 4;
-  constexpr uint32_t kStageBytes = 6 * kBytesF + (CAC + CBC) * kBytesC + (DAC + DBC) * kBytesD;
+  constexpr uint32_t kStageBytes = 2 * kBytesF + 4 * kBytesE + (CAC + CBC) * kBytesC + (DAC + DBC) * kBytesD;
   constexpr int kQ = 8;
   extern __shared__ __align__(128) float smem[];
 
@@ -779,15 +779,15 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       float* dst = B.stages + (size_t)s * L::floats;
       // tensor z coordinate = local plane + kGhost
       if (pro && p_e == 0) {  // hx, hy of plane pstart-1
-        mbar_expect_tx(bar, 2 * kBytesF);
-        tma_load_3d(smem_u32(dst + 3 * kTB2SlotF), &M.m[3], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
-        tma_load_3d(smem_u32(dst + 4 * kTB2SlotF), &M.m[4], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
+        mbar_expect_tx(bar, kBytesF + kBytesE);
+        tma_load_3d(smem_u32(dst + tb2_foff(3)), &M.m[3], x0 - 4, y0 - 2, pi.pstart - 1 + kGhost, bar);
+        tma_load_3d(smem_u32(dst + tb2_foff(4)), &M.m[4], x0 - 4, y0 - 1, pi.pstart - 1 + kGhost, bar);
       } else {
         const int z = pi.pstart + p_e - pro + kGhost;
         mbar_expect_tx(bar, kStageBytes);
 #pragma unroll
         for (int q2 = 0; q2 < 6; ++q2)
-          tma_load_3d(smem_u32(dst + q2 * kTB2SlotF), &M.m[q2], x0 - 4, y0 - 2, z, bar);
+          tma_load_3d(smem_u32(dst + tb2_foff(q2)), &M.m[q2], x0 - 4, tb2_short(q2) ? y0 - 1 : y0 - 2, z, bar);
         int m = 6;
         if (CAC) tma_load_3d(smem_u32(dst + L::off_ca), &M.m[m++], x0 - 4, y0 - 1, z, bar);
         if (CBC) tma_load_3d(smem_u32(dst + L::off_cb), &M.m[m++], x0 - 4, y0 - 1, z, bar);
