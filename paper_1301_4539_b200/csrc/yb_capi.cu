@@ -164,6 +164,7 @@ struct yb_sim {
   unsigned pcnt_base[2] = {0u, 0u};
   bool pending_full = false;  // ... whose boundary launch already covered every plane
   bool persist = true;        // multi-sweep two-step launches (YB_TB2_PERSIST=0: off)
+  int pf2 = 0;                // two-step L2 prefetch distance in planes (YB_TB2_PF)
   bool qskip = false;         // yb_set_quiescent_skip
   bool q_valid = false;       // quiescent map matches the state buffers
   unsigned* qbits = nullptr;  // quiescent map (tiles x words)
@@ -526,6 +527,7 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
   yb::FusedArgs a{};
   a.g = s->g;
   a.nstages = s->stages2;
+  a.pf = s->pf2;
   a.ntx = s->ntx;
   a.nty = s->nty;
   const dim3 grid = set_chunks(s, a, zchunk, z);
@@ -805,6 +807,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   s->zchunk_req = d->zchunk;
   if (const char* e = std::getenv("YB_STPOL")) s->store_policy = std::atoi(e);
   if (const char* e = std::getenv("YB_TB2_PERSIST")) s->persist = std::atoi(e) != 0;
+  if (const char* e = std::getenv("YB_TB2_PF")) s->pf2 = std::max(0, std::atoi(e));
   Geo& g = s->g;
   g.nx = d->nx;
   g.ny = d->ny;

@@ -79,6 +79,7 @@ struct TMaps {
 struct FusedArgs {
   Geo g;
   int nstages;
+  int pf;  // two-step producer: L2 prefetch (cp.async.bulk.prefetch.tensor) this many planes ahead (0: off)
   int zchunk;
   // z-chunks of this launch: nch0 chunks over planes [zb0, ze0), then the
   // rest over [zb1, ze1) (a whole sweep: [0, nz) and an empty second range;

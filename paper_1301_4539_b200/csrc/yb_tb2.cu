@@ -794,6 +794,14 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         if (DAC) tma_load_3d(smem_u32(dst + L::off_da), &M.m[m++], x0 - 4, y0 - 1, z, bar);
         if (DBC) tma_load_3d(smem_u32(dst + L::off_db), &M.m[m++], x0 - 4, y0 - 1, z, bar);
         (void)NARR;
+        // the same boxes a.pf planes further on, into L2 only (within the item's planes)
+        if (a.pf > 0 && z + a.pf <= pi.pin_end + kGhost) {
+#pragma unroll
+          for (int q2 = 0; q2 < 6; ++q2)
+            tma_prefetch_3d(&M.m[q2], x0 - 4, tb2_short(q2) ? y0 - 1 : y0 - 2, z + a.pf);
+#pragma unroll
+          for (int q2 = 6; q2 < NARR; ++q2) tma_prefetch_3d(&M.m[q2], x0 - 4, y0 - 1, z + a.pf);
+        }
       }
       if (++p_e == p_nE) p_item = -1;
     }
