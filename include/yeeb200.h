@@ -275,6 +275,18 @@ int yb_peer_wait(yb_sim* sim);
  * wait, split sweep, push. Start a run with one yb_peer_push of the current
  * state. */
 int yb_peer_step(yb_sim* sim, int64_t nsteps);
+/* Chained exchange periods: nsteps (even) / 2 periods in ONE persistent
+ * two-step launch — per sweep, the bottom / top z-chunk items wait in-kernel
+ * for the neighbour's previous sweep, store their boundary planes into its
+ * ghost planes and signal, while the sweeps follow each other through
+ * device-side neighbourhood counts (no launch gap or wave tail between
+ * periods). sims[0..n): n = 1, one rank's slab (its neighbours make the same
+ * call on their GPUs); n = 2..8, linked slabs of ONE device run in the same
+ * launch (the one-GPU emulation of n ranks — never separate launches that
+ * wait on each other). Two-step variant, no probes; starts, like
+ * yb_peer_step, after one yb_peer_push of the current state. Extension (the
+ * reference has no multi-GPU path). */
+int yb_peer_run(yb_sim* const* sims, int n, int64_t nsteps);
 int yb_halo_pack(yb_sim* sim, int side, void* dst_device);
 int yb_halo_unpack(yb_sim* sim, int side, const void* src_device);
 

@@ -43,6 +43,7 @@ ABI_SYMBOLS = (
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
     "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
     "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait", "yb_peer_step",
+    "yb_peer_run",
     "yb_fs_apply", "yb_fs_total_energy",
 )
 
@@ -142,6 +143,7 @@ def lib():
         L.yb_peer_push.argtypes = [vp, C.c_int]
         L.yb_peer_wait.argtypes = [vp]
         L.yb_peer_step.argtypes = [vp, C.c_int64]
+        L.yb_peer_run.argtypes = [C.POINTER(vp), C.c_int, C.c_int64]
         L.yb_total_energy.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
         L.yb_halo_bytes.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
         L.yb_halo_pack.argtypes = [vp, C.c_int, vp]
@@ -336,6 +338,11 @@ class Simulation:
         boundary planes straight into the neighbours' ghost planes)."""
         _check(lib().yb_peer_step(self._h, nsteps))
 
+    def peer_run(self, nsteps):
+        """nsteps (even) / 2 exchange periods of this slab in ONE persistent launch
+        (chained periods; the neighbours make the same call on their GPUs)."""
+        peer_run([self], nsteps)
+
     def run_timed(self, nsteps):
         ms = C.c_float()
         _check(lib().yb_advance_timed(self._h, nsteps, C.byref(ms)))
@@ -425,6 +432,13 @@ class Simulation:
 
 
 OP_UPDATE_E, OP_UPDATE_H, OP_ZERO, OP_AMPERE, OP_FARADAY, OP_PEC = range(6)
+
+
+def peer_run(sims, nsteps):
+    """yb_peer_run: chained exchange periods of 1..8 linked slabs. Several slabs of one
+    device (yb_peer_link) run in ONE launch — the one-GPU emulation of that many ranks."""
+    hs = (C.c_void_p * len(sims))(*[s._h for s in sims])
+    _check(lib().yb_peer_run(hs, len(sims), nsteps))
 
 
 def fs_apply(fields, cd, op, comp=0, box=None, device=0):

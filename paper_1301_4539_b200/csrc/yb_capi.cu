@@ -172,6 +172,9 @@ struct yb_sim {
   unsigned long long* qskipped = nullptr;  // device counter of skipped items
   int* werr = nullptr;        // wait-error record of the bounded spin waits (yb::WaitErr, 8 ints)
   unsigned long long wait_ns = 20000000000ull;  // their deadline (YB_WAIT_TIMEOUT_MS, default 20 s)
+  // chained exchange periods (yb_peer_run, two-step kernel MODE 4)
+  unsigned* pcnt4 = nullptr;            // per side and sweep: boundary row warps done (2 x kChainSweeps)
+  cudaEvent_t chain_ev = nullptr;
 };
 
 namespace {
@@ -893,6 +896,8 @@ int yb_destroy(yb_sim* s) {
   for (int q = 0; q < 6; ++q) cudaFree(s->axis_dev[q]);
   cudaFree(s->sched);
   cudaFree(s->sched2);
+  if (s->pcnt4) cudaFree(s->pcnt4);
+  if (s->chain_ev) cudaEventDestroy(s->chain_ev);
   cudaFree(s->werr);
   if (s->side) cudaStreamDestroy(s->side);
   if (s->xfer) cudaStreamDestroy(s->xfer);
@@ -1900,6 +1905,184 @@ int yb_peer_step(yb_sim* s, int64_t nsteps) {
   if (int rc = yb_advance_begin(s, nsteps)) return rc;  // one step: split sweep + push
   if (int rc = yb_peer_push(s, 0)) return rc;
   return yb_advance_end(s);
+}
+
+// Chained exchange periods: nsteps / 2 two-step periods of one slab (a rank:
+// n = 1, its neighbours run the same call on their GPUs) or of n linked slabs
+// of this device (the one-GPU emulation of n ranks) in ONE persistent launch
+// (k_tb2 MODE 4): per sweep, the boundary z-chunks' items wait for the
+// neighbours' previous sweep, store their boundary planes into the neighbours'
+// ghost planes and signal; the sweeps follow each other through MODE 2's
+// device-side neighbourhood counts. Needs the first exchange (yb_peer_push)
+// done, like yb_peer_step.
+namespace {
+constexpr int kChainSweeps = 1024;  // sweeps per launch (longer runs take several launches)
+
+int chain_zchunk(const yb_sim* s) {  // the multi-sweep chunk, with both end chunks >= 2 planes
+  const int nz = s->g.nz;
+  int len = s->zchunk2p > 0 ? s->zchunk2p : s->zchunk2;
+  len = std::max(2, std::min(len, nz));
+  while (len < nz && nz % len == 1) ++len;  // a 1-plane top chunk cannot hold the folded exchange
+  return len;
+}
+}  // namespace
+
+int yb_peer_run(yb_sim* const* sims, int n, int64_t nsteps) {
+  if (!sims || n < 1 || n > yb::kChainMax) return fail(YB_INVALID_ARGUMENT, "1 .. %d slabs", yb::kChainMax);
+  if (nsteps < 2 || (nsteps & 1)) return fail(YB_INVALID_ARGUMENT, "chained periods advance an even step count");
+  yb_sim* s0 = sims[0];
+  for (int i = 0; i < n; ++i) {
+    yb_sim* s = sims[i];
+    if (!s) return fail(YB_INVALID_ARGUMENT, "null handle");
+    // (a handle without peers is a chain of one: plain multi-sweep periods through this path)
+    if (s->variant != YB_VARIANT_TB2) return fail(YB_INVALID_ARGUMENT, "chained periods need the two-step kernel");
+    if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight");
+    if (!s->probes.empty()) return fail(YB_INVALID_ARGUMENT, "probes sample single steps: use yb_peer_step");
+    if (s->device != s0->device || s->g.nx != s0->g.nx || s->g.ny != s0->g.ny || cell_mask(s) != cell_mask(s0))
+      return fail(YB_INVALID_ARGUMENT, "slabs of one launch share device, x/y extents and coefficient set");
+    if (s->g.nz < 2) return fail(YB_INVALID_ARGUMENT, "slab %d thinner than the two-plane exchange", i);
+    for (int j = 0; j < i; ++j)
+      if (sims[j] == s) return fail(YB_INVALID_ARGUMENT, "slab %d listed twice", i);
+  }
+  YB_CU(cudaSetDevice(s0->device));
+  if (!s0->chain_ev) YB_CU(cudaEventCreateWithFlags(&s0->chain_ev, cudaEventDisableTiming));
+  for (int i = 0; i < n; ++i) {
+    yb_sim* s = sims[i];
+    if (int rc = prepare_fused(s)) return rc;
+    if (!s->pcnt4) YB_CU(cudaMalloc(&s->pcnt4, 2 * kChainSweeps * sizeof(unsigned)));
+    if (s->peer_inflight) {  // a push still reading my planes
+      YB_CU(cudaStreamWaitEvent(s0->stream, s->peer_done, 0));
+      s->peer_inflight = false;
+    }
+    if (s != s0) {  // everything queued on the other slabs' streams comes first
+      if (!s->chain_ev) YB_CU(cudaEventCreateWithFlags(&s->chain_ev, cudaEventDisableTiming));
+      YB_CU(cudaEventRecord(s->chain_ev, s->stream));
+      YB_CU(cudaStreamWaitEvent(s0->stream, s->chain_ev, 0));
+    }
+  }
+  cudaStream_t st = s0->stream;
+  for (int64_t done = 0; done < nsteps;) {
+    const int K = (int)std::min<int64_t>((nsteps - done) / 2, kChainSweeps);
+    std::vector<yb::ChainSlab> cs(n);
+    yb::FusedArgs c{};  // the launch's own arguments: schedule and the chain
+    c.nchain = n;
+    for (int i = 0; i < n; ++i) {
+      yb_sim* s = sims[i];
+      const int nxt = s->cur ^ 1;
+      yb::FusedArgs& a = cs[i].a;
+      a = yb::FusedArgs{};
+      a.g = s->g;
+      a.nstages = s->stages2;
+      a.ntx = s->ntx;
+      a.nty = s->nty;
+      set_chunks(s, a, chain_zchunk(s), zfull(s));
+      a.nsweeps = K;
+      a.err = s->werr;
+      a.wait_ns = s->wait_ns;
+      for (int q = 0; q < 6; ++q) {  // even sweeps write nxt, odd ones cur: the neighbours' same buffers
+        a.pdn[q] = s->peer[0].on ? s->peer[0].buf[nxt][q] : nullptr;
+        a.pup[q] = s->peer[1].on ? s->peer[1].buf[nxt][q] : nullptr;
+        a.pdn_o[q] = s->peer[0].on ? s->peer[0].buf[s->cur][q] : nullptr;
+        a.pup_o[q] = s->peer[1].on ? s->peer[1].buf[s->cur][q] : nullptr;
+      }
+      a.pdn_k0 = s->peer[0].nz;
+      a.pfold = 1;
+      a.pflag = s->pflags;
+      a.pneed = s->push_count;
+      a.psig_val = s->push_count + 1;
+      a.psig[0] = s->peer[0].on ? s->peer[0].flags + 1 : nullptr;
+      a.psig[1] = s->peer[1].on ? s->peer[1].flags + 0 : nullptr;
+      a.pcnt = s->pcnt4;
+      YB_CU(cudaMemsetAsync(s->pcnt4, 0, 2 * (size_t)K * sizeof(unsigned), st));
+      a.perr = s->werr;
+      if (s->done_n != a.nitems) {
+        cudaFree(s->done);
+        s->done = nullptr;
+        YB_CU(cudaMalloc(&s->done, (size_t)a.nitems * sizeof(unsigned)));
+        YB_CU(cudaMemsetAsync(s->done, 0, (size_t)a.nitems * sizeof(unsigned), st));
+        s->done_n = a.nitems;
+        s->epoch = 0;
+      }
+      if (s->srcs_cap < K) {
+        cudaFree(s->srcs_dev);
+        s->srcs_dev = nullptr;
+        YB_CU(cudaMalloc(&s->srcs_dev, (size_t)K * sizeof(yb::SrcArgs)));
+        s->srcs_cap = K;
+      }
+      std::vector<yb::SrcArgs> sv(K);
+      for (int q = 0; q < K; ++q) sv[q] = sources_at(s, s->step_index + 2 * q, true);
+      YB_CU(cudaMemcpyAsync(s->srcs_dev, sv.data(), sv.size() * sizeof(yb::SrcArgs), cudaMemcpyHostToDevice, st));
+      a.done = s->done;
+      a.epoch = s->epoch;
+      a.srcs = s->srcs_dev;
+      a.no_faces = 0;
+      a.store_policy = 1;
+      a.co = coef_args(s);
+      for (int q = 0; q < 6; ++q) {
+        a.in[q] = s->buf[s->cur][q];
+        a.out[q] = s->buf[nxt][q];
+      }
+      a.src = sources_at(s, s->step_index, true);
+      a.skipped = s->qskipped;
+      cs[i].tm = s->tm2[s->cur];
+      cs[i].tm_o = s->tm2[nxt];
+      c.chain_off[i + 1] = c.chain_off[i] + a.nitems;
+    }
+    c.g = s0->g;
+    c.nstages = s0->stages2;
+    c.pf = s0->pf2;
+    c.ntx = s0->ntx;
+    c.nty = s0->nty;
+    c.nsweeps = K;
+    c.nitems = c.chain_off[n];
+    c.sched = s0->sched;
+    c.sched_base = s0->sched_base;
+    c.err = s0->werr;
+    c.wait_ns = s0->wait_ns;
+    const int mask = cell_mask(s0);
+    const size_t smem = yb::tb2_smem_bytes(mask, s0->stages2);
+    const dim3 grid(std::min(c.nitems, s0->num_sms), 1, 1);
+    TimerPair* tp = nullptr;
+    if (s0->timing) {
+      if (s0->timers_used == s0->timers.size()) {
+        TimerPair p;
+        YB_CU(cudaEventCreate(&p.a));
+        YB_CU(cudaEventCreate(&p.b));
+        s0->timers.push_back(p);
+      }
+      tp = &s0->timers[s0->timers_used++];
+      YB_CU(cudaEventRecord(tp->a, st));
+    }
+    if (n == 1) {  // a rank's launch: the slab's own arguments as the kernel's, maps as parameters
+      yb::FusedArgs a1 = cs[0].a;
+      a1.nchain = 1;
+      a1.chain_off[0] = 0;
+      a1.chain_off[1] = a1.nitems;
+      a1.nsweeps = K;
+      a1.sched = c.sched;
+      a1.sched_base = c.sched_base;
+      a1.pf = c.pf;
+      YB_CU(yb::launch_tb2(a1, cs[0].tm, cs[0].tm_o, mask, grid, smem, st));
+    } else {
+      YB_CU(yb::launch_tb2_chain(c, cs.data(), n, mask, grid, smem, st));
+    }
+    if (tp) YB_CU(cudaEventRecord(tp->b, st));
+    s0->sched_base += (unsigned long long)c.nitems * K + grid.x;
+    s0->launches += 1;
+    for (int i = 0; i < n; ++i) {
+      yb_sim* s = sims[i];
+      s->epoch += (unsigned)K;
+      s->push_count += (unsigned)K;
+      s->step_index += 2 * K;
+      s->steps += 2 * K;
+      if (K & 1) s->cur ^= 1;
+      s->q_valid = false;  // MODE 4 does not maintain the quiescent map
+    }
+    done += 2 * K;
+  }
+  YB_CU(cudaEventRecord(s0->chain_ev, st));
+  for (int i = 1; i < n; ++i) YB_CU(cudaStreamWaitEvent(sims[i]->stream, s0->chain_ev, 0));
+  return YB_OK;
 }
 
 int yb_peer_wait(yb_sim* s) {

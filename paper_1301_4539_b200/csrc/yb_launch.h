@@ -69,7 +69,7 @@ inline int tb2_stage_floats(int cell_mask) {
 
 inline size_t tb2_smem_bytes(int cell_mask, int stages) {
   return (size_t)stages * tb2_stage_floats(cell_mask) * 4 + (size_t)(kTB2E1 + kTB2H1 + kTB2E2 + kTB2Edge) * 4 +
-         (size_t)stages * 16 + 16 * 4;  // mbarriers, item + sweep queues
+         (size_t)stages * 16 + 24 * 4;  // mbarriers, item + sweep + slab queues
 }
 
 struct TMaps {
@@ -130,6 +130,29 @@ struct FusedArgs {
   unsigned* pcnt;                // per side: boundary items completed (monotonic)
   unsigned pcnt_base[2];         // their values at this launch's start
   int* perr;                     // wait-error record of a timed-out neighbour wait
+  // Chained exchange periods (two-step kernel MODE 4): nsweeps periods of one
+  // or several linked slabs in ONE persistent launch — MODE 2's device-side
+  // sweep dependencies plus MODE 3's folded peer stores / waits / signals per
+  // sweep. Sweep s stores its boundary planes into the neighbour's buffers of
+  // s's output parity (pdn/pup for even s, pdn_o/pup_o for odd s), its
+  // boundary items wait for the neighbour's flag >= pneed + s, and the last
+  // of a side's row warps of sweep s (counter pcnt[side * nsweeps + s], zeroed
+  // per launch) publishes psig_val + s. The launch's own arguments carry
+  // nchain slabs (their arguments and read maps are kernel parameters next to
+  // these: ChainParams, yb_tb2.cu) and chain_off (items of slabs 0..k-1 per
+  // sweep); work item v = (sweep, slab, item). nchain > 1 runs several slabs of
+  // one GPU in one launch — the one-GPU emulation of the multi-GPU schedule; a
+  // rank runs nchain = 1.
+  float* pdn_o[6];
+  float* pup_o[6];
+  int nchain;
+  int chain_off[9];
+};
+
+constexpr int kChainMax = 8;
+struct ChainSlab {
+  FusedArgs a;
+  TMaps tm, tm_o;  // read maps of the launch's even / odd sweeps
 };
 
 // Wait-error record, 8 ints per handle: [0] code (0 none; WAIT_DEP: a
@@ -173,6 +196,10 @@ cudaError_t launch_fused(const FusedArgs& a, const TMaps& tm, int cell_mask, dim
                          size_t smem, cudaStream_t st);
 cudaError_t fused_set_smem_limits();
 // Two full steps per launch (maps with kTB2BY-row boxes).
+// MODE 4: a = the launch's schedule (nsweeps, nchain, chain_off, sched, ...),
+// slabs[0..n) every slab's own arguments and read maps.
+cudaError_t launch_tb2_chain(const FusedArgs& a, const ChainSlab* slabs, int n, int cell_mask, dim3 grid,
+                             size_t smem, cudaStream_t st);
 cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, const TMaps& tm_out, int cell_mask, dim3 grid,
                        size_t smem, cudaStream_t st);
 cudaError_t tb2_set_smem_limits();

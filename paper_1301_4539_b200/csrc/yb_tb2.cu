@@ -28,7 +28,10 @@
 // (every row warp adds 1 to done[item] after a fence; no item-end barrier);
 // 3 z-slab peer stores — boundary planes also stored into the neighbours'
 // ghost planes, boundary chunks handed out first, in-kernel wait on the
-// neighbours' flags and a per-side row-warp count whose last member signals.
+// neighbours' flags and a per-side row-warp count whose last member signals;
+// 4 chained exchange periods — 2 and 3 together: several sweeps of one or
+// several linked slabs in one launch, per-sweep peer waits and signals
+// (FusedArgs::chain; several slabs = the one-GPU emulation of N ranks).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -293,8 +296,9 @@ struct Cursor {
 // shared memory (column c-1 / c+4; the edge columns for lanes 0 / 31).
 template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
 struct Rows {
-  // MODE: 0 plain, 1 quiescent skip, 2 several sweeps per launch, 3 peer stores
-  static constexpr bool QS = MODE == 1, MS = MODE == 2, PS = MODE == 3;
+  // MODE: 0 plain, 1 quiescent skip, 2 several sweeps per launch, 3 peer stores,
+  // 4 several sweeps with peer stores (chained exchange periods)
+  static constexpr bool QS = MODE == 1, MS = MODE == 2 || MODE == 4, PS = MODE == 3 || MODE == 4;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   static constexpr int E1C = RW * BX, E1B = 3 * E1C;              // comp / buffer strides
   static constexpr int H1C = (RW - 1) * BX, H1B = 3 * H1C;
@@ -308,7 +312,6 @@ struct Rows {
   const SrcArgs& srcm;  // this sweep's sources (MS)
   const int er, l, j, c, i0;
   const bool xedge;
-  const bool pitem;  // MODE 3: this item owns boundary planes a neighbour mirrors
   const uint64_t st_pol;
   float* const e1o;  // E1 buffer 0, comp 0, row er, column c
   float* const h1o;  // H1 buffer 0, comp 0, row er, column c
@@ -325,7 +328,7 @@ struct Rows {
                                   float* const* out_, const SrcArgs& src_, int er_, int l_, uint64_t pol)
       : a(a_), it(it_), B(B_), cur(cur_), outm(out_), srcm(src_), er(er_), l(l_), j(it_.y0 - 1 + er_), c(4 + 4 * l_),
         i0(it_.x0 + 4 * l_), xedge(i0 == 0 || i0 + 4 > a_.g.nx),
-        pitem(PS && ((it_.kz0 < 2 && a_.pdn[0]) || (it_.kz1 > a_.g.nz - 2 && a_.pup[0]))), st_pol(pol),
+        st_pol(pol),
         e1o(B_.e1b + er_ * BX + c), h1o(B_.h1b + er_ * BX + c), e2o(B_.e2b + (er_ - 1) * BX + c) {
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     cdy_e = a.co.cdy_e[max(j, 0)];
@@ -341,22 +344,6 @@ struct Rows {
 
   __device__ __forceinline__ float* const* outs() const { return MS ? outm : a.out; }
 
-  // peer-store mode: an owned row of boundary plane k also goes to the neighbour's ghost plane
-  __device__ __forceinline__ void peer_rows(int c0, int k, const F4x3& v) {
-    const Geo& g = a.g;
-    float* const* dst = nullptr;
-    int kp = 0;
-    if (k < 2 && a.pdn[0]) {
-      dst = a.pdn;
-      kp = a.pdn_k0 + k;
-    } else if (k >= g.nz - 2 && a.pup[0]) {
-      dst = a.pup;
-      kp = k - g.nz;
-    }
-    if (!dst) return;
-    const long long gp = gidx(g, i0, j, kp);
-    store_rows3(dst + c0, gp, i0, g.nx, v.x, v.y, v.z, st_pol);
-  }
   __device__ __forceinline__ const SrcArgs& src() const { return MS ? srcm : a.src; }
 
   __device__ __forceinline__ void prologue() {
@@ -475,7 +462,6 @@ struct Rows {
       if (own) {  // E^{n+2} of the owned rows -> HBM
         const long long gp = gidx(g, i0, j, kh);
         store_rows3(outs(), gp, i0, g.nx, e2c.x, e2c.y, e2c.z, st_pol);
-        if (PS && pitem) peer_rows(0, kh, e2c);
       }
       if (QS) {
         const bool nz = own && (nonzero4(e2c.x) | nonzero4(e2c.y) | nonzero4(e2c.z));
@@ -510,7 +496,6 @@ struct Rows {
       if (j < g.ny) {
         const long long gp = gidx(g, i0, j, k4);
         store_rows3(outs() + 3, gp, i0, g.nx, h2.x, h2.y, h2.z, st_pol);
-        if (PS && pitem) peer_rows(3, k4, h2);
       }
       if (QS && j < g.ny) {
         const bool nz = nonzero4(h2.x) | nonzero4(h2.y) | nonzero4(h2.z);
@@ -540,6 +525,43 @@ __device__ __forceinline__ void tb2_rows(const FusedArgs& a, const Item& it, con
   Rows<CAC, CBC, DAC, DBC, MODE> R(a, it, B, cur, out, src, er, l, st_pol);
   if (it.pro) R.prologue();
   for (int p = it.pstart; p <= it.pend; ++p) R.plane(p);
+}
+
+// Peer stores (MODE 3 / 4), after a boundary item's sweep: row warp er copies
+// its own rows (y0..y0+7) of the slab's boundary planes — 0, 1 below, nz-2,
+// nz-1 above — of all six next-state components from its own output (just
+// written by this thread; read back from L2) into the neighbour's ghost
+// planes, over NVLink across GPUs. Outside the plane loop, so the sweep's
+// registers are not taxed by the exchange.
+__device__ __noinline__ void peer_copy_rows(const FusedArgs& a, const Item& it, float* const* out,
+                                            float* const* dn, float* const* up, int er, int l, uint64_t pol) {
+  const Geo& g = a.g;
+  const int j = it.y0 - 1 + er, i0 = it.x0 + 4 * l;
+  if (er < 1 || er > kTB2Rows || j >= g.ny || i0 >= g.nx) return;
+  for (int side = 0; side < 2; ++side) {
+    float* const* dst = side == 0 ? dn : up;
+    if (!dst[0]) continue;
+    for (int q = 0; q < 2; ++q) {
+      const int k = side == 0 ? q : g.nz - 2 + q;  // my boundary plane
+      if (k < it.kz0 || k >= it.kz1) continue;     // not this item's
+      const int kp = side == 0 ? a.pdn_k0 + k : k - g.nz;
+      const long long src = gidx(g, i0, j, k), dstp = gidx(g, i0, j, kp);
+      float4 v[6];
+      if (i0 + 3 < g.nx) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) v[c] = __ldcg(reinterpret_cast<const float4*>(out[c] + src));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = 0; e < 4; ++e)
+            if (i0 + e < g.nx) el(v[c], e) = __ldcg(out[c] + src + e);
+        }
+      }
+      store_rows3(dst, dstp, i0, g.nx, v[0], v[1], v[2], pol);
+      store_rows3(dst + 3, dstp, i0, g.nx, v[3], v[4], v[5], pol);
+    }
+  }
 }
 
 // ============================================================= edge warp
@@ -662,10 +684,15 @@ __device__ __forceinline__ void tb2_edge(const FusedArgs& a, const Item& it, con
   }
 }
 
-template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
-__global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm,
-                                       const __grid_constant__ TMaps tm_o) {
-  constexpr bool QS = MODE == 1, MS = MODE == 2, PS = MODE == 3;
+// The kernel body. MODE 4 with CHP: several slabs, `chain` points at their
+// arguments in parameter space (ChainParams) and every per-item field access
+// is a constant-bank load with a register offset; without CHP (one slab, a
+// rank's launch) `a` is the slab itself and its fields stay immediate
+// constant operands, as in the other modes.
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE, bool CHP>
+__device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, const TMaps& tm_o,
+                                         const ChainSlab* chain) {
+  constexpr bool QS = MODE == 1, MS = MODE == 2 || MODE == 4, PS = MODE == 3 || MODE == 4, CH = MODE == 4;
   using L = StageLayout<CAC, CBC, DAC, DBC>;
   constexpr int NARR = 6 + CAC + CBC + DAC + DBC;
   constexpr uint32_t kBytesF = kBX * kTB2BY * 4, kBytesE = kBX * kTB2RowsE * 4, kBytesC = kBX * kTB2RowsCA * 4,
@@ -687,6 +714,7 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
   B.empty = B.full + S;
   int* item_q = reinterpret_cast<int*>(B.empty + S);
   int* sweep_q = item_q + kQ;
+  int* slab_q = sweep_q + kQ;  // MODE 4: the item's slab in a.chain
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int T = a.ntx * a.nty;
 
@@ -703,6 +731,19 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
     // (no sweep reads them for a valid update, so all sweeps' steps are applied
     // here in order, into the buffer that holds the launch's final state)
     if (a.no_faces) return;
+    if (CH) {  // every slab of the chain, all sweeps in order, into its final-state buffer
+      for (int sl = 0; sl < a.nchain; ++sl) {
+        const FusedArgs& A = CHP ? chain[sl].a : a;
+        const long long nf = face_points(A.g);
+        float* const* fin =
+            (a.nsweeps & 1) ? A.out : const_cast<float* const*>(reinterpret_cast<const float* const*>(A.in));
+        for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {
+          face_point(A.g, A.in, fin, A.co, t);
+          for (int q = 1; q < 2 * a.nsweeps; ++q) face_point(A.g, fin, fin, A.co, t);
+        }
+      }
+      return;
+    }
     const long long nf = face_points(g);
     if (!MS) {
       for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {
@@ -721,15 +762,25 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
 
   if (w == PROD) {  // TMA producer (one lane)
     if (l != 0) return;
-    int p_item = -1, p_e = 0, p_nE = 0, p_seq = 0, p_sweep = 0;
+    int p_item = -1, p_e = 0, p_nE = 0, p_seq = 0, p_sweep = 0, p_slab = 0;
     for (int q = 0;; ++q) {
       const int s = q % S;
       if (q >= S) mbar_wait(smem_u32(&B.empty[s]), (uint32_t)(((q / S) - 1) & 1));
       const uint32_t bar = smem_u32(&B.full[s]);
       if (p_item < 0) {
         const unsigned long long v = atomicAdd(a.sched, 1ull) - a.sched_base;
-        int it = -1, sw = 0;
-        if (!MS) {
+        int it = -1, sw = 0, sl = 0;
+        if (CH) {  // (sweep, slab, item) in z order: the chunks of all slabs, bottom to top, per sweep
+          // (not MODE 3's boundary-chunks-first order: with several sweeps in flight that
+          // would make each sweep's top chunk wait for the previous sweep's last chunk)
+          const unsigned long long tot = (unsigned long long)a.chain_off[a.nchain];
+          if (v < tot * a.nsweeps) {
+            sw = (int)(v / tot);
+            const int r = (int)(v - (unsigned long long)sw * tot);
+            while (sl + 1 < a.nchain && r >= a.chain_off[sl + 1]) ++sl;
+            it = r - a.chain_off[sl];
+          }
+        } else if (!MS) {
           it = v < (unsigned long long)a.nitems ? (int)v : -1;
           if (PS && it >= 0 && a.pfold) {  // bottom chunk, top chunk, then the interior
             const int nch = a.nitems / T, q = it / T, tile = it - q * T;
@@ -746,17 +797,27 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         }
         item_q[p_seq % kQ] = it;
         if (MS) sweep_q[p_seq % kQ] = sw;
+        if (CH) slab_q[p_seq % kQ] = sl;
         ++p_seq;
         if (it < 0) {
           mbar_arrive(bar);
           return;
         }
+        const FusedArgs& A = CHP ? chain[sl].a : a;
         if (MS && sw > 0) {  // the neighbourhood must have finished the previous sweep
-          wait_neighbours(a, it, sw);
+          wait_neighbours(A, it, sw);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
         }
+        if (CH) {  // a boundary item: the neighbour's sweep sw-1 has stored my ghost planes
+          const int nch = A.nitems / T, ch = it / T;
+          const bool wd = ch == 0 && A.pdn[0], wu = ch == nch - 1 && A.pup[0];
+          if (wd) peer_flag_wait(A.pflag, A.pneed + (unsigned)sw, A.perr, A.wait_ns, it, 0);
+          if (wu) peer_flag_wait(A.pflag + 1, A.pneed + (unsigned)sw, A.perr, A.wait_ns, it, 1);
+          if (wd || wu) asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         p_sweep = sw;
-        const Item pi = make_item(a, g, it, T, a.ntx);
+        p_slab = sl;
+        const Item pi = make_item(A, A.g, it, T, a.ntx);
         if (QS) {  // quiescent item: input box all +0, no source in either step -> skip
           const int tl = it % T;
           const int k0 = pi.pro ? pi.pstart - 1 : pi.pstart;
@@ -772,10 +833,12 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
         p_e = 0;
         p_nE = (pi.pro ? 1 : 0) + pi.pin_end - pi.pstart + 1;
       }
-      const Item pi = make_item(a, g, p_item, T, a.ntx);
+      const FusedArgs& PA = CHP ? chain[p_slab].a : a;
+      const Item pi = make_item(PA, PA.g, p_item, T, a.ntx);
       const int x0 = pi.x0, y0 = pi.y0;
       const int pro = pi.pro ? 1 : 0;
-      const TMaps& M = (MS && (p_sweep & 1)) ? tm_o : tm;  // this sweep's input state
+      const TMaps& M = CHP ? ((p_sweep & 1) ? chain[p_slab].tm_o : chain[p_slab].tm)
+                           : ((MS && (p_sweep & 1)) ? tm_o : tm);  // this sweep's input state
       float* dst = B.stages + (size_t)s * L::floats;
       // tensor z coordinate = local plane + kGhost
       if (pro && p_e == 0) {  // hx, hy of plane pstart-1
@@ -816,21 +879,47 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
     cur.peeked = true;
     const int item = item_q[c_seq % kQ];
     const int sw = MS ? sweep_q[c_seq % kQ] : 0;
+    const FusedArgs& A = CHP ? chain[slab_q[c_seq % kQ]].a : a;
     ++c_seq;
     if (item < 0) break;
     if (QS && (item & kSkipItem)) {  // quiescent: consume the empty stage, nothing to write
       release_stage(B.empty, cur.wait(B, S), l);
       continue;
     }
-    const SrcArgs& src = MS ? a.srcs[sw] : a.src;
-    float* const* out = (MS && (sw & 1)) ? const_cast<float* const*>(reinterpret_cast<const float* const*>(a.in)) : a.out;
-    Item it = make_item(a, g, item, T, a.ntx);
+    const SrcArgs& src = MS ? A.srcs[sw] : A.src;
+    float* const* out = (MS && (sw & 1)) ? const_cast<float* const*>(reinterpret_cast<const float* const*>(A.in)) : A.out;
+    Item it = make_item(A, A.g, item, T, a.ntx);
     mark_sources(src, it);
     if (w == EDGE)
-      tb2_edge<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, src, l);
+      tb2_edge<CAC, CBC, DAC, DBC, MODE>(A, it, B, cur, src, l);
     else
-      tb2_rows<CAC, CBC, DAC, DBC, MODE>(a, it, B, cur, out, src, w, l, st_pol);
-    if (PS) {  // boundary item: its peer stores before the signal
+      tb2_rows<CAC, CBC, DAC, DBC, MODE>(A, it, B, cur, out, src, w, l, st_pol);
+    if (PS && w < RW) {  // an item's rows of the slab's boundary planes -> the neighbours' ghost planes
+      // (by plane, not by chunk: unfolded MODE 3 launches may cut 1-plane chunks)
+      if ((it.kz0 < 2 && A.pdn[0]) || (it.kz1 > A.g.nz - 2 && A.pup[0])) {
+        const bool odd = CH && (sw & 1);  // MODE 4: the neighbours' buffers of this sweep's output parity
+        peer_copy_rows(A, it, out, odd ? A.pdn_o : A.pdn, odd ? A.pup_o : A.pup, w, l, st_pol);
+      }
+    }
+    if (CH) {  // boundary item: per sweep and side, the last row warp signals the neighbour
+      const int ch = item / T, nch = A.nitems / T;
+      const bool bd = ch == 0 && A.pdn[0], bu = ch == nch - 1 && A.pup[0];
+      if ((bd || bu) && w < RW) {
+        __syncwarp();
+        if (l == 0) {
+          __threadfence_system();
+          const unsigned last = (unsigned)T * RW - 1u, val = A.psig_val + (unsigned)sw;
+          if (bd && atomicAdd(A.pcnt + sw, 1u) == last) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.psig[0]), "r"(val) : "memory");
+          }
+          if (bu && atomicAdd(A.pcnt + a.nsweeps + sw, 1u) == last) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.psig[1]), "r"(val) : "memory");
+          }
+        }
+      }
+    } else if (PS) {  // boundary item: its peer stores before the signal
       const int ch = item / T, nch = a.nitems / T;
       const bool bd = ch == 0 && a.pdn[0], bu = ch == nch - 1 && a.pup[0];
       if (bd || bu) {
@@ -860,10 +949,40 @@ __global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, cons
       __syncwarp();
       if (l == 0) {
         __threadfence();
-        atomicAdd(a.done + item, 1u);
+        atomicAdd(A.done + item, 1u);
       }
     }
   }
+}
+
+template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
+__global__ void __maxnreg__(128) k_tb2(const __grid_constant__ FusedArgs a, const __grid_constant__ TMaps tm,
+                                       const __grid_constant__ TMaps tm_o) {
+  tb2_body<CAC, CBC, DAC, DBC, MODE, false>(a, tm, tm_o, nullptr);
+}
+
+// MODE 4: the launch's schedule arguments and every slab's arguments and read
+// maps as kernel parameters (8 x 3.5 KB + 0.9 KB, within the 32 KB limit)
+struct ChainParams {
+  FusedArgs a;
+  ChainSlab s[kChainMax];
+};
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+__global__ void __maxnreg__(128) k_tb2_chain(const __grid_constant__ ChainParams P) {
+  tb2_body<CAC, CBC, DAC, DBC, 4, true>(P.a, P.s[0].tm, P.s[0].tm_o, P.s);
+}
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+cudaError_t launch_chain_t(const ChainParams& P, dim3 grid, size_t smem, cudaStream_t st) {
+  k_tb2_chain<CAC, CBC, DAC, DBC><<<grid, kTB2Threads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <bool CAC, bool CBC, bool DAC, bool DBC>
+cudaError_t set_limit_chain_t() {
+  return cudaFuncSetAttribute(k_tb2_chain<CAC, CBC, DAC, DBC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024);
 }
 
 template <bool CAC, bool CBC, bool DAC, bool DBC, int MODE>
@@ -882,15 +1001,24 @@ cudaError_t set_limit_t() {
 using LaunchFn = cudaError_t (*)(const FusedArgs&, const TMaps&, const TMaps&, dim3, size_t, cudaStream_t);
 using LimitFn = cudaError_t (*)();
 
-// index: bits 0-3 per-cell Ca/Cb/Da/Db, then 16 * MODE
+// index: bits 0-3 per-cell Ca/Cb/Da/Db, then 16 * MODE (0..4)
 #define YB_B(m) (m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m >> 4)
 #define YB_T(m) launch_t<YB_B(m)>
 #define YB_L(m) set_limit_t<YB_B(m)>
 #define YB_8(F, b) F(b), F(b + 1), F(b + 2), F(b + 3), F(b + 4), F(b + 5), F(b + 6), F(b + 7)
-const LaunchFn kLaunch[64] = {YB_8(YB_T, 0),  YB_8(YB_T, 8),  YB_8(YB_T, 16), YB_8(YB_T, 24),
-                              YB_8(YB_T, 32), YB_8(YB_T, 40), YB_8(YB_T, 48), YB_8(YB_T, 56)};
-const LimitFn kLimit[64] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16), YB_8(YB_L, 24),
-                            YB_8(YB_L, 32), YB_8(YB_L, 40), YB_8(YB_L, 48), YB_8(YB_L, 56)};
+const LaunchFn kLaunch[80] = {YB_8(YB_T, 0),  YB_8(YB_T, 8),  YB_8(YB_T, 16), YB_8(YB_T, 24),
+                              YB_8(YB_T, 32), YB_8(YB_T, 40), YB_8(YB_T, 48), YB_8(YB_T, 56),
+                              YB_8(YB_T, 64), YB_8(YB_T, 72)};
+const LimitFn kLimit[80] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16), YB_8(YB_L, 24),
+                            YB_8(YB_L, 32), YB_8(YB_L, 40), YB_8(YB_L, 48), YB_8(YB_L, 56),
+                            YB_8(YB_L, 64), YB_8(YB_L, 72)};
+using ChainFn = cudaError_t (*)(const ChainParams&, dim3, size_t, cudaStream_t);
+#define YB_C(m) launch_chain_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
+#define YB_CL(m) set_limit_chain_t<(m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0>
+const ChainFn kChain[16] = {YB_8(YB_C, 0), YB_8(YB_C, 8)};
+const LimitFn kChainLimit[16] = {YB_8(YB_CL, 0), YB_8(YB_CL, 8)};
+#undef YB_C
+#undef YB_CL
 #undef YB_8
 #undef YB_T
 #undef YB_L
@@ -899,8 +1027,12 @@ const LimitFn kLimit[64] = {YB_8(YB_L, 0),  YB_8(YB_L, 8),  YB_8(YB_L, 16), YB_8
 }  // namespace
 
 cudaError_t tb2_set_smem_limits() {
-  for (int m = 0; m < 64; ++m) {
+  for (int m = 0; m < 80; ++m) {
     const cudaError_t e = kLimit[m]();
+    if (e != cudaSuccess) return e;
+  }
+  for (int m = 0; m < 16; ++m) {
+    const cudaError_t e = kChainLimit[m]();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -908,8 +1040,18 @@ cudaError_t tb2_set_smem_limits() {
 
 cudaError_t launch_tb2(const FusedArgs& a, const TMaps& tm, const TMaps& tm_out, int cell_mask, dim3 grid,
                        size_t smem, cudaStream_t st) {
-  const int mode = (a.pdn[0] || a.pup[0]) ? 3 : (a.nsweeps > 1 ? 2 : (a.qm.bits ? 1 : 0));
+  const int mode = a.nchain > 0 ? 4 : (a.pdn[0] || a.pup[0]) ? 3 : (a.nsweeps > 1 ? 2 : (a.qm.bits ? 1 : 0));
   return kLaunch[(cell_mask & 15) | (mode << 4)](a, tm, tm_out, grid, smem, st);
+}
+
+cudaError_t launch_tb2_chain(const FusedArgs& a, const ChainSlab* slabs, int n, int cell_mask, dim3 grid,
+                             size_t smem, cudaStream_t st) {
+  if (n < 1 || n > kChainMax) return cudaErrorInvalidValue;
+  thread_local ChainParams P;  // ~29 KB: not on the stack
+  P.a = a;
+  P.a.nchain = n;
+  for (int i = 0; i < n; ++i) P.s[i] = slabs[i];
+  return kChain[cell_mask & 15](P, grid, smem, st);
 }
 
 }  // namespace yb

@@ -554,6 +554,105 @@ def test_gpu_slabs_peer_step(yb, oracle, monkeypatch, fold, variant, nranks, nzg
         s.close()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks,nzg,steps,medium,fseed,zchunk", [
+    (2, 12, 10, (7, 7), 8, 0),       # thin slabs: one z-chunk each (bottom = top chunk)
+    (3, 29, 16, (7, 7), 8, 0),
+    (4, 23, 8, (4, -1), None, 0),    # zero start, point source, Cb only
+    (3, 150, 12, (7, 7), 8, 0),      # multi-chunk slabs, interior chunks between the boundary ones
+    (2, 61, 20, (-1, -1), 5, 7),     # vacuum, ragged chunks (31 = 4 x 7 + 3, 30 = 4 x 7 + 2)
+    (4, 67, 14, (7, 7), 8, 4),       # more items than CTAs per sweep
+])
+def test_gpu_slabs_peer_run_chained(yb, oracle, nranks, nzg, steps, medium, fseed, zchunk):
+    """Chained exchange periods (yb_peer_run, k_tb2 MODE 4): all slabs of the
+    decomposition run in ONE persistent launch on the one GPU — the emulation
+    of nranks ranks prescribed for fewer GPUs than ranks: every sweep's
+    boundary items wait in-kernel for the neighbour slab's previous sweep,
+    store their boundary planes into its ghost planes and signal, the sweeps
+    follow each other through the device-side neighbourhood counts. Bit-exact
+    against one domain (which itself matches the oracle, test_parity_gpu)."""
+    nx, ny = 136, 40
+    tab = oracle.gauss_table(steps + 4)
+    srcs = [(2, nx // 2, ny // 2, nzg // 2, tab)] if fseed is None else []
+    sims = []
+    for z0, n in partition(nzg, nranks):
+        s = yb.Simulation(nx, ny, n, z_offset=z0, nz_global=nzg, zchunk=zchunk, variant=TB2)
+        s.generate_medium(*medium)
+        for q in srcs:
+            s.add_source(*q)
+        if fseed is not None:
+            s.fill(fseed)
+        sims.append(s)
+    for lo, hi in zip(sims[:-1], sims[1:]):
+        lo.peer_link(1, hi)
+        hi.peer_link(0, lo)
+    for s in sims:
+        s.peer_push(False)
+    yb.peer_run(sims, steps // 2 * 2 - 2)  # one launch of several periods ...
+    yb.peer_run(sims, 2)                   # ... and one more (state, counters, flags carried over)
+    out = oracle.zeros_state(nx, ny, nzg)
+    for s in sims:
+        s.synchronize()
+        assert s.step_index == steps // 2 * 2
+        d = s.download()
+        at_top = s.z_offset + s.nz == nzg
+        for c in range(6):
+            k = s.nz + (1 if c in (0, 1, 5) and at_top else 0)
+            out[c][s.z_offset:s.z_offset + k] = d[c][:k]
+    with yb.Simulation(nx, ny, nzg) as one:
+        one.generate_medium(*medium)
+        for q in srcs:
+            one.add_source(*q)
+        if fseed is not None:
+            one.fill(fseed)
+        one.run(steps // 2 * 2)
+        want = one.download()
+    for c in range(6):
+        assert bits_equal(out[c], want[c]), c
+    for s in sims:
+        s.close()
+
+
+@pytest.mark.gpu
+def test_peer_run_errors(yb):
+    with yb.Simulation(16, 8, 6, z_offset=0, nz_global=12) as a, \
+            yb.Simulation(16, 8, 6, z_offset=6, nz_global=12) as b:
+        with pytest.raises(yb.YeeError):
+            yb.peer_run([a], 0)  # nothing to advance
+        a.peer_link(1, b)
+        b.peer_link(0, a)
+        with pytest.raises(yb.YeeError):
+            yb.peer_run([a, b], 3)  # odd step count
+        with pytest.raises(yb.YeeError):
+            yb.peer_run([a, a], 2)  # listed twice
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 3])
+def test_gpu_peer_run_single_domain(yb, oracle, n):
+    """yb_peer_run over unlinked single-domain handles: a chain of n independent
+    domains in one launch (n = 1: the rank's direct-parameter MODE 4 kernel;
+    n = 3: the parameter-array kernel of the emulation) equals yb_advance."""
+    nx, ny, nz, steps = 136, 40, 37, 8
+    sims = []
+    for q in range(n):
+        s = yb.Simulation(nx, ny, nz, variant=TB2)
+        s.generate_medium(7, 7)
+        s.fill(8 + q)
+        sims.append(s)
+    yb.peer_run(sims, steps)
+    for q, s in enumerate(sims):
+        got = s.download()
+        with yb.Simulation(nx, ny, nz) as one:
+            one.generate_medium(7, 7)
+            one.fill(8 + q)
+            one.run(steps)
+            want = one.download()
+        for c in range(6):
+            assert bits_equal(got[c], want[c]), (q, c)
+        s.close()
+
+
 def _ipc_worker(rank, world, port, result_path, variant, steps):
     """One slab per process, all on cuda:0, linked through CUDA IPC
     (PeerExchange). Ranks take turns — each period rank r steps while the
