@@ -423,8 +423,10 @@ def main():
     if exch is not None:
         config["exchange_every_steps"] = depth
         if args.exchange == "p2p":
-            config["exchange"] = ("peer memory (CUDA IPC / NVLink): the sweep kernel stores its boundary "
-                                  "planes into the neighbours' ghost planes; device-side flags")
+            config["exchange"] = ("peer memory (CUDA IPC / NVLink), chained periods: one persistent two-step "
+                                  "launch per rank for the whole timed region (yb_peer_run); per sweep the "
+                                  "boundary items wait in-kernel for the neighbours, store their boundary planes "
+                                  "into the neighbours' ghost planes and signal")
         else:
             config["halo_bytes_per_exchange_per_gpu"] = exch.bytes_per_exchange
             config["exchange"] = ("NCCL P2P, serial" if args.no_overlap else

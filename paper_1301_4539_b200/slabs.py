@@ -148,14 +148,23 @@ class PeerExchange:
             raise RuntimeError(f"peer-memory exchange unavailable on rank {bad[0][0]}: {bad[0][1]}")
 
 
-def run_steps_peer(sim, nsteps: int, depth: int):
+def run_steps_peer(sim, nsteps: int, depth: int, chained: bool = True):
     """run_steps for PeerExchange / peer_link'ed slabs: push the current
-    boundary planes once, then per exchange period one yb_peer_step — a
-    two-step sweep whose boundary-plane stores also land in the neighbours'
-    ghost planes, its bottom / top z-chunk items waiting for and signalling the
-    neighbours in-kernel (compute, exchange and ordering in one launch)."""
+    boundary planes once, then (chained, two-step kernel) ALL the run's
+    exchange periods in one persistent launch per rank (yb_peer_run: per sweep
+    the boundary items wait in-kernel for the neighbours' previous sweep, store
+    their boundary planes into the neighbours' ghost planes and signal); a
+    trailing odd step, the one-step kernel and chained=False use one
+    yb_peer_step per period instead (compute, exchange and ordering in one
+    launch each). Every rank must make the same calls: chained launches of
+    neighbouring ranks wait on each other, so they need the ranks on
+    different GPUs (or, on one GPU, yb_peer_run over all slabs at once)."""
     sim.peer_push(False)
     done = 0
+    if chained and depth == 2 and nsteps >= 2:
+        n = nsteps // 2 * 2
+        sim.peer_run(n)
+        done = n
     while done < nsteps:
         n = min(depth, nsteps - done)
         sim.peer_step(n)
