@@ -564,6 +564,27 @@ __device__ __noinline__ void peer_copy_rows(const FusedArgs& a, const Item& it, 
   }
 }
 
+// MODE 4, after a boundary item (row warps): each counts itself in its side's
+// counter of this sweep once its stores are visible system-wide; the last of
+// the side's T * RW row warps publishes psig_val + sweep to the neighbour.
+__device__ __noinline__ void chain_signal(const FusedArgs& A, int item, int T, int sw, int nsweeps, int l) {
+  const int ch = item / T, nch = A.nitems / T;
+  const bool bd = ch == 0 && A.pdn[0], bu = ch == nch - 1 && A.pup[0];
+  if (!(bd || bu)) return;
+  __syncwarp();
+  if (l != 0) return;
+  __threadfence_system();
+  const unsigned last = (unsigned)T * RW - 1u, val = A.psig_val + (unsigned)sw;
+  if (bd && atomicAdd(A.pcnt + sw, 1u) == last) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.psig[0]), "r"(val) : "memory");
+  }
+  if (bu && atomicAdd(A.pcnt + nsweeps + sw, 1u) == last) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.psig[1]), "r"(val) : "memory");
+  }
+}
+
 // ============================================================= edge warp
 // The columns the row warps' lanes cannot cover: x0-1 (CL), x0+128 (CR),
 // x0+129 (CR+1). Work is spread over the lanes as (row, column) tasks per
@@ -902,23 +923,7 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
       }
     }
     if (CH) {  // boundary item: per sweep and side, the last row warp signals the neighbour
-      const int ch = item / T, nch = A.nitems / T;
-      const bool bd = ch == 0 && A.pdn[0], bu = ch == nch - 1 && A.pup[0];
-      if ((bd || bu) && w < RW) {
-        __syncwarp();
-        if (l == 0) {
-          __threadfence_system();
-          const unsigned last = (unsigned)T * RW - 1u, val = A.psig_val + (unsigned)sw;
-          if (bd && atomicAdd(A.pcnt + sw, 1u) == last) {
-            __threadfence_system();
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.psig[0]), "r"(val) : "memory");
-          }
-          if (bu && atomicAdd(A.pcnt + a.nsweeps + sw, 1u) == last) {
-            __threadfence_system();
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.psig[1]), "r"(val) : "memory");
-          }
-        }
-      }
+      if (w < RW) chain_signal(A, item, T, sw, a.nsweeps, l);
     } else if (PS) {  // boundary item: its peer stores before the signal
       const int ch = item / T, nch = a.nitems / T;
       const bool bd = ch == 0 && a.pdn[0], bu = ch == nch - 1 && a.pup[0];
