@@ -465,7 +465,7 @@ def main():
                 cell_arrays = {q: med[q] for q in want}
             e_steps = cfg_steps
 
-            def run_e2e(qskip, upload_fields=True):
+            def run_e2e(qskip, upload_fields=True, streamed=True):
                 s2 = make_sim()
                 if table is not None:
                     s2.add_source(*src, table)
@@ -482,13 +482,16 @@ def main():
                     s2.set_cell_coeffs_many(cell_arrays)
                 if upload_fields:
                     s2.upload(host_f)
-                if ex2 is None:
-                    s2.run(e_steps)
-                elif args.exchange == "p2p":
-                    run_steps_peer(s2, e_steps, depth)
+                if ex2 is None and streamed:  # run + readback, each tile row's copies overlapping the run
+                    s2.run_to_host(e_steps, out=host_out)
                 else:
-                    run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
-                s2.download(out=host_out)
+                    if ex2 is None:
+                        s2.run(e_steps)
+                    elif args.exchange == "p2p":
+                        run_steps_peer(s2, e_steps, depth)
+                    else:
+                        run_steps(s2, ex2, e_steps, depth, overlap=not args.no_overlap)
+                    s2.download(out=host_out)
                 dt = time.perf_counter() - t0
                 skipped = s2.info()["skipped_items"]
                 if dist:  # no neighbour may still be storing into this slab's (IPC-mapped) memory
@@ -514,6 +517,8 @@ def main():
             # best of two runs (each on a fresh handle): host-side jitter (page-cache / pinned-memory
             # state) moves single e2e runs by several percent
             dt = min(run_e2e(False, upload_fields=not zero_start)[0] for _ in range(2))
+            # the same flow with the readback after the run (yb_advance + yb_download_fields)
+            ds = run_e2e(False, upload_fields=not zero_start, streamed=False)[0] if world == 1 else None
             h2d = coef_b + (0 if zero_start else field_b)
             e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
@@ -521,7 +526,12 @@ def main():
                    "path": ("Simulation: set_cell_coeffs (pinned host) -> run(config steps) from the zero-initialised "
                             "state -> download all six fields (pinned host)" if zero_start else
                             "Simulation: set_cell_coeffs + upload all six fields (pinned host) -> run(config steps) "
-                            "-> download all six fields (pinned host)")}
+                            "-> download all six fields (pinned host)") +
+                           ("; run + readback as one yb_run_to_host call (each tile row's device->host copies start "
+                            "when it finished its last sweep)" if world == 1 else "")}
+            if ds is not None:
+                e2e["readback_after_run"] = {"value": cells_total * e_steps / ds / 1e9, "unit": UNIT, "wall_s": ds,
+                                             "note": "yb_advance then yb_download_fields (no overlap)"}
             if zero_start:  # the same run with the zero fields uploaded from the host as well
                 du, _ = run_e2e(False, upload_fields=True)
                 e2e["with_zero_field_upload"] = {"value": cells_total * e_steps / du / 1e9, "unit": UNIT,

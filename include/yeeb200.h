@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define YB_ABI_VERSION 3
+#define YB_ABI_VERSION 4
 
 /* Status codes. The shim maps INVALID_ARGUMENT -> std::invalid_argument,
  * OUT_OF_RANGE -> std::out_of_range, the rest -> std::runtime_error. */
@@ -86,6 +86,7 @@ typedef struct {
   int halo_depth;          /* z-slab mode: ghost planes refreshed per exchange = steps per exchange */
   int quiescent_skip;      /* yb_set_quiescent_skip state */
   int64_t skipped_items;   /* work items skipped as quiescent (RunStats::skipped_tiles analogue) */
+  int64_t streamed_readbacks; /* yb_run_to_host calls whose readback overlapped the run */
 } yb_info;
 
 /* Last error message of the calling thread ("" if none). */
@@ -148,6 +149,16 @@ int yb_upload_fields(yb_sim* sim, const float* const* dense6);
  * yb_set_cell_coeffs(which[i], cells[i], 0). */
 int yb_set_cell_coeffs_n(yb_sim* sim, int n, const int* which, const float* const* cells);
 int yb_download_fields(yb_sim* sim, float* const* dense6);
+/* Simulation::run followed by the FieldSet readout (runner.hpp:243-266 +
+ * fields.hpp:21-67): advance nsteps, then leave all six components in the
+ * dense host buffers — the drop-in form of `sim.run(n); sim.fields()`.
+ * With page-locked buffers and the two-step kernel on a single domain
+ * (no probes, no quiescent skip, nsteps >= 4) the readback overlaps the run:
+ * the last multi-sweep launch hands its items out along y-skewed diagonals,
+ * and each tile row's device->host copies start as soon as it finished its
+ * last sweep. Otherwise it is yb_advance + yb_download_fields. Same result
+ * either way (bit-identical). */
+int yb_run_to_host(yb_sim* sim, int64_t nsteps, float* const* dense6);
 /* FieldSet::zero() (fields.hpp:60-63) and seeded init (yeeb200_inputs.h). */
 int yb_zero_fields(yb_sim* sim);
 int yb_fill_fields(yb_sim* sim, uint64_t seed);

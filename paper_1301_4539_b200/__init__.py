@@ -26,7 +26,7 @@ CSRC = os.path.join(HERE, "csrc")
 EX, EY, EZ, HX, HY, HZ = range(6)
 COMP_NAMES = ("ex", "ey", "ez", "hx", "hy", "hz")
 CA, CB, DA, DB = range(4)
-ABI_VERSION = 3  # YB_ABI_VERSION of include/yeeb200.h
+ABI_VERSION = 4  # YB_ABI_VERSION of include/yeeb200.h
 VARIANT_TB2, VARIANT_NAIVE, VARIANT_FUSED, VARIANT_TB4 = 0, 1, 2, 3  # YB_VARIANT_* (TB2 = 0: the default)
 S_BITS = 0x3F1252DB
 S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt(3))
@@ -43,7 +43,7 @@ ABI_SYMBOLS = (
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
     "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
     "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait", "yb_peer_step",
-    "yb_peer_run",
+    "yb_peer_run", "yb_run_to_host",
     "yb_fs_apply", "yb_fs_total_energy",
 )
 
@@ -72,7 +72,8 @@ class Info(C.Structure):
                 ("n_cell_arrays", C.c_int), ("variant", C.c_int), ("stages", C.c_int),
                 ("grid_x", C.c_int), ("grid_y", C.c_int), ("grid_z", C.c_int), ("zchunk", C.c_int),
                 ("bytes_per_cell_update", C.c_double), ("device_bytes", C.c_size_t),
-                ("halo_depth", C.c_int), ("quiescent_skip", C.c_int), ("skipped_items", C.c_int64)]
+                ("halo_depth", C.c_int), ("quiescent_skip", C.c_int), ("skipped_items", C.c_int64),
+                ("streamed_readbacks", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -108,6 +109,7 @@ def lib():
         L.yb_upload_fields.argtypes = [vp, C.POINTER(vp)]
         L.yb_download_fields.argtypes = [vp, C.POINTER(vp)]
         L.yb_download_field.argtypes = [vp, C.c_int, _f32p]
+        L.yb_run_to_host.argtypes = [vp, C.c_int64, C.POINTER(vp)]
         L.yb_zero_fields.argtypes = [vp]
         L.yb_fill_fields.argtypes = [vp, C.c_uint64]
         L.yb_set_step_index.argtypes = [vp, C.c_int64]
@@ -274,6 +276,21 @@ class Simulation:
             res.append(a)
         ptrs = (C.c_void_p * 6)(*[a.ctypes.data for a in res])
         _check(lib().yb_download_fields(self._h, ptrs))
+        return res
+
+    def run_to_host(self, nsteps, out=None):
+        """run(nsteps) then download(out) in one call (yb_run_to_host): with
+        page-locked `out` buffers the device->host copies of each tile row
+        start as soon as it finished its last sweep, overlapping the rest of
+        the run. Returns the six dense arrays."""
+        res = []
+        for c in range(6):
+            shape = comp_extents(self.nx, self.ny, self.nz, c)[::-1]
+            a = np.empty(shape, np.float32) if out is None else out[c]
+            assert a.shape == shape and a.dtype == np.float32 and a.flags.c_contiguous
+            res.append(a)
+        ptrs = (C.c_void_p * 6)(*[a.ctypes.data for a in res])
+        _check(lib().yb_run_to_host(self._h, nsteps, ptrs))
         return res
 
     def zero(self):

@@ -175,6 +175,16 @@ struct yb_sim {
   // chained exchange periods (yb_peer_run, two-step kernel MODE 4)
   unsigned* pcnt4 = nullptr;            // per side and sweep: boundary row warps done (2 x kChainSweeps)
   cudaEvent_t chain_ev = nullptr;
+  // streamed readback (yb_run_to_host): skewed item order of the last launch,
+  // per tile-row completion counters (+ faces) polled by the copy stream
+  bool drain = false;         // the next multi-sweep launch skews its last sweeps and counts bands
+  int* diag_dev = nullptr;    // diagonal offsets (FusedArgs::diag)
+  int diag_cap = 0, diag_sweeps = 0, diag_nty = 0, ndiag = 0;
+  unsigned* band_dev = nullptr;  // nty tile-row counters + 1 face counter (monotonic)
+  int band_n = 0;
+  unsigned band_base = 0, face_base = 0;
+  unsigned last_grid = 0;     // CTAs of the last two-step launch
+  int64_t streamed = 0;       // yb_run_to_host calls that streamed
 };
 
 namespace {
@@ -607,6 +617,12 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
     a.done = s->done;
     a.epoch = s->epoch;
     a.srcs = s->srcs_dev;
+    if (s->drain) {  // streamed readback: skewed last sweeps, band counters (set up by yb_run_to_host)
+      a.diag = s->diag_dev;
+      a.ndiag = s->ndiag;
+      a.skew0 = nsweeps - s->diag_sweeps;
+      a.band = s->band_dev;
+    }
   }
   a.sched = sc;
   a.sched_base = base;
@@ -634,6 +650,7 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
     YB_CU(cudaEventRecord(tp->a, st));
   }
   YB_CU(yb::launch_tb2(a, s->tm2[s->cur], s->tm2[nxt], mask, grid, smem, st));
+  s->last_grid = grid.x;
   base += (unsigned long long)a.nitems * nsweeps + grid.x;
   if (nsweeps > 1) s->epoch += (unsigned)nsweeps;
   if (tp) YB_CU(cudaEventRecord(tp->b, st));
@@ -911,6 +928,8 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->qskipped);
   cudaFree(s->done);
   cudaFree(s->srcs_dev);
+  cudaFree(s->diag_dev);
+  cudaFree(s->band_dev);
   for (float* p : s->snap_h) cudaFree(p);
   for (PeerSide& ps : s->peer)
     for (void* p : ps.ipc) cudaIpcCloseMemHandle(p);
@@ -1263,6 +1282,169 @@ int yb_download_fields(yb_sim* s, float* const* d) {
     YB_CU(cudaMemsetAsync(s->buf[s->cur ^ 1][c] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
   YB_CU(cudaStreamSynchronize(s->stream));
   return YB_OK;
+}
+
+static int check_wait_error(yb_sim* s);
+
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn wait_value_fn() {
+  static WaitValue32Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValue32Fn>(p);
+  }
+  return fn;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Diagonal offsets of the skewed order for (sweeps, tile rows): diag[d] =
+// (sweep, tile row) groups with 2*sweep + row < d, d = 0 .. ndiag.
+static int ensure_drain(yb_sim* s, int nsw) {
+  const int nty = s->nty, nd = 2 * (nsw - 1) + nty;
+  if (s->diag_sweeps != nsw || s->diag_nty != nty) {
+    std::vector<int> h(nd + 1, 0);
+    for (int d = 0; d < nd; ++d) {
+      const int lo = std::max(0, (d - nty + 2) / 2), hi = std::min(nsw - 1, d / 2);
+      h[d + 1] = h[d] + std::max(0, hi - lo + 1);
+    }
+    if (h[nd] != nsw * nty) return fail(YB_CUDA_ERROR, "internal: skewed order covers %d of %d groups", h[nd], nsw * nty);
+    if (s->diag_cap < nd + 1) {
+      cudaFree(s->diag_dev);
+      s->diag_dev = nullptr;
+      YB_CU(cudaMalloc(&s->diag_dev, (size_t)(nd + 1) * sizeof(int)));
+      s->diag_cap = nd + 1;
+    }
+    YB_CU(cudaMemcpyAsync(s->diag_dev, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    YB_CU(cudaStreamSynchronize(s->stream));
+    s->diag_sweeps = nsw;
+    s->diag_nty = nty;
+    s->ndiag = nd;
+  }
+  if (s->band_n != nty + 1) {
+    cudaFree(s->band_dev);
+    s->band_dev = nullptr;
+    YB_CU(cudaMalloc(&s->band_dev, (size_t)(nty + 1) * sizeof(unsigned)));
+    YB_CU(cudaMemsetAsync(s->band_dev, 0, (size_t)(nty + 1) * sizeof(unsigned), s->stream));
+    YB_CU(cudaStreamSynchronize(s->stream));
+    s->band_n = nty + 1;
+    s->band_base = s->face_base = 0;
+  }
+  return YB_OK;
+}
+
+int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
+  if (!s || !d) return fail(YB_INVALID_ARGUMENT, "null argument");
+  for (int c = 0; c < 6; ++c)
+    if (!d[c]) return fail(YB_INVALID_ARGUMENT, "null component %d", c);
+  if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
+  YB_CU(cudaSetDevice(s->device));
+  if (s->variant != YB_VARIANT_NAIVE)
+    if (int rc = prepare_fused(s)) return rc;  // sets the multi-sweep chunk (zchunk2p)
+  bool pinned = true;
+  for (int c = 0; c < 6; ++c) pinned = pinned && is_pinned(d[c]);
+  const bool stream = pinned && s->variant == YB_VARIANT_TB2 && s->persist && s->zchunk2p > 0 &&
+                      s->probes.empty() && !s->qskip && s->g.nzg == s->g.nz && !s->peer[0].on &&
+                      !s->peer[1].on && nsteps >= 4 && wait_value_fn() != nullptr &&
+                      std::getenv("YB_NO_DRAIN") == nullptr;
+  if (!stream) {  // the same result, read back after the run
+    if (int rc = yb_advance(s, nsteps)) return rc;
+    return yb_download_fields(s, d);
+  }
+  // the leading steps (an odd one, earlier launches of a long run) as usual,
+  // then one multi-sweep launch whose tile rows stream out as they finish
+  const int nsw = (int)std::min<int64_t>(nsteps / 2, 1024);
+  if (int rc = yb_advance(s, nsteps - 2 * (int64_t)nsw)) return rc;
+  if (int rc = prepare_fused(s)) return rc;
+  // Skew only the last K sweeps: enough lead for the readback (~24 B per cell
+  // over PCIe at ~52 GB/s is ~40 two-step sweeps of the kernel at ~190
+  // Gcell/s, ~32 at ~160 with four coefficient arrays), at most what the tile
+  // rows allow (a row leads the next by half a sweep); modelled and measured
+  // with tools/drain_phases.py (config 4: K = 40 of 100).
+  int K = popcount4(cell_mask(s)) > 2 ? 32 : 40;
+  if (const char* e = std::getenv("YB_DRAIN_K")) K = std::atoi(e);
+  K = std::max(1, std::min({K, nsw, s->nty / 2 + 1}));
+  if (int rc = ensure_drain(s, K)) return rc;
+  if (int rc = ensure_xfer(s)) return rc;
+  // YB_DRAIN_TRACE=1 (measurement): events around the launch and after every
+  // tile row's copies, printed to stderr as ms from the launch start
+  const bool trace = std::getenv("YB_DRAIN_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  if (trace) {
+    tev.resize(s->nty + 2);
+    for (cudaEvent_t& e : tev) YB_CU(cudaEventCreate(&e));
+    YB_CU(cudaEventRecord(tev[0], s->stream));
+  }
+  s->drain = true;
+  const int rc = step_tb2(s, zfull(s), s->zchunk2p, true, nsw);
+  s->drain = false;
+  if (rc) return rc;
+  if (trace) YB_CU(cudaEventRecord(tev[1], s->stream));
+  s->step_index += 2 * nsw;
+  s->steps += 2 * nsw;
+  // readback on the transfer stream: band ty (rows 8ty .. 8ty+7, the last band
+  // up to the face row) once all its last-sweep row warps and all face warps counted
+  const int nch = (s->g.nz + s->zchunk2p - 1) / s->zchunk2p;
+  const unsigned per = (unsigned)(s->ntx * nch * yb::kTB2RowWarps);
+  const unsigned band_need = s->band_base + per, face_need = s->face_base + s->last_grid;
+  WaitValue32Fn wv = wait_value_fn();
+  CUstream xs = reinterpret_cast<CUstream>(s->xfer);
+  auto dptr = [&](int q) { return reinterpret_cast<CUdeviceptr>(s->band_dev + q); };
+  if (CUresult r = wv(xs, dptr(s->nty), face_need, CU_STREAM_WAIT_VALUE_GEQ))
+    return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
+  const int fin = s->cur;  // step_tb2 flipped to the launch's final-state buffer
+  for (int ty = 0; ty < s->nty; ++ty) {
+    if (CUresult r = wv(xs, dptr(ty), band_need, CU_STREAM_WAIT_VALUE_GEQ))
+      return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
+    for (int c = 0; c < 6; ++c) {
+      int e[3];
+      comp_ext(s->g, c, e);
+      const int j0 = ty * yb::kTB2Rows, j1 = ty == s->nty - 1 ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
+      if (j1 <= j0) continue;
+      cudaMemcpy3DParms p{};
+      p.srcPtr = make_cudaPitchedPtr(s->buf[fin][c], (size_t)s->g.PX * 4, (size_t)s->g.PX, (size_t)s->g.PY);
+      p.srcPos = make_cudaPos(0, (size_t)j0, 0);
+      p.dstPtr = make_cudaPitchedPtr(d[c], (size_t)e[0] * 4, (size_t)e[0], (size_t)e[1]);
+      p.dstPos = make_cudaPos(0, (size_t)j0, 0);
+      p.extent = make_cudaExtent((size_t)e[0] * 4, (size_t)(j1 - j0), (size_t)e[2]);
+      p.kind = cudaMemcpyDeviceToHost;
+      YB_CU(cudaMemcpy3DAsync(&p, s->xfer));
+    }
+    if (trace) YB_CU(cudaEventRecord(tev[2 + ty], s->xfer));
+  }
+  s->band_base += per;
+  s->face_base += s->last_grid;
+  s->streamed += 1;
+  YB_CU(cudaEventRecord(s->xev[6], s->xfer));
+  YB_CU(cudaStreamWaitEvent(s->stream, s->xev[6], 0));
+  YB_CU(cudaStreamSynchronize(s->stream));
+  if (trace) {
+    float k = 0.f;
+    YB_CU(cudaEventElapsedTime(&k, tev[0], tev[1]));
+    std::fprintf(stderr, "yb_run_to_host: %d sweeps (last %d skewed), %d tile rows; kernel %.2f ms; rows done (ms):",
+                 nsw, K, s->nty, k);
+    for (int ty = 0; ty < s->nty; ty += std::max(1, s->nty / 16)) {
+      float t = 0.f;
+      YB_CU(cudaEventElapsedTime(&t, tev[0], tev[2 + ty]));
+      std::fprintf(stderr, " %d:%.1f", ty, t);
+    }
+    float t = 0.f;
+    YB_CU(cudaEventElapsedTime(&t, tev[0], tev[1 + s->nty]));
+    std::fprintf(stderr, " last:%.1f\n", t);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
+  return check_wait_error(s);
 }
 
 int yb_zero_fields(yb_sim* s) {
@@ -2169,6 +2351,7 @@ int yb_get_info(yb_sim* s, yb_info* info) {
     YB_CU(cudaStreamSynchronize(s->stream));
     info->skipped_items = (int64_t)v;
   }
+  info->streamed_readbacks = s->streamed;
   return YB_OK;
 }
 

@@ -147,6 +147,16 @@ struct FusedArgs {
   float* pup_o[6];
   int nchain;
   int chain_off[9];
+  // Streamed readback (yb_run_to_host, MODE 2): sweeps skew0.. are handed out
+  // along y-skewed diagonals d = 2*(sweep - skew0) + tile_row (diag[d] = (sweep,
+  // tile row) groups before diagonal d, ndiag diagonals; the sweeps before
+  // skew0 sweep-major) so a tile row finishes its last sweep early; every row warp of a last-sweep item adds 1 to band[tile row]
+  // and every face warp to band[nty] (system-scope fence first), so copy-engine
+  // readbacks waiting on those counters (cuStreamWaitValue32) overlap the
+  // sweeps still running. band == nullptr: sweep-major order, no counting.
+  const int* diag;
+  int ndiag, skew0;
+  unsigned* band;
 };
 
 constexpr int kChainMax = 8;

@@ -217,6 +217,37 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
+// Streamed readback order (FusedArgs::diag): work item v of a multi-sweep
+// launch -> (sweep, item); sweeps before skew0 sweep-major, the rest along
+// y-skewed diagonals d = 2*(sweep - skew0) + tile row, sweeps ascending within
+// a diagonal, then z-chunk, then tile column. An item's dependencies (sweep-1,
+// tile rows ty-1..ty+1) come earlier (diagonals d-1..d-3, or the sweep-major
+// part), so the order is a topological one, and tile row ty finishes its last
+// sweep at diagonal 2*(nsweeps-1-skew0) + ty — the bottom rows long before the
+// top ones. (Only the last sweeps are skewed: neighbouring tile rows of one
+// sweep are a diagonal apart there, so their shared halo rows miss L2.)
+__device__ __noinline__ void skew_item(const FusedArgs& a, unsigned long long v, int T, int& sw, int& it) {
+  const unsigned long long flat = (unsigned long long)a.skew0 * a.nitems;
+  if (v < flat) {
+    sw = (int)(v / (unsigned long long)a.nitems);
+    it = (int)(v - (unsigned long long)sw * a.nitems);
+    return;
+  }
+  v -= flat;
+  const int per = a.nitems / a.nty;  // items of one (sweep, tile row) group
+  const int grp = (int)(v / (unsigned long long)per), rem = (int)(v - (unsigned long long)grp * per);
+  int lo = 0, hi = a.ndiag - 1;  // the last diagonal d with diag[d] <= grp
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(a.diag + mid) <= grp) lo = mid;
+    else hi = mid - 1;
+  }
+  const int sk = max(0, (lo - a.nty + 2) / 2) + (grp - __ldg(a.diag + lo));
+  const int ty = lo - 2 * sk, ch = rem / a.ntx, tx = rem - ch * a.ntx;
+  it = ch * T + ty * a.ntx + tx;
+  sw = a.skew0 + sk;
+}
+
 // MODE 3 (folded exchange): spin, bounded by the launch's deadline, until a
 // neighbour's flag word reaches need.
 __device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, int* err, unsigned long long wait_ns,
@@ -778,6 +809,13 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
       face_point(g, a.in, fin, co, t);
       for (int q = 1; q < 2 * a.nsweeps; ++q) face_point(g, fin, fin, co, t);
     }
+    if (MODE == 2 && a.band) {  // streamed readback: this CTA's face DoFs are final
+      __syncwarp();
+      if (l == 0) {
+        __threadfence_system();
+        atomicAdd(a.band + a.nty, 1u);
+      }
+    }
     return;
   }
 
@@ -813,8 +851,12 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
             if (wd || wu) asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads
           }
         } else if (v < (unsigned long long)a.nitems * a.nsweeps) {
-          sw = (int)(v / (unsigned long long)a.nitems);
-          it = (int)(v - (unsigned long long)sw * a.nitems);
+          if (MODE == 2 && a.diag) {
+            skew_item(a, v, T, sw, it);
+          } else {
+            sw = (int)(v / (unsigned long long)a.nitems);
+            it = (int)(v - (unsigned long long)sw * a.nitems);
+          }
         }
         item_q[p_seq % kQ] = it;
         if (MS) sweep_q[p_seq % kQ] = sw;
@@ -955,6 +997,10 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
       if (l == 0) {
         __threadfence();
         atomicAdd(A.done + item, 1u);
+        if (MODE == 2 && A.band && sw == a.nsweeps - 1) {  // streamed readback: my rows of the band are final
+          __threadfence_system();
+          atomicAdd(A.band + (item % T) / a.ntx, 1u);
+        }
       }
     }
   }
