@@ -50,13 +50,6 @@ constexpr int CL = 3, CR = 4 + kTX;  // edge columns x0-1, x0+128 (and CR+1)
 
 constexpr int kConsumers = 32 * (RW + 1);  // row warps + edge warp
 
-// Own-row values a row warp keeps in registers from L2 to L3 of the same plane
-// instead of re-reading them from shared memory after the barrier:
-// bit 0: H1(p-1) (the L2 result), bit 1: E1(p-1) (L2's operands).
-#ifndef YB_TB2_KEEP
-#define YB_TB2_KEEP 0
-#endif
-
 // A consumer warp is done reading a stage: every lane's loads have been
 // consumed, lane 0 arrives on the stage's "empty" barrier (count RW + 1).
 __device__ __forceinline__ void release_stage(uint64_t* empty, int s, int l) {
@@ -361,9 +354,6 @@ struct Rows {
   float ze, zh, ze1, zh1;
   F4x3 h0p;
   float4 cap, cbp, dap, dbp, dap2, dbp2;
-  // YB_TB2_KEEP bit 2: the i+1 neighbours of this lane's E1(p-1) / E2(p-2) ey, ez, shuffled
-  // from lane l+1 when those were computed (a plane earlier, off the critical path)
-  float e1y_ip = 0.f, e1z_ip = 0.f, e2y_ip = 0.f, e2z_ip = 0.f;
 
   __device__ __forceinline__ Rows(const FusedArgs& a_, const Item& it_, const Bufs& B_, Cursor& cur_,
                                   float* const* out_, const SrcArgs& src_, int er_, int l_, uint64_t pol)
@@ -440,9 +430,6 @@ struct Rows {
       sts4(w + E1C, e1c.y);
       sts4(w + 2 * E1C, e1c.z);
     }
-    constexpr bool KS = (YB_TB2_KEEP & 4) != 0;
-    const float e1y_n = KS ? __shfl_down_sync(~0u, e1c.y.x, 1) : 0.f;  // for the next plane's L2
-    const float e1z_n = KS ? __shfl_down_sync(~0u, e1c.z.x, 1) : 0.f;
     // No CTA barrier between L1 and L2: L2 reads E1(p-1) (ordered by the
     // previous plane's barrier B) and its own row of E1(p) from registers;
     // the only shared resource L1 frees is the stage.
@@ -450,23 +437,15 @@ struct Rows {
 
     // ----------------------------------------------------- L2: H1(p-1)
     const int kh = p - 1;
-    F4x3 h1c = {z4, z4, z4};
-    float4 ex_h = z4, ey_h = z4, ez_h = z4;
     if (kh >= it.pstart && kh <= it.up && er <= RW - 2) {
       const float cdz_h = zh;
       const float* e = e1o + Q * E1B;  // E1(p-1), row j
-      ex_h = lds4(e);
-      const float4 ex_jp = lds4(e + BX);
-      ey_h = lds4(e + E1C);
-      ez_h = lds4(e + 2 * E1C);
-      const float4 ez_jp = lds4(e + 2 * E1C + BX);
-      float yw = e1y_ip, zw = e1z_ip;
-      if (!KS || l == 31) {  // the edge warp's column (every lane's +4 column without KS)
-        yw = e[E1C + 4];
-        zw = e[2 * E1C + 4];
-      }
-      const float4 ey_ip = make_float4(ey_h.y, ey_h.z, ey_h.w, yw);
-      const float4 ez_ip = make_float4(ez_h.y, ez_h.z, ez_h.w, zw);
+      const float4 ex_h = lds4(e), ex_jp = lds4(e + BX);
+      const float4 ey_h = lds4(e + E1C);
+      const float4 ez_h = lds4(e + 2 * E1C), ez_jp = lds4(e + 2 * E1C + BX);
+      const float4 ey_ip = make_float4(ey_h.y, ey_h.z, ey_h.w, e[E1C + 4]);
+      const float4 ez_ip = make_float4(ez_h.y, ez_h.z, ez_h.w, e[2 * E1C + 4]);
+      F4x3 h1c;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float A = DAC ? elc(dap, q) : co.da_s;
@@ -483,8 +462,6 @@ struct Rows {
       sts4(w + H1C, h1c.y);
       sts4(w + 2 * H1C, h1c.z);
     }
-    const float h1y_im = KS ? __shfl_up_sync(~0u, h1c.y.w, 1) : 0.f;  // L3's i-1 neighbours
-    const float h1z_im = KS ? __shfl_up_sync(~0u, h1c.z.w, 1) : 0.f;
     consumer_sync();  // (B) H1(p-1) complete
 
     // ----------------------------------------------------- L3: E2(p-1)
@@ -493,19 +470,13 @@ struct Rows {
       const float cdz_e = ze1;
       const float* h = h1o + Q * H1B;    // H1(p-1), row j
       const float* hp = h1o + PAR * H1B;  // H1(p-2), row j
-      constexpr bool KH = (YB_TB2_KEEP & 1) != 0, KE = (YB_TB2_KEEP & 2) != 0;
-      const float4 hx = KH ? h1c.x : lds4(h), hy = KH ? h1c.y : lds4(h + H1C), hz = KH ? h1c.z : lds4(h + 2 * H1C);
-      float yv = h1y_im, zv = h1z_im;
-      if (!KS || l == 0) {
-        yv = h[H1C - 1];
-        zv = h[2 * H1C - 1];
-      }
-      const float4 hy_im = make_float4(yv, hy.x, hy.y, hy.z);
-      const float4 hz_im = make_float4(zv, hz.x, hz.y, hz.z);
+      const float4 hx = lds4(h), hy = lds4(h + H1C), hz = lds4(h + 2 * H1C);
+      const float4 hy_im = make_float4(h[H1C - 1], hy.x, hy.y, hy.z);
+      const float4 hz_im = make_float4(h[2 * H1C - 1], hz.x, hz.y, hz.z);
       const float* e = e1o + Q * E1B;
-      e2c = e_update4<CAC, CBC>(co, g, i0, xedge, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp,
-                                KE ? ex_h : lds4(e), KE ? ey_h : lds4(e + E1C), KE ? ez_h : lds4(e + 2 * E1C), hx, hy,
-                                hz, lds4(h - BX), lds4(h + 2 * H1C - BX), hy_im, hz_im, lds4(hp), lds4(hp + H1C));
+      e2c = e_update4<CAC, CBC>(co, g, i0, xedge, j, kh + g.zoff, cdy_e, cdz_e, cdx_e, cap, cbp, lds4(e),
+                                lds4(e + E1C), lds4(e + 2 * E1C), hx, hy, hz, lds4(h - BX), lds4(h + 2 * H1C - BX),
+                                hy_im, hz_im, lds4(hp), lds4(hp + H1C));
       if (it.src && src_row(src(), 2, j, kh)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -537,13 +508,8 @@ struct Rows {
       const float4 ex_h = lds4(e), ex_jp = lds4(e + BX);
       const float4 ey_h = lds4(e + E2C);
       const float4 ez_h = lds4(e + 2 * E2C), ez_jp = lds4(e + 2 * E2C + BX);
-      float yw = e2y_ip, zw = e2z_ip;
-      if (!KS || l == 31) {
-        yw = e[E2C + 4];
-        zw = e[2 * E2C + 4];
-      }
-      const float4 ey_ip = make_float4(ey_h.y, ey_h.z, ey_h.w, yw);
-      const float4 ez_ip = make_float4(ez_h.y, ez_h.z, ez_h.w, zw);
+      const float4 ey_ip = make_float4(ey_h.y, ey_h.z, ey_h.w, e[E2C + 4]);
+      const float4 ez_ip = make_float4(ez_h.y, ez_h.z, ez_h.w, e[2 * E2C + 4]);
       const float* h = h1o + PAR * H1B;  // H1(p-2), row j
       const float4 h1x = lds4(h), h1y = lds4(h + H1C), h1z = lds4(h + 2 * H1C);
       F4x3 h2;
@@ -568,12 +534,6 @@ struct Rows {
       }
     }
     // ---------------------------------------------------------- rotate
-    if (KS) {
-      e1y_ip = e1y_n;
-      e1z_ip = e1z_n;
-      e2y_ip = __shfl_down_sync(~0u, e2c.y.x, 1);  // for the next plane's L4
-      e2z_ip = __shfl_down_sync(~0u, e2c.z.x, 1);
-    }
     ze1 = ze;
     zh1 = zh;
     ze = ze_n;
@@ -1094,7 +1054,7 @@ using LimitFn = cudaError_t (*)();
 
 // index: bits 0-3 per-cell Ca/Cb/Da/Db, then 16 * MODE (0..4)
 #define YB_B(m) (m & 1) != 0, (m & 2) != 0, (m & 4) != 0, (m & 8) != 0, (m >> 4)
-#ifdef YB_TB2_AB  // measurement builds: only the multi-sweep kernels of configs 1 / 2, 4 / 3, 5
+#ifdef YB_TB2_AB  // measurement builds (tools/ab_build.sh): only the multi-sweep kernels of configs 1 / 2, 4 / 3, 5
 template <int M>
 constexpr bool ab_has = (M >> 4) == 2 && ((M & 15) == 0 || (M & 15) == 2 || (M & 15) == 15);
 template <int M>
