@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define YB_ABI_VERSION 4
+#define YB_ABI_VERSION 5
 
 /* Status codes. The shim maps INVALID_ARGUMENT -> std::invalid_argument,
  * OUT_OF_RANGE -> std::out_of_range, the rest -> std::runtime_error. */
@@ -87,6 +87,7 @@ typedef struct {
   int quiescent_skip;      /* yb_set_quiescent_skip state */
   int64_t skipped_items;   /* work items skipped as quiescent (RunStats::skipped_tiles analogue) */
   int64_t streamed_readbacks; /* yb_run_to_host calls whose readback overlapped the run */
+  int64_t streamed_uploads;   /* yb_run_streamed calls whose upload overlapped the run */
 } yb_info;
 
 /* Last error message of the calling thread ("" if none). */
@@ -159,6 +160,23 @@ int yb_download_fields(yb_sim* sim, float* const* dense6);
  * last sweep. Otherwise it is yb_advance + yb_download_fields. Same result
  * either way (bit-identical). */
 int yb_run_to_host(yb_sim* sim, int64_t nsteps, float* const* dense6);
+/* run_simulation's whole host flow in one call (runner.hpp:349-362: construct
+ * from a GridSpec + state, run, read the FieldSet back): upload ncoef per-cell
+ * coefficient arrays (which[] = YB_CA..YB_DB, dense nx*ny*nz each) and, when
+ * in6 is not NULL, the six initial field components; advance nsteps; leave
+ * all six components in out6. in6 == NULL runs from the handle's current
+ * state (the zero FieldSet of a fresh handle). With page-locked buffers on a
+ * single domain with the two-step kernel (no probes, no quiescent skip, an
+ * even nsteps in 8 .. 2048) both transfers overlap the run: the copies go up
+ * tile row by tile row and the one multi-sweep launch hands out its first
+ * sweeps along the mirrored y-skewed diagonals, each first-sweep item
+ * starting once its rows have landed (per-row words the copy stream writes,
+ * cuStreamWriteValue32), and its last sweeps as yb_run_to_host does. The
+ * arrays are stored as given (no uniformity compression). Otherwise it is
+ * yb_set_cell_coeffs_n + yb_upload_fields + yb_run_to_host. Same result either
+ * way (bit-identical). */
+int yb_run_streamed(yb_sim* sim, int64_t nsteps, int ncoef, const int* which, const float* const* cells,
+                    const float* const* in6, float* const* out6);
 /* FieldSet::zero() (fields.hpp:60-63) and seeded init (yeeb200_inputs.h). */
 int yb_zero_fields(yb_sim* sim);
 int yb_fill_fields(yb_sim* sim, uint64_t seed);

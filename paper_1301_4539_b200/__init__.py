@@ -26,7 +26,7 @@ CSRC = os.path.join(HERE, "csrc")
 EX, EY, EZ, HX, HY, HZ = range(6)
 COMP_NAMES = ("ex", "ey", "ez", "hx", "hy", "hz")
 CA, CB, DA, DB = range(4)
-ABI_VERSION = 4  # YB_ABI_VERSION of include/yeeb200.h
+ABI_VERSION = 5  # YB_ABI_VERSION of include/yeeb200.h
 VARIANT_TB2, VARIANT_NAIVE, VARIANT_FUSED, VARIANT_TB4 = 0, 1, 2, 3  # YB_VARIANT_* (TB2 = 0: the default)
 S_BITS = 0x3F1252DB
 S = np.array([S_BITS], dtype=np.uint32).view(np.float32)[0]  # (float)(0.99/sqrt(3))
@@ -43,7 +43,7 @@ ABI_SYMBOLS = (
     "yb_host_field_slab", "yb_host_medium_slab", "yb_set_probes", "yb_read_probes",
     "yb_snapshot_h", "yb_total_energy", "yb_set_quiescent_skip", "yb_advance_begin", "yb_advance_end",
     "yb_peer_handle_bytes", "yb_peer_export", "yb_peer_open", "yb_peer_link", "yb_peer_push", "yb_peer_wait", "yb_peer_step",
-    "yb_peer_run", "yb_run_to_host",
+    "yb_peer_run", "yb_run_to_host", "yb_run_streamed",
     "yb_fs_apply", "yb_fs_total_energy",
 )
 
@@ -73,7 +73,7 @@ class Info(C.Structure):
                 ("grid_x", C.c_int), ("grid_y", C.c_int), ("grid_z", C.c_int), ("zchunk", C.c_int),
                 ("bytes_per_cell_update", C.c_double), ("device_bytes", C.c_size_t),
                 ("halo_depth", C.c_int), ("quiescent_skip", C.c_int), ("skipped_items", C.c_int64),
-                ("streamed_readbacks", C.c_int64)]
+                ("streamed_readbacks", C.c_int64), ("streamed_uploads", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -110,6 +110,8 @@ def lib():
         L.yb_download_fields.argtypes = [vp, C.POINTER(vp)]
         L.yb_download_field.argtypes = [vp, C.c_int, _f32p]
         L.yb_run_to_host.argtypes = [vp, C.c_int64, C.POINTER(vp)]
+        L.yb_run_streamed.argtypes = [vp, C.c_int64, C.c_int, C.POINTER(C.c_int), C.POINTER(vp), C.POINTER(vp),
+                                      C.POINTER(vp)]
         L.yb_zero_fields.argtypes = [vp]
         L.yb_fill_fields.argtypes = [vp, C.c_uint64]
         L.yb_set_step_index.argtypes = [vp, C.c_int64]
@@ -291,6 +293,36 @@ class Simulation:
             res.append(a)
         ptrs = (C.c_void_p * 6)(*[a.ctypes.data for a in res])
         _check(lib().yb_run_to_host(self._h, nsteps, ptrs))
+        return res
+
+    def run_streamed(self, nsteps, cell_arrays=None, fields=None, out=None):
+        """run_simulation's host flow in one call (yb_run_streamed): upload the
+        per-cell coefficient arrays {which: cells} and (if given) the six
+        initial fields, advance nsteps, read all six components back. With
+        page-locked buffers both transfers overlap the run (tile row by tile
+        row); otherwise the phases run one after the other. Returns the six
+        dense arrays."""
+        items = [(w, _f32c(a)) for w, a in (cell_arrays or {}).items()]
+        for _, a in items:
+            assert a.size == self.nx * self.ny * self.nz
+        which = (C.c_int * max(1, len(items)))(*[w for w, _ in items])
+        cptr = (C.c_void_p * max(1, len(items)))(*[a.ctypes.data for _, a in items])
+        fin = None
+        if fields is not None:
+            arrs = []
+            for c in range(6):
+                a = _f32c(fields[c])
+                assert a.shape == comp_extents(self.nx, self.ny, self.nz, c)[::-1], (c, a.shape)
+                arrs.append(a)
+            fin = (C.c_void_p * 6)(*[a.ctypes.data for a in arrs])
+        res = []
+        for c in range(6):
+            shape = comp_extents(self.nx, self.ny, self.nz, c)[::-1]
+            a = np.empty(shape, np.float32) if out is None else out[c]
+            assert a.shape == shape and a.dtype == np.float32 and a.flags.c_contiguous
+            res.append(a)
+        optr = (C.c_void_p * 6)(*[a.ctypes.data for a in res])
+        _check(lib().yb_run_streamed(self._h, nsteps, len(items), which, cptr, fin, optr))
         return res
 
     def zero(self):

@@ -185,6 +185,13 @@ struct yb_sim {
   unsigned band_base = 0, face_base = 0;
   unsigned last_grid = 0;     // CTAs of the last two-step launch
   int64_t streamed = 0;       // yb_run_to_host calls that streamed
+  // streamed upload (yb_run_streamed): the first sweeps of the launch follow the host->device
+  // copies tile row by tile row (per-row words written by the copy stream)
+  bool upstream = false;      // the next multi-sweep launch skews its first sweeps and waits on upband
+  unsigned* upband_dev = nullptr;  // nty words (monotonic)
+  int upband_n = 0;
+  unsigned up_base = 0;
+  int64_t streamed_up = 0;    // yb_run_streamed calls whose upload overlapped the run
 };
 
 namespace {
@@ -623,6 +630,11 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
       a.skew0 = nsweeps - s->diag_sweeps;
       a.band = s->band_dev;
     }
+    if (s->upstream) {  // streamed upload: skewed first sweeps behind the copies (yb_run_streamed)
+      a.skewh = s->diag_sweeps;
+      a.upband = s->upband_dev;
+      a.up_need = s->up_base + 1;
+    }
   }
   a.sched = sc;
   a.sched_base = base;
@@ -926,6 +938,7 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->probe_dev);
   cudaFree(s->qbits);
   cudaFree(s->qskipped);
+  cudaFree(s->upband_dev);
   cudaFree(s->done);
   cudaFree(s->srcs_dev);
   cudaFree(s->diag_dev);
@@ -1343,6 +1356,44 @@ static int ensure_drain(yb_sim* s, int nsw) {
   return YB_OK;
 }
 
+// The readback half of a streamed run, enqueued on the transfer stream after the
+// skewed launch: band ty (rows 8ty .. 8ty+7, the last band up to the face row) is
+// copied once all its last-sweep row warps and all face warps have counted.
+static int enqueue_band_readback(yb_sim* s, float* const* d, std::vector<cudaEvent_t>* tevp) {
+  const bool trace = tevp != nullptr;
+  const int nch = (s->g.nz + s->zchunk2p - 1) / s->zchunk2p;
+  const unsigned per = (unsigned)(s->ntx * nch * yb::kTB2RowWarps);
+  const unsigned band_need = s->band_base + per, face_need = s->face_base + s->last_grid;
+  WaitValue32Fn wv = wait_value_fn();
+  CUstream xs = reinterpret_cast<CUstream>(s->xfer);
+  auto dptr = [&](int q) { return reinterpret_cast<CUdeviceptr>(s->band_dev + q); };
+  if (CUresult r = wv(xs, dptr(s->nty), face_need, CU_STREAM_WAIT_VALUE_GEQ))
+    return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
+  const int fin = s->cur;  // step_tb2 flipped to the launch's final-state buffer
+  for (int ty = 0; ty < s->nty; ++ty) {
+    if (CUresult r = wv(xs, dptr(ty), band_need, CU_STREAM_WAIT_VALUE_GEQ))
+      return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
+    for (int c = 0; c < 6; ++c) {
+      int e[3];
+      comp_ext(s->g, c, e);
+      const int j0 = ty * yb::kTB2Rows, j1 = ty == s->nty - 1 ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
+      if (j1 <= j0) continue;
+      cudaMemcpy3DParms p{};
+      p.srcPtr = make_cudaPitchedPtr(s->buf[fin][c], (size_t)s->g.PX * 4, (size_t)s->g.PX, (size_t)s->g.PY);
+      p.srcPos = make_cudaPos(0, (size_t)j0, 0);
+      p.dstPtr = make_cudaPitchedPtr(d[c], (size_t)e[0] * 4, (size_t)e[0], (size_t)e[1]);
+      p.dstPos = make_cudaPos(0, (size_t)j0, 0);
+      p.extent = make_cudaExtent((size_t)e[0] * 4, (size_t)(j1 - j0), (size_t)e[2]);
+      p.kind = cudaMemcpyDeviceToHost;
+      YB_CU(cudaMemcpy3DAsync(&p, s->xfer));
+    }
+    if (trace) YB_CU(cudaEventRecord((*tevp)[2 + ty], s->xfer));
+  }
+  s->band_base += per;
+  s->face_base += s->last_grid;
+  return YB_OK;
+}
+
 int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   if (!s || !d) return fail(YB_INVALID_ARGUMENT, "null argument");
   for (int c = 0; c < 6; ++c)
@@ -1393,38 +1444,7 @@ int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   if (trace) YB_CU(cudaEventRecord(tev[1], s->stream));
   s->step_index += 2 * nsw;
   s->steps += 2 * nsw;
-  // readback on the transfer stream: band ty (rows 8ty .. 8ty+7, the last band
-  // up to the face row) once all its last-sweep row warps and all face warps counted
-  const int nch = (s->g.nz + s->zchunk2p - 1) / s->zchunk2p;
-  const unsigned per = (unsigned)(s->ntx * nch * yb::kTB2RowWarps);
-  const unsigned band_need = s->band_base + per, face_need = s->face_base + s->last_grid;
-  WaitValue32Fn wv = wait_value_fn();
-  CUstream xs = reinterpret_cast<CUstream>(s->xfer);
-  auto dptr = [&](int q) { return reinterpret_cast<CUdeviceptr>(s->band_dev + q); };
-  if (CUresult r = wv(xs, dptr(s->nty), face_need, CU_STREAM_WAIT_VALUE_GEQ))
-    return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
-  const int fin = s->cur;  // step_tb2 flipped to the launch's final-state buffer
-  for (int ty = 0; ty < s->nty; ++ty) {
-    if (CUresult r = wv(xs, dptr(ty), band_need, CU_STREAM_WAIT_VALUE_GEQ))
-      return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
-    for (int c = 0; c < 6; ++c) {
-      int e[3];
-      comp_ext(s->g, c, e);
-      const int j0 = ty * yb::kTB2Rows, j1 = ty == s->nty - 1 ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
-      if (j1 <= j0) continue;
-      cudaMemcpy3DParms p{};
-      p.srcPtr = make_cudaPitchedPtr(s->buf[fin][c], (size_t)s->g.PX * 4, (size_t)s->g.PX, (size_t)s->g.PY);
-      p.srcPos = make_cudaPos(0, (size_t)j0, 0);
-      p.dstPtr = make_cudaPitchedPtr(d[c], (size_t)e[0] * 4, (size_t)e[0], (size_t)e[1]);
-      p.dstPos = make_cudaPos(0, (size_t)j0, 0);
-      p.extent = make_cudaExtent((size_t)e[0] * 4, (size_t)(j1 - j0), (size_t)e[2]);
-      p.kind = cudaMemcpyDeviceToHost;
-      YB_CU(cudaMemcpy3DAsync(&p, s->xfer));
-    }
-    if (trace) YB_CU(cudaEventRecord(tev[2 + ty], s->xfer));
-  }
-  s->band_base += per;
-  s->face_base += s->last_grid;
+  if (int rc = enqueue_band_readback(s, d, trace ? &tev : nullptr)) return rc;
   s->streamed += 1;
   YB_CU(cudaEventRecord(s->xev[6], s->xfer));
   YB_CU(cudaStreamWaitEvent(s->stream, s->xev[6], 0));
@@ -1444,6 +1464,150 @@ int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
     std::fprintf(stderr, " last:%.1f\n", t);
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
+  return check_wait_error(s);
+}
+
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WriteValue32Fn write_value_fn() {
+  static WriteValue32Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+  }
+  return fn;
+}
+
+// Host -> device copy of rows [j0, j1) of every plane of a dense e0 x e1 x e2 array into the
+// padded node box (both pitched; the copy engine, no kernel).
+static cudaError_t copy_rows_h2d(const yb_sim* s, float* padded, const float* dense, const int e[3], int j0, int j1,
+                                 cudaStream_t st) {
+  cudaMemcpy3DParms p{};
+  p.srcPtr = make_cudaPitchedPtr(const_cast<float*>(dense), (size_t)e[0] * 4, (size_t)e[0], (size_t)e[1]);
+  p.srcPos = make_cudaPos(0, (size_t)j0, 0);
+  p.dstPtr = make_cudaPitchedPtr(padded, (size_t)s->g.PX * 4, (size_t)s->g.PX, (size_t)s->g.PY);
+  p.dstPos = make_cudaPos(0, (size_t)j0, 0);
+  p.extent = make_cudaExtent((size_t)e[0] * 4, (size_t)(j1 - j0), (size_t)e[2]);
+  p.kind = cudaMemcpyHostToDevice;
+  return cudaMemcpy3DAsync(&p, st);
+}
+
+int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, const float* const* cells,
+                    const float* const* in6, float* const* d) {
+  if (!s || !d || (ncoef > 0 && (!which || !cells))) return fail(YB_INVALID_ARGUMENT, "null argument");
+  if (ncoef < 0 || ncoef > 4) return fail(YB_INVALID_ARGUMENT, "0 .. 4 coefficient arrays (got %d)", ncoef);
+  for (int i = 0; i < ncoef; ++i) {
+    if (which[i] < 0 || which[i] > 3 || !cells[i]) return fail(YB_INVALID_ARGUMENT, "bad array %d", i);
+    for (int k = 0; k < i; ++k)
+      if (which[k] == which[i]) return fail(YB_INVALID_ARGUMENT, "coefficient %d given twice", which[i]);
+  }
+  for (int c = 0; c < 6; ++c)
+    if (!d[c] || (in6 && !in6[c])) return fail(YB_INVALID_ARGUMENT, "null component %d", c);
+  if (nsteps < 0) return fail(YB_INVALID_ARGUMENT, "run: negative step count");
+  if (s->pending) return fail(YB_INVALID_ARGUMENT, "a split sweep is in flight (yb_advance_end first)");
+  YB_CU(cudaSetDevice(s->device));
+  auto plain = [&]() -> int {  // the same result, one phase after the other
+    if (ncoef > 0)
+      if (int rc = yb_set_cell_coeffs_n(s, ncoef, which, cells)) return rc;
+    if (in6)
+      if (int rc = yb_upload_fields(s, in6)) return rc;
+    return yb_run_to_host(s, nsteps, d);
+  };
+  bool pinned = true;
+  for (int c = 0; c < 6; ++c) pinned = pinned && is_pinned(d[c]) && (!in6 || is_pinned(in6[c]));
+  for (int i = 0; i < ncoef; ++i) pinned = pinned && is_pinned(cells[i]);
+  const int nsw = (int)(nsteps / 2);
+  const bool slab = s->g.nzg != s->g.nz;
+  const int nty0 = (s->g.ny + yb::kTB2Rows - 1) / yb::kTB2Rows;  // tile rows (the plan is made below)
+  // one multi-sweep launch carries the whole run: an even step count, at most 2048 steps,
+  // enough sweeps and tile rows to skew both ends; every host array page-locked
+  if (!(pinned && (ncoef > 0 || in6) && s->variant == YB_VARIANT_TB2 && s->persist && s->probes.empty() && !s->qskip &&
+        !slab && !s->peer[0].on && !s->peer[1].on && nsteps % 2 == 0 && nsw >= 4 && nsw <= 1024 && nty0 >= 4 &&
+        wait_value_fn() && write_value_fn() && std::getenv("YB_NO_DRAIN") == nullptr &&
+        std::getenv("YB_NO_UPSTREAM") == nullptr))
+  {
+    if (std::getenv("YB_STREAM_DEBUG"))
+      std::fprintf(stderr,
+                   "yb_run_streamed: phase by phase (pinned %d, arrays %d, variant %d, persist %d, probes %d, qskip %d, "
+                   "slab %d, nsteps %lld, tile rows %d, wait fn %d, write fn %d)\n",
+                   (int)pinned, ncoef + (in6 ? 6 : 0), s->variant, (int)s->persist, (int)s->probes.size(), (int)s->qskip,
+                   (int)slab, (long long)nsteps, nty0, wait_value_fn() != nullptr, write_value_fn() != nullptr);
+    return plain();
+  }
+  // The arrays as given, zero outside the cell box (no uniformity compression: a uniform array
+  // multiplies by the same values the scalar would); their clamped duplicates are filled after the run.
+  for (int i = 0; i < ncoef; ++i) {
+    const int w = which[i];
+    if (!s->cell[w]) {
+      float* p = nullptr;
+      YB_CU(cudaMalloc(&p, (size_t)s->g.total * 4));
+      s->cell[w] = p + yb::kGhost * s->g.plane;
+      s->dev_bytes += (size_t)s->g.total * 4;
+    }
+    YB_CU(cudaMemsetAsync(s->cell[w] - yb::kGhost * s->g.plane, 0, (size_t)s->g.total * 4, s->stream));
+    if (w == YB_CB) s->cb_uniform = false;
+    if (w == YB_DB) s->db_uniform = false;
+  }
+  if (ncoef > 0) s->tm_valid = false;
+  s->q_valid = false;
+  if (int rc = prepare_fused(s)) return rc;
+  if (s->zchunk2p <= 0 || s->nty != nty0) return plain();
+  int K = popcount4(cell_mask(s)) > 2 ? 32 : 40;  // as yb_run_to_host; the same depth at both ends
+  if (const char* e = std::getenv("YB_DRAIN_K")) K = std::atoi(e);
+  K = std::max(1, std::min({K, nsw / 2, s->nty / 2 + 1}));
+  if (int rc = ensure_drain(s, K)) return rc;
+  if (int rc = ensure_xfer(s)) return rc;
+  if (s->upband_n != s->nty) {
+    cudaFree(s->upband_dev);
+    s->upband_dev = nullptr;
+    YB_CU(cudaMalloc(&s->upband_dev, (size_t)s->nty * sizeof(unsigned)));
+    YB_CU(cudaMemsetAsync(s->upband_dev, 0, (size_t)s->nty * sizeof(unsigned), s->stream));
+    s->upband_n = s->nty;
+    s->up_base = 0;
+  }
+  // the copies: tile row by tile row on the transfer stream, each row's word written behind them
+  YB_CU(cudaEventRecord(s->xev[6], s->stream));  // the zeroed arrays; earlier work on the state
+  YB_CU(cudaStreamWaitEvent(s->xfer, s->xev[6], 0));
+  WriteValue32Fn wr = write_value_fn();
+  CUstream xs = reinterpret_cast<CUstream>(s->xfer);
+  const unsigned need = s->up_base + 1;
+  const int ce[3] = {s->g.nx, s->g.ny, s->g.nz};
+  for (int ty = 0; ty < s->nty; ++ty) {
+    const int j0 = ty * yb::kTB2Rows;
+    const bool last = ty == s->nty - 1;
+    for (int i = 0; i < ncoef; ++i) {
+      const int j1 = last ? ce[1] : std::min(j0 + yb::kTB2Rows, ce[1]);
+      if (j1 > j0) YB_CU(copy_rows_h2d(s, s->cell[which[i]], cells[i], ce, j0, j1, s->xfer));
+    }
+    if (in6)
+      for (int c = 0; c < 6; ++c) {
+        int e[3];
+        comp_ext(s->g, c, e);
+        const int j1 = last ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
+        if (j1 > j0) YB_CU(copy_rows_h2d(s, s->buf[s->cur][c], in6[c], e, j0, j1, s->xfer));
+      }
+    if (CUresult r = wr(xs, reinterpret_cast<CUdeviceptr>(s->upband_dev + ty), need, 0))
+      return fail(YB_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", (int)r);
+  }
+  s->drain = true;
+  s->upstream = true;
+  const int rc = step_tb2(s, zfull(s), s->zchunk2p, true, nsw);
+  s->drain = false;
+  s->upstream = false;
+  s->up_base = need;
+  if (rc) return rc;
+  s->step_index += 2 * nsw;
+  s->steps += 2 * nsw;
+  for (int i = 0; i < ncoef; ++i)  // the arrays' clamped duplicates (other kernels read them), behind the run
+    YB_CU(yb::launch_clamp_fill(s->g, s->cell[which[i]], 0, s->g.nz - 1, s->stream));
+  if (int rc2 = enqueue_band_readback(s, d, nullptr)) return rc2;
+  s->streamed += 1;
+  s->streamed_up += 1;
+  YB_CU(cudaEventRecord(s->xev[6], s->xfer));
+  YB_CU(cudaStreamWaitEvent(s->stream, s->xev[6], 0));
+  YB_CU(cudaStreamSynchronize(s->stream));
   return check_wait_error(s);
 }
 
@@ -2352,6 +2516,7 @@ int yb_get_info(yb_sim* s, yb_info* info) {
     info->skipped_items = (int64_t)v;
   }
   info->streamed_readbacks = s->streamed;
+  info->streamed_uploads = s->streamed_up;
   return YB_OK;
 }
 

@@ -136,7 +136,11 @@ __device__ __forceinline__ float coefB(const float* cell, const float* axis, int
 // does not own. Tangential E there is PEC (written +0); the normal H (hx at
 // i=nx, hy at j=ny, hz at k=nz) reads only those PEC zeros, so its update is
 // Da*h + (Db*(0-0) - Db*(0-0)), computed in exactly that form. Reads `in`,
-// writes `out` (disjoint from the sweep's writes).
+// writes `out` (disjoint from the sweep's writes). Per-cell Da / Db are read
+// at the clamped cell (i, j, k limited to the cell box) — the value the
+// arrays' clamped duplicates at i=nx / j=ny / k=nz hold — so the face update
+// does not depend on those duplicates being filled yet (yb_run_streamed fills
+// them after the run).
 // Owned node planes of the slab: 0..nz-1, plus plane nz at the global top.
 __device__ __forceinline__ int face_nk(const Geo& g) { return at_top(g) ? g.nz + 1 : g.nz; }
 
@@ -153,30 +157,30 @@ __device__ __forceinline__ void face_point(const Geo& g, const float* const* in,
   const long long nyf = (long long)(g.nx + 1) * nk;
   if (t < nxf) {
     const int j = (int)(t % (g.ny + 1)), k = (int)(t / (g.ny + 1)), i = g.nx;
-    const long long p = gidx(g, i, j, k);
+    const long long p = gidx(g, i, j, k), pc = p - 1;
     if (j < g.ny) out[1][p] = 0.0f;
     if (k < g.nz) out[2][p] = 0.0f;
     if (j < g.ny && k < g.nz)
-      out[3][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in[3][p], coefB(co.cell[3], co.cdz_h, k, p),
-                          0.0f, 0.0f, coefB(co.cell[3], co.cdy_h, j, p), 0.0f, 0.0f);
+      out[3][p] = yee_upd(coefA(co.cell[2], co.da_s, pc), in[3][p], coefB(co.cell[3], co.cdz_h, k, pc),
+                          0.0f, 0.0f, coefB(co.cell[3], co.cdy_h, j, pc), 0.0f, 0.0f);
   } else if (t < nxf + nyf) {
     const long long u = t - nxf;
     const int i = (int)(u % (g.nx + 1)), k = (int)(u / (g.nx + 1)), j = g.ny;
-    const long long p = gidx(g, i, j, k);
+    const long long p = gidx(g, i, j, k), pc = p - g.PX;
     if (i < g.nx) out[0][p] = 0.0f;
     if (k < g.nz) out[2][p] = 0.0f;
     if (i < g.nx && k < g.nz)
-      out[4][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in[4][p], coefB(co.cell[3], co.cdx_h, i, p),
-                          0.0f, 0.0f, coefB(co.cell[3], co.cdz_h, k, p), 0.0f, 0.0f);
+      out[4][p] = yee_upd(coefA(co.cell[2], co.da_s, pc), in[4][p], coefB(co.cell[3], co.cdx_h, i, pc),
+                          0.0f, 0.0f, coefB(co.cell[3], co.cdz_h, k, pc), 0.0f, 0.0f);
   } else {
     const long long u = t - nxf - nyf;
     const int i = (int)(u % (g.nx + 1)), j = (int)(u / (g.nx + 1)), k = g.nz;
-    const long long p = gidx(g, i, j, k);
+    const long long p = gidx(g, i, j, k), pc = p - (long long)g.PX * g.PY;
     if (i < g.nx) out[0][p] = 0.0f;
     if (j < g.ny) out[1][p] = 0.0f;
     if (i < g.nx && j < g.ny)
-      out[5][p] = yee_upd(coefA(co.cell[2], co.da_s, p), in[5][p], coefB(co.cell[3], co.cdy_h, j, p),
-                          0.0f, 0.0f, coefB(co.cell[3], co.cdx_h, i, p), 0.0f, 0.0f);
+      out[5][p] = yee_upd(coefA(co.cell[2], co.da_s, pc), in[5][p], coefB(co.cell[3], co.cdy_h, j, pc),
+                          0.0f, 0.0f, coefB(co.cell[3], co.cdx_h, i, pc), 0.0f, 0.0f);
   }
 }
 

@@ -157,6 +157,17 @@ struct FusedArgs {
   const int* diag;
   int ndiag, skew0;
   unsigned* band;
+  // Streamed upload (yb_run_streamed, MODE 2): the mirror image at the launch's
+  // start — the first skewh sweeps (skewh == nsweeps - skew0, or no tail skew)
+  // run along the mirrored diagonals, so tile row 0 starts first and the others
+  // follow in ascending order, half a sweep apart; a sweep-0 item of tile row
+  // ty loads only after upband[min(ty + 1, nty - 1)] >= up_need (the copy
+  // stream writes upband[q] = up_need once the host->device copies of tile
+  // rows 0..q have landed: cuStreamWriteValue32), and the face warps wait for
+  // the last row's word. upband == nullptr: the state is resident.
+  int skewh;
+  const unsigned* upband;
+  unsigned up_need;
 };
 
 constexpr int kChainMax = 8;
@@ -168,9 +179,9 @@ struct ChainSlab {
 // Wait-error record, 8 ints per handle: [0] code (0 none; WAIT_DEP: a
 // multi-sweep item waited for its neighbourhood; WAIT_PEER_KERNEL: the
 // folded peer wait of a boundary item; WAIT_PEER: the separate peer-wait
-// launch), [1] item (-1 if none), [2] sweep / side, [3] counter value seen,
+// launch; WAIT_UPLOAD: a first-sweep item waited for its tile rows' upload), [1] item (-1 if none), [2] sweep / side, [3] counter value seen,
 // [4] value needed.
-enum { WAIT_DEP = 1, WAIT_PEER_KERNEL = 2, WAIT_PEER = 3 };
+enum { WAIT_DEP = 1, WAIT_PEER_KERNEL = 2, WAIT_PEER = 3, WAIT_UPLOAD = 4 };
 
 // planes [kz0, kz1) of z-chunk c of a launch
 __device__ __forceinline__ void chunk_planes(const FusedArgs& a, int c, int& kz0, int& kz1) {

@@ -227,13 +227,23 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
 // top ones. (Only the last sweeps are skewed: neighbouring tile rows of one
 // sweep are a diagonal apart there, so their shared halo rows miss L2.)
 __device__ __noinline__ void skew_item(const FusedArgs& a, unsigned long long v, int T, int& sw, int& it) {
+  const unsigned long long head = (unsigned long long)a.skewh * a.nitems;
   const unsigned long long flat = (unsigned long long)a.skew0 * a.nitems;
-  if (v < flat) {
+  // Streamed upload: the first skewh sweeps in the mirrored order — position v
+  // of the head holds what position head-1-v of a skewed tail holds, with the
+  // sweeps and tile rows reversed (a dependency, one sweep later and a row
+  // apart in the tail order, becomes one sweep earlier here and still comes
+  // first), so tile row 0 of sweep 0 is first and rows follow in ascending order.
+  const bool mirror = v < head;
+  if (mirror) {
+    v = head - 1 - v;
+  } else if (v < flat) {
     sw = (int)(v / (unsigned long long)a.nitems);
     it = (int)(v - (unsigned long long)sw * a.nitems);
     return;
+  } else {
+    v -= flat;
   }
-  v -= flat;
   const int per = a.nitems / a.nty;  // items of one (sweep, tile row) group
   const int grp = (int)(v / (unsigned long long)per), rem = (int)(v - (unsigned long long)grp * per);
   int lo = 0, hi = a.ndiag - 1;  // the last diagonal d with diag[d] <= grp
@@ -244,14 +254,14 @@ __device__ __noinline__ void skew_item(const FusedArgs& a, unsigned long long v,
   }
   const int sk = max(0, (lo - a.nty + 2) / 2) + (grp - __ldg(a.diag + lo));
   const int ty = lo - 2 * sk, ch = rem / a.ntx, tx = rem - ch * a.ntx;
-  it = ch * T + ty * a.ntx + tx;
-  sw = a.skew0 + sk;
+  it = ch * T + (mirror ? a.nty - 1 - ty : ty) * a.ntx + tx;
+  sw = mirror ? a.skewh - 1 - sk : a.skew0 + sk;
 }
 
 // MODE 3 (folded exchange): spin, bounded by the launch's deadline, until a
 // neighbour's flag word reaches need.
 __device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, int* err, unsigned long long wait_ns,
-                                            int item, int side) {
+                                            int item, int side, int code = WAIT_PEER_KERNEL) {
   unsigned long long t0 = 0;
   for (long long n = 0;; ++n) {
     unsigned v;
@@ -259,7 +269,7 @@ __device__ __noinline__ void peer_flag_wait(const unsigned* f, unsigned need, in
     if ((int)(v - need) >= 0) return;
     if (n == 0) t0 = globaltimer_ns();
     else if (globaltimer_ns() - t0 > wait_ns) {  // the neighbour never signalled
-      wait_timed_out(err, WAIT_PEER_KERNEL, item, side, v, need);
+      wait_timed_out(err, code, item, side, v, need);
       return;
     }
     __nanosleep(100);
@@ -805,6 +815,10 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
       return;
     }
     float* const* fin = (a.nsweeps & 1) ? a.out : const_cast<float* const*>(reinterpret_cast<const float* const*>(a.in));
+    if (MODE == 2 && a.upband) {  // streamed upload: the face DoFs span every tile row
+      if (l == 0) peer_flag_wait(a.upband + a.nty - 1, a.up_need, a.err, a.wait_ns, -1, a.nty - 1, WAIT_UPLOAD);
+      __syncwarp();
+    }
     for (long long t = blockIdx.x * 32LL + l; t < nf; t += gridDim.x * 32LL) {
       face_point(g, a.in, fin, co, t);
       for (int q = 1; q < 2 * a.nsweeps; ++q) face_point(g, fin, fin, co, t);
@@ -867,6 +881,11 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
           return;
         }
         const FusedArgs& A = CHP ? chain[sl].a : a;
+        if (MODE == 2 && a.upband && sw == 0) {  // streamed upload: my tile rows (and the halo rows above) have landed
+          const int q = min((it % T) / a.ntx + 1, a.nty - 1);
+          peer_flag_wait(a.upband + q, a.up_need, a.err, a.wait_ns, it, q, WAIT_UPLOAD);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // the copy engine's writes, then our TMA reads
+        }
         if (MS && sw > 0) {  // the neighbourhood must have finished the previous sweep
           wait_neighbours(A, it, sw);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // their stores, then our TMA reads

@@ -26,7 +26,7 @@ def test_library_exports_all_symbols(yb):
     L = C.CDLL(yb.LIB_PATH)
     for s in header_symbols():
         assert hasattr(L, s), s
-    assert L.yb_abi_version() == 4
+    assert L.yb_abi_version() == 5
 
 
 def test_library_is_sm100a_only(yb):
