@@ -465,7 +465,7 @@ def main():
                 cell_arrays = {q: med[q] for q in want}
             e_steps = cfg_steps
 
-            def run_e2e(qskip, upload_fields=True, streamed=True):
+            def run_e2e(qskip, upload_fields=True, streamed=True, up_streamed=True):
                 s2 = make_sim()
                 if table is not None:
                     s2.add_source(*src, table)
@@ -478,11 +478,17 @@ def main():
                     dist.barrier()
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                if cell_arrays:
-                    s2.set_cell_coeffs_many(cell_arrays)
-                if upload_fields:
-                    s2.upload(host_f)
-                if ex2 is None and streamed:  # run + readback, each tile row's copies overlapping the run
+                one_call = ex2 is None and streamed and up_streamed and not qskip and (cell_arrays or upload_fields)
+                if one_call:  # upload + run + readback in one call, both transfers overlapping the run
+                    s2.run_streamed(e_steps, cell_arrays, host_f if upload_fields else None, out=host_out)
+                else:
+                    if cell_arrays:
+                        s2.set_cell_coeffs_many(cell_arrays)
+                    if upload_fields:
+                        s2.upload(host_f)
+                if one_call:
+                    pass
+                elif ex2 is None and streamed:  # run + readback, each tile row's copies overlapping the run
                     s2.run_to_host(e_steps, out=host_out)
                 else:
                     if ex2 is None:
@@ -494,6 +500,8 @@ def main():
                     s2.download(out=host_out)
                 dt = time.perf_counter() - t0
                 skipped = s2.info()["skipped_items"]
+                if one_call and e_steps % 2 == 0 and 8 <= e_steps <= 2048 and ny >= 25 and nx >= 1024:
+                    assert s2.info()["streamed_uploads"] == 1, "yb_run_streamed fell back to the phase-by-phase path"
                 if dist:  # no neighbour may still be storing into this slab's (IPC-mapped) memory
                     torch.cuda.synchronize()
                     dist.barrier()
@@ -527,8 +535,13 @@ def main():
                             "state -> download all six fields (pinned host)" if zero_start else
                             "Simulation: set_cell_coeffs + upload all six fields (pinned host) -> run(config steps) "
                             "-> download all six fields (pinned host)") +
-                           ("; run + readback as one yb_run_to_host call (each tile row's device->host copies start "
+                           ("; all of it as one yb_run_streamed call (the host->device copies go up tile row by tile "
+                            "row with the first sweeps following them, each tile row's device->host copies start "
                             "when it finished its last sweep)" if world == 1 else "")}
+            if world == 1:  # the round-2 mid-point: uploads first, then run + streamed readback
+                dm = run_e2e(False, upload_fields=not zero_start, up_streamed=False)[0]
+                e2e["upload_then_run_to_host"] = {"value": cells_total * e_steps / dm / 1e9, "unit": UNIT, "wall_s": dm,
+                                                  "note": "yb_set_cell_coeffs_n / yb_upload_fields, then yb_run_to_host"}
             if ds is not None:
                 e2e["readback_after_run"] = {"value": cells_total * e_steps / ds / 1e9, "unit": UNIT, "wall_s": ds,
                                              "note": "yb_advance then yb_download_fields (no overlap)"}

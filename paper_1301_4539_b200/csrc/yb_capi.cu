@@ -188,6 +188,8 @@ struct yb_sim {
   // streamed upload (yb_run_streamed): the first sweeps of the launch follow the host->device
   // copies tile row by tile row (per-row words written by the copy stream)
   bool upstream = false;      // the next multi-sweep launch skews its first sweeps and waits on upband
+  int* diagh_dev = nullptr;   // diagonal offsets of the head skew (FusedArgs::diagh)
+  int diagh_cap = 0, diagh_sweeps = 0, diagh_nty = 0, ndiagh = 0;
   unsigned* upband_dev = nullptr;  // nty words (monotonic)
   int upband_n = 0;
   unsigned up_base = 0;
@@ -631,7 +633,9 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
       a.band = s->band_dev;
     }
     if (s->upstream) {  // streamed upload: skewed first sweeps behind the copies (yb_run_streamed)
-      a.skewh = s->diag_sweeps;
+      a.skewh = s->diagh_sweeps;
+      a.diagh = s->diagh_dev;
+      a.ndiagh = s->ndiagh;
       a.upband = s->upband_dev;
       a.up_need = s->up_base + 1;
     }
@@ -939,6 +943,7 @@ int yb_destroy(yb_sim* s) {
   cudaFree(s->qbits);
   cudaFree(s->qskipped);
   cudaFree(s->upband_dev);
+  cudaFree(s->diagh_dev);
   cudaFree(s->done);
   cudaFree(s->srcs_dev);
   cudaFree(s->diag_dev);
@@ -1323,27 +1328,33 @@ static bool is_pinned(const void* p) {
 
 // Diagonal offsets of the skewed order for (sweeps, tile rows): diag[d] =
 // (sweep, tile row) groups with 2*sweep + row < d, d = 0 .. ndiag.
-static int ensure_drain(yb_sim* s, int nsw) {
+static int skew_table(yb_sim* s, int nsw, int*& dev, int& cap, int& sweeps, int& tnty, int& ndiag) {
   const int nty = s->nty, nd = 2 * (nsw - 1) + nty;
-  if (s->diag_sweeps != nsw || s->diag_nty != nty) {
+  if (sweeps != nsw || tnty != nty) {
     std::vector<int> h(nd + 1, 0);
     for (int d = 0; d < nd; ++d) {
       const int lo = std::max(0, (d - nty + 2) / 2), hi = std::min(nsw - 1, d / 2);
       h[d + 1] = h[d] + std::max(0, hi - lo + 1);
     }
     if (h[nd] != nsw * nty) return fail(YB_CUDA_ERROR, "internal: skewed order covers %d of %d groups", h[nd], nsw * nty);
-    if (s->diag_cap < nd + 1) {
-      cudaFree(s->diag_dev);
-      s->diag_dev = nullptr;
-      YB_CU(cudaMalloc(&s->diag_dev, (size_t)(nd + 1) * sizeof(int)));
-      s->diag_cap = nd + 1;
+    if (cap < nd + 1) {
+      cudaFree(dev);
+      dev = nullptr;
+      YB_CU(cudaMalloc(&dev, (size_t)(nd + 1) * sizeof(int)));
+      cap = nd + 1;
     }
-    YB_CU(cudaMemcpyAsync(s->diag_dev, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    YB_CU(cudaMemcpyAsync(dev, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
     YB_CU(cudaStreamSynchronize(s->stream));
-    s->diag_sweeps = nsw;
-    s->diag_nty = nty;
-    s->ndiag = nd;
+    sweeps = nsw;
+    tnty = nty;
+    ndiag = nd;
   }
+  return YB_OK;
+}
+
+static int ensure_drain(yb_sim* s, int nsw) {
+  const int nty = s->nty;
+  if (int rc = skew_table(s, nsw, s->diag_dev, s->diag_cap, s->diag_sweeps, s->diag_nty, s->ndiag)) return rc;
   if (s->band_n != nty + 1) {
     cudaFree(s->band_dev);
     s->band_dev = nullptr;
@@ -1353,6 +1364,48 @@ static int ensure_drain(yb_sim* s, int nsw) {
     s->band_n = nty + 1;
     s->band_base = s->face_base = 0;
   }
+  return YB_OK;
+}
+
+using Memcpy3DAsyncFn = CUresult (*)(const CUDA_MEMCPY3D*, CUstream);
+static Memcpy3DAsyncFn memcpy3d_fn() {
+  static Memcpy3DAsyncFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemcpy3DAsync", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<Memcpy3DAsyncFn>(p);
+  }
+  return fn;
+}
+
+// Host <-> device copy of rows [j0, j1) of every plane of a dense e0 x e1 x e2 host array and the
+// padded node box (both pitched; the copy engine, no kernel). The driver entry point with both
+// memory types stated: the runtime's cudaMemcpy3DAsync spends ~150 us of host time per call.
+static int copy_rows(const yb_sim* s, float* padded, float* dense, const int e[3], int j0, int j1, bool to_device,
+                     cudaStream_t st) {
+  CUDA_MEMCPY3D p{};
+  const size_t hp = (size_t)e[0] * 4, dp = (size_t)s->g.PX * 4;
+  p.srcMemoryType = to_device ? CU_MEMORYTYPE_HOST : CU_MEMORYTYPE_DEVICE;
+  p.dstMemoryType = to_device ? CU_MEMORYTYPE_DEVICE : CU_MEMORYTYPE_HOST;
+  if (to_device) {
+    p.srcHost = dense;
+    p.dstDevice = reinterpret_cast<CUdeviceptr>(padded);
+  } else {
+    p.srcDevice = reinterpret_cast<CUdeviceptr>(padded);
+    p.dstHost = dense;
+  }
+  p.srcPitch = to_device ? hp : dp;
+  p.srcHeight = to_device ? (size_t)e[1] : (size_t)s->g.PY;
+  p.dstPitch = to_device ? dp : hp;
+  p.dstHeight = to_device ? (size_t)s->g.PY : (size_t)e[1];
+  p.srcY = p.dstY = (size_t)j0;
+  p.WidthInBytes = hp;
+  p.Height = (size_t)(j1 - j0);
+  p.Depth = (size_t)e[2];
+  if (CUresult r = memcpy3d_fn()(&p, reinterpret_cast<CUstream>(st)))
+    return fail(YB_CUDA_ERROR, "cuMemcpy3DAsync failed (%d)", (int)r);
   return YB_OK;
 }
 
@@ -1378,14 +1431,7 @@ static int enqueue_band_readback(yb_sim* s, float* const* d, std::vector<cudaEve
       comp_ext(s->g, c, e);
       const int j0 = ty * yb::kTB2Rows, j1 = ty == s->nty - 1 ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
       if (j1 <= j0) continue;
-      cudaMemcpy3DParms p{};
-      p.srcPtr = make_cudaPitchedPtr(s->buf[fin][c], (size_t)s->g.PX * 4, (size_t)s->g.PX, (size_t)s->g.PY);
-      p.srcPos = make_cudaPos(0, (size_t)j0, 0);
-      p.dstPtr = make_cudaPitchedPtr(d[c], (size_t)e[0] * 4, (size_t)e[0], (size_t)e[1]);
-      p.dstPos = make_cudaPos(0, (size_t)j0, 0);
-      p.extent = make_cudaExtent((size_t)e[0] * 4, (size_t)(j1 - j0), (size_t)e[2]);
-      p.kind = cudaMemcpyDeviceToHost;
-      YB_CU(cudaMemcpy3DAsync(&p, s->xfer));
+      if (int rc = copy_rows(s, s->buf[fin][c], d[c], e, j0, j1, false, s->xfer)) return rc;
     }
     if (trace) YB_CU(cudaEventRecord((*tevp)[2 + ty], s->xfer));
   }
@@ -1407,7 +1453,7 @@ int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   for (int c = 0; c < 6; ++c) pinned = pinned && is_pinned(d[c]);
   const bool stream = pinned && s->variant == YB_VARIANT_TB2 && s->persist && s->zchunk2p > 0 &&
                       s->probes.empty() && !s->qskip && s->g.nzg == s->g.nz && !s->peer[0].on &&
-                      !s->peer[1].on && nsteps >= 4 && wait_value_fn() != nullptr &&
+                      !s->peer[1].on && nsteps >= 4 && wait_value_fn() != nullptr && memcpy3d_fn() != nullptr &&
                       std::getenv("YB_NO_DRAIN") == nullptr;
   if (!stream) {  // the same result, read back after the run
     if (int rc = yb_advance(s, nsteps)) return rc;
@@ -1480,20 +1526,6 @@ static WriteValue32Fn write_value_fn() {
   return fn;
 }
 
-// Host -> device copy of rows [j0, j1) of every plane of a dense e0 x e1 x e2 array into the
-// padded node box (both pitched; the copy engine, no kernel).
-static cudaError_t copy_rows_h2d(const yb_sim* s, float* padded, const float* dense, const int e[3], int j0, int j1,
-                                 cudaStream_t st) {
-  cudaMemcpy3DParms p{};
-  p.srcPtr = make_cudaPitchedPtr(const_cast<float*>(dense), (size_t)e[0] * 4, (size_t)e[0], (size_t)e[1]);
-  p.srcPos = make_cudaPos(0, (size_t)j0, 0);
-  p.dstPtr = make_cudaPitchedPtr(padded, (size_t)s->g.PX * 4, (size_t)s->g.PX, (size_t)s->g.PY);
-  p.dstPos = make_cudaPos(0, (size_t)j0, 0);
-  p.extent = make_cudaExtent((size_t)e[0] * 4, (size_t)(j1 - j0), (size_t)e[2]);
-  p.kind = cudaMemcpyHostToDevice;
-  return cudaMemcpy3DAsync(&p, st);
-}
-
 int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, const float* const* cells,
                     const float* const* in6, float* const* d) {
   if (!s || !d || (ncoef > 0 && (!which || !cells))) return fail(YB_INVALID_ARGUMENT, "null argument");
@@ -1521,18 +1553,23 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
   const int nsw = (int)(nsteps / 2);
   const bool slab = s->g.nzg != s->g.nz;
   const int nty0 = (s->g.ny + yb::kTB2Rows - 1) / yb::kTB2Rows;  // tile rows (the plan is made below)
+  // Rows under 4 KB go up faster as whole arrays (measured: pitched copies of 2 KB rows reach 30 GB/s
+  // against 45-52 GB/s contiguous, 4 KB rows 42 GB/s): such grids upload first, then stream the
+  // readback only (YB_UP_STREAM=1 forces the streamed upload, for tests and measurement)
+  const char* force = std::getenv("YB_UP_STREAM");
+  const bool wide = s->g.nx >= 1024 || (force && force[0] == '1');
   // one multi-sweep launch carries the whole run: an even step count, at most 2048 steps,
   // enough sweeps and tile rows to skew both ends; every host array page-locked
-  if (!(pinned && (ncoef > 0 || in6) && s->variant == YB_VARIANT_TB2 && s->persist && s->probes.empty() && !s->qskip &&
+  if (!(pinned && wide && (ncoef > 0 || in6) && s->variant == YB_VARIANT_TB2 && s->persist && s->probes.empty() && !s->qskip &&
         !slab && !s->peer[0].on && !s->peer[1].on && nsteps % 2 == 0 && nsw >= 4 && nsw <= 1024 && nty0 >= 4 &&
-        wait_value_fn() && write_value_fn() && std::getenv("YB_NO_DRAIN") == nullptr &&
+        wait_value_fn() && write_value_fn() && memcpy3d_fn() && std::getenv("YB_NO_DRAIN") == nullptr &&
         std::getenv("YB_NO_UPSTREAM") == nullptr))
   {
     if (std::getenv("YB_STREAM_DEBUG"))
       std::fprintf(stderr,
-                   "yb_run_streamed: phase by phase (pinned %d, arrays %d, variant %d, persist %d, probes %d, qskip %d, "
+                   "yb_run_streamed: phase by phase (pinned %d, wide %d, arrays %d, variant %d, persist %d, probes %d, qskip %d, "
                    "slab %d, nsteps %lld, tile rows %d, wait fn %d, write fn %d)\n",
-                   (int)pinned, ncoef + (in6 ? 6 : 0), s->variant, (int)s->persist, (int)s->probes.size(), (int)s->qskip,
+                   (int)pinned, (int)wide, ncoef + (in6 ? 6 : 0), s->variant, (int)s->persist, (int)s->probes.size(), (int)s->qskip,
                    (int)slab, (long long)nsteps, nty0, wait_value_fn() != nullptr, write_value_fn() != nullptr);
     return plain();
   }
@@ -1554,10 +1591,25 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
   s->q_valid = false;
   if (int rc = prepare_fused(s)) return rc;
   if (s->zchunk2p <= 0 || s->nty != nty0) return plain();
-  int K = popcount4(cell_mask(s)) > 2 ? 32 : 40;  // as yb_run_to_host; the same depth at both ends
+  // Tail skew as yb_run_to_host. Head skew: as many sweeps as the upload lasts (they trail it tile
+  // row by tile row; ~45 GB/s of pitched copies against ~185 / ~155 Gcell/s sweeps) plus two —
+  // skewed sweeps are ~15% slower (a tile row's y-halo rows miss L2), so no deeper than needed.
+  const bool heavy = popcount4(cell_mask(s)) > 2;
+  int K = heavy ? 32 : 40;
   if (const char* e = std::getenv("YB_DRAIN_K")) K = std::atoi(e);
-  K = std::max(1, std::min({K, nsw / 2, s->nty / 2 + 1}));
+  const double cells1 = (double)s->g.nx * s->g.ny * s->g.nz;
+  const double up_s = (ncoef * cells1 + (in6 ? 6.0 * cells1 : 0.0)) * 4.0 / 45e9;
+  int Kh = (int)std::ceil(up_s / (2.0 * cells1 / (heavy ? 155e9 : 185e9))) + 2;
+  if (const char* e = std::getenv("YB_UP_K")) Kh = std::atoi(e);
+  const int kmax = s->nty / 2 + 1;
+  K = std::max(1, std::min(K, kmax));
+  Kh = std::max(1, std::min(Kh, kmax));
+  if (K + Kh > nsw) {  // a short run: share the sweeps in proportion
+    Kh = std::max(1, std::min(nsw - 1, (int)((long long)nsw * Kh / (K + Kh))));
+    K = nsw - Kh;
+  }
   if (int rc = ensure_drain(s, K)) return rc;
+  if (int rc = skew_table(s, Kh, s->diagh_dev, s->diagh_cap, s->diagh_sweeps, s->diagh_nty, s->ndiagh)) return rc;
   if (int rc = ensure_xfer(s)) return rc;
   if (s->upband_n != s->nty) {
     cudaFree(s->upband_dev);
@@ -1572,42 +1624,77 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
   YB_CU(cudaStreamWaitEvent(s->xfer, s->xev[6], 0));
   WriteValue32Fn wr = write_value_fn();
   CUstream xs = reinterpret_cast<CUstream>(s->xfer);
+  // YB_DRAIN_TRACE=1 (measurement): events after every tile row's copies (both directions) and
+  // around the launch, printed to stderr as ms from the first copy
+  const bool trace = std::getenv("YB_DRAIN_TRACE") != nullptr;
+  std::vector<cudaEvent_t> uev, tev;
+  if (trace) {
+    uev.resize(s->nty + 1);
+    tev.resize(s->nty + 2);
+    for (cudaEvent_t& e : uev) YB_CU(cudaEventCreate(&e));
+    for (cudaEvent_t& e : tev) YB_CU(cudaEventCreate(&e));
+    YB_CU(cudaEventRecord(uev[s->nty], s->xfer));
+  }
   const unsigned need = s->up_base + 1;
   const int ce[3] = {s->g.nx, s->g.ny, s->g.nz};
+  if (trace) YB_CU(cudaEventRecord(tev[0], s->stream));
+  s->drain = true;
+  s->upstream = true;
+  const int cur0 = s->cur;  // the launch's input state (step_tb2 flips to the final-state buffer)
+  const int rc = step_tb2(s, zfull(s), s->zchunk2p, true, nsw);
+  s->drain = false;
+  s->upstream = false;
+  s->up_base = need;
+  if (rc) return rc;
+  // the launch is in flight (its first-sweep items poll the row words): now the copies
+  // (one copy stream: the arrays alternating over two streams measured no faster)
   for (int ty = 0; ty < s->nty; ++ty) {
     const int j0 = ty * yb::kTB2Rows;
     const bool last = ty == s->nty - 1;
     for (int i = 0; i < ncoef; ++i) {
       const int j1 = last ? ce[1] : std::min(j0 + yb::kTB2Rows, ce[1]);
-      if (j1 > j0) YB_CU(copy_rows_h2d(s, s->cell[which[i]], cells[i], ce, j0, j1, s->xfer));
+      if (j1 > j0)
+        if (int rc = copy_rows(s, s->cell[which[i]], const_cast<float*>(cells[i]), ce, j0, j1, true, s->xfer)) return rc;
     }
     if (in6)
       for (int c = 0; c < 6; ++c) {
         int e[3];
         comp_ext(s->g, c, e);
         const int j1 = last ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
-        if (j1 > j0) YB_CU(copy_rows_h2d(s, s->buf[s->cur][c], in6[c], e, j0, j1, s->xfer));
+        if (j1 > j0)
+          if (int rc = copy_rows(s, s->buf[cur0][c], const_cast<float*>(in6[c]), e, j0, j1, true, s->xfer)) return rc;
       }
     if (CUresult r = wr(xs, reinterpret_cast<CUdeviceptr>(s->upband_dev + ty), need, 0))
       return fail(YB_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", (int)r);
+    if (trace) YB_CU(cudaEventRecord(uev[ty], s->xfer));
   }
-  s->drain = true;
-  s->upstream = true;
-  const int rc = step_tb2(s, zfull(s), s->zchunk2p, true, nsw);
-  s->drain = false;
-  s->upstream = false;
-  s->up_base = need;
-  if (rc) return rc;
   s->step_index += 2 * nsw;
   s->steps += 2 * nsw;
   for (int i = 0; i < ncoef; ++i)  // the arrays' clamped duplicates (other kernels read them), behind the run
     YB_CU(yb::launch_clamp_fill(s->g, s->cell[which[i]], 0, s->g.nz - 1, s->stream));
-  if (int rc2 = enqueue_band_readback(s, d, nullptr)) return rc2;
+  if (trace) YB_CU(cudaEventRecord(tev[1], s->stream));
+  if (int rc2 = enqueue_band_readback(s, d, trace ? &tev : nullptr)) return rc2;
   s->streamed += 1;
   s->streamed_up += 1;
   YB_CU(cudaEventRecord(s->xev[6], s->xfer));
   YB_CU(cudaStreamWaitEvent(s->stream, s->xev[6], 0));
   YB_CU(cudaStreamSynchronize(s->stream));
+  if (trace) {
+    auto ms = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, uev[s->nty], e);
+      return t;
+    };
+    std::fprintf(stderr, "yb_run_streamed: %d sweeps (first %d, last %d skewed), %d tile rows; launch %.1f .. %.1f ms; rows up (ms):",
+                 nsw, Kh, K, s->nty, ms(tev[0]), ms(tev[1]));
+    const int st = std::max(1, s->nty / 8);
+    for (int ty = 0; ty < s->nty; ty += st) std::fprintf(stderr, " %d:%.1f", ty, ms(uev[ty]));
+    std::fprintf(stderr, " last:%.1f; rows down (ms):", ms(uev[s->nty - 1]));
+    for (int ty = 0; ty < s->nty; ty += st) std::fprintf(stderr, " %d:%.1f", ty, ms(tev[2 + ty]));
+    std::fprintf(stderr, " last:%.1f\n", ms(tev[1 + s->nty]));
+    for (cudaEvent_t e : uev) cudaEventDestroy(e);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
   return check_wait_error(s);
 }
 

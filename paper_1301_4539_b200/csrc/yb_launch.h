@@ -158,7 +158,7 @@ struct FusedArgs {
   int ndiag, skew0;
   unsigned* band;
   // Streamed upload (yb_run_streamed, MODE 2): the mirror image at the launch's
-  // start — the first skewh sweeps (skewh == nsweeps - skew0, or no tail skew)
+  // start — the first skewh sweeps (skewh <= skew0; their own table diagh / ndiagh)
   // run along the mirrored diagonals, so tile row 0 starts first and the others
   // follow in ascending order, half a sweep apart; a sweep-0 item of tile row
   // ty loads only after upband[min(ty + 1, nty - 1)] >= up_need (the copy
@@ -166,6 +166,8 @@ struct FusedArgs {
   // rows 0..q have landed: cuStreamWriteValue32), and the face warps wait for
   // the last row's word. upband == nullptr: the state is resident.
   int skewh;
+  const int* diagh;
+  int ndiagh;
   const unsigned* upband;
   unsigned up_need;
 };

@@ -246,13 +246,14 @@ __device__ __noinline__ void skew_item(const FusedArgs& a, unsigned long long v,
   }
   const int per = a.nitems / a.nty;  // items of one (sweep, tile row) group
   const int grp = (int)(v / (unsigned long long)per), rem = (int)(v - (unsigned long long)grp * per);
-  int lo = 0, hi = a.ndiag - 1;  // the last diagonal d with diag[d] <= grp
+  const int* dg = mirror ? a.diagh : a.diag;
+  int lo = 0, hi = (mirror ? a.ndiagh : a.ndiag) - 1;  // the last diagonal d with dg[d] <= grp
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(a.diag + mid) <= grp) lo = mid;
+    if (__ldg(dg + mid) <= grp) lo = mid;
     else hi = mid - 1;
   }
-  const int sk = max(0, (lo - a.nty + 2) / 2) + (grp - __ldg(a.diag + lo));
+  const int sk = max(0, (lo - a.nty + 2) / 2) + (grp - __ldg(dg + lo));
   const int ty = lo - 2 * sk, ch = rem / a.ntx, tx = rem - ch * a.ntx;
   it = ch * T + (mirror ? a.nty - 1 - ty : ty) * a.ntx + tx;
   sw = mirror ? a.skewh - 1 - sk : a.skew0 + sk;

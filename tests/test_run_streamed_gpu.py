@@ -15,6 +15,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def force_streamed_upload(monkeypatch):
+    # rows under 4 KB (nx < 1024) upload as whole arrays by default (faster copies); the cut-down
+    # grids here force the tile-row upload so that path is what is tested
+    monkeypatch.setenv("YB_UP_STREAM", "1")
+
+
 def bits(a):
     return np.ascontiguousarray(a).view(np.uint32)
 
@@ -70,6 +77,8 @@ CASES = [
     (300, 90, 64, 8, (3, 3, (0, 1, 2, 3)), 6, False),    # the shortest streamed run (4 sweeps)
     (200, 120, 33, 40, (4, -1, (0, 1, 2, 3)), 7, True),  # uniform Ca / Da / Db given as full arrays
     (128, 256, 24, 100, None, 5, False),                 # fields only, 50 sweeps, both skews 16 deep
+    (140, 100, 30, 14, (5, 5, (0, 1, 2, 3)), 8, True),   # an odd number of sweeps (the final state in the other buffer)
+    (96, 64, 20, 22, None, 9, True),                     # odd, fields only
 ]
 
 
@@ -120,7 +129,7 @@ def test_run_streamed_vs_oracle(yb):
         assert np.array_equal(bits(got[c]), bits(want[c])), c
 
 
-def test_run_streamed_repeated_and_fallbacks(yb):
+def test_run_streamed_repeated_and_fallbacks(yb, monkeypatch):
     nx, ny, nz = 160, 72, 28
     cells, fields = inputs(yb, nx, ny, nz, (2, 2, (0, 1, 2, 3)), 3)
     pc = {q: pin(a) for q, a in cells.items()}
@@ -147,6 +156,14 @@ def test_run_streamed_repeated_and_fallbacks(yb):
         for c in range(6):
             assert np.array_equal(bits(got[c]), bits(want[c])), c
         assert s.info()["streamed_uploads"] == n_up
+        # a narrow grid without the override: whole-array uploads, then the streamed readback
+        monkeypatch.delenv("YB_UP_STREAM")
+        s.step_index = 0
+        n_rd = s.info()["streamed_readbacks"]
+        got = s.run_streamed(10, pc, pf, out=out)
+        for c in range(6):
+            assert np.array_equal(bits(got[c]), bits(want[c])), c
+        assert s.info()["streamed_uploads"] == n_up and s.info()["streamed_readbacks"] == n_rd + 1
 
 
 def test_run_streamed_argument_errors(yb):
