@@ -1384,7 +1384,7 @@ static Memcpy3DAsyncFn memcpy3d_fn() {
 // padded node box (both pitched; the copy engine, no kernel). The driver entry point with both
 // memory types stated: the runtime's cudaMemcpy3DAsync spends ~150 us of host time per call.
 static int copy_rows(const yb_sim* s, float* padded, float* dense, const int e[3], int j0, int j1, bool to_device,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool host_block = false) {
   CUDA_MEMCPY3D p{};
   const size_t hp = (size_t)e[0] * 4, dp = (size_t)s->g.PX * 4;
   p.srcMemoryType = to_device ? CU_MEMORYTYPE_HOST : CU_MEMORYTYPE_DEVICE;
@@ -1396,11 +1396,15 @@ static int copy_rows(const yb_sim* s, float* padded, float* dense, const int e[3
     p.srcDevice = reinterpret_cast<CUdeviceptr>(padded);
     p.dstHost = dense;
   }
+  // host side: the whole dense array (rows j0.. of every plane), or — host_block — a dense block
+  // of just these rows per plane (a staging chunk)
+  const size_t hh = host_block ? (size_t)(j1 - j0) : (size_t)e[1], hy = host_block ? 0 : (size_t)j0;
   p.srcPitch = to_device ? hp : dp;
-  p.srcHeight = to_device ? (size_t)e[1] : (size_t)s->g.PY;
+  p.srcHeight = to_device ? hh : (size_t)s->g.PY;
   p.dstPitch = to_device ? dp : hp;
-  p.dstHeight = to_device ? (size_t)s->g.PY : (size_t)e[1];
-  p.srcY = p.dstY = (size_t)j0;
+  p.dstHeight = to_device ? (size_t)s->g.PY : hh;
+  p.srcY = to_device ? hy : (size_t)j0;
+  p.dstY = to_device ? (size_t)j0 : hy;
   p.WidthInBytes = hp;
   p.Height = (size_t)(j1 - j0);
   p.Depth = (size_t)e[2];
@@ -1440,6 +1444,84 @@ static int enqueue_band_readback(yb_sim* s, float* const* d, std::vector<cudaEve
   return YB_OK;
 }
 
+// A tile row's rows of one component as a dense block must fit a staging chunk.
+static bool band_fits_staging(const yb_sim* s) {
+  return (size_t)(yb::kTB2Rows + 1) * (s->g.nx + 1) * (s->g.nz + 1) * 4 <= yb::kStageBytes;
+}
+
+// The same readback into pageable buffers (the reference's own storage, array3.hpp:120): each
+// (tile row, component) unit goes through the pinned staging ring of yb_xfer.cu — its pitched
+// device-to-host copy lands in a chunk as a dense block (the rows x e0 of every plane), and the
+// copy threads move the block's planes to their places in the caller's array while the next
+// units' copies run and the rows above still sweep. Returns when all six arrays hold the state.
+static int band_readback_pageable(yb_sim* s, float* const* d) {
+  const int nch = (s->g.nz + s->zchunk2p - 1) / s->zchunk2p;
+  const unsigned per = (unsigned)(s->ntx * nch * yb::kTB2RowWarps);
+  const unsigned band_need = s->band_base + per, face_need = s->face_base + s->last_grid;
+  s->band_base += per;
+  s->face_base += s->last_grid;
+  WaitValue32Fn wv = wait_value_fn();
+  CUstream xs = reinterpret_cast<CUstream>(s->xfer);
+  auto dptr = [&](int q) { return reinterpret_cast<CUdeviceptr>(s->band_dev + q); };
+  struct Unit {
+    int ty, c, j0, j1, e[3];
+    bool first;
+  };
+  std::vector<Unit> units;
+  for (int ty = 0; ty < s->nty; ++ty) {
+    bool first = true;
+    for (int c = 0; c < 6; ++c) {
+      Unit u{};
+      comp_ext(s->g, c, u.e);
+      u.ty = ty;
+      u.c = c;
+      u.j0 = ty * yb::kTB2Rows;
+      u.j1 = ty == s->nty - 1 ? u.e[1] : std::min(u.j0 + yb::kTB2Rows, u.e[1]);
+      if (u.j1 <= u.j0) continue;
+      u.first = first;
+      first = false;
+      units.push_back(u);
+    }
+  }
+  std::lock_guard<std::mutex> ring(yb::stage_lock());
+  YB_CU(yb::stage_init());
+  if (CUresult r = wv(xs, dptr(s->nty), face_need, CU_STREAM_WAIT_VALUE_GEQ))
+    return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
+  const int fin = s->cur;
+  auto issue = [&](size_t i) -> int {
+    const Unit& u = units[i];
+    const int k = (int)(i % yb::kStageChunks);
+    YB_CU(yb::stage_acquire(k, s->device));
+    if (u.first)
+      if (CUresult r = wv(xs, dptr(u.ty), band_need, CU_STREAM_WAIT_VALUE_GEQ))
+        return fail(YB_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", (int)r);
+    if (int rc = copy_rows(s, s->buf[fin][u.c], static_cast<float*>(yb::stage_buf(k)), u.e, u.j0, u.j1, false, s->xfer,
+                           true))
+      return rc;
+    YB_CU(cudaEventRecord(yb::stage_event(k), s->xfer));
+    return YB_OK;
+  };
+  for (size_t i = 0; i < std::min<size_t>(units.size(), yb::kStageChunks); ++i)
+    if (int rc = issue(i)) return rc;
+  for (size_t i = 0; i < units.size(); ++i) {
+    const Unit& u = units[i];
+    const int k = (int)(i % yb::kStageChunks);
+    YB_CU(cudaEventSynchronize(yb::stage_event(k)));
+    const size_t blk = (size_t)(u.j1 - u.j0) * u.e[0];  // floats of one plane's rows
+    const float* src = static_cast<const float*>(yb::stage_buf(k));
+    float* dst = d[u.c];
+    const int tasks = std::min(u.e[2], 16);
+    yb::par_for(tasks, [&](int t) {
+      const int k0 = (int)((long long)u.e[2] * t / tasks), k1 = (int)((long long)u.e[2] * (t + 1) / tasks);
+      for (int kk = k0; kk < k1; ++kk)
+        std::memcpy(dst + ((size_t)kk * u.e[1] + u.j0) * u.e[0], src + (size_t)kk * blk, blk * 4);
+    });
+    if (i + yb::kStageChunks < units.size())
+      if (int rc = issue(i + yb::kStageChunks)) return rc;
+  }
+  return YB_OK;
+}
+
 int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   if (!s || !d) return fail(YB_INVALID_ARGUMENT, "null argument");
   for (int c = 0; c < 6; ++c)
@@ -1449,9 +1531,12 @@ int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   YB_CU(cudaSetDevice(s->device));
   if (s->variant != YB_VARIANT_NAIVE)
     if (int rc = prepare_fused(s)) return rc;  // sets the multi-sweep chunk (zchunk2p)
-  bool pinned = true;
-  for (int c = 0; c < 6; ++c) pinned = pinned && is_pinned(d[c]);
-  const bool stream = pinned && s->variant == YB_VARIANT_TB2 && s->persist && s->zchunk2p > 0 &&
+  bool pinned = true, pageable = band_fits_staging(s) && std::getenv("YB_NO_PAGEABLE_DRAIN") == nullptr;
+  for (int c = 0; c < 6; ++c) {
+    pinned = pinned && is_pinned(d[c]);
+    pageable = pageable && yb::host_is_pageable(d[c]);
+  }
+  const bool stream = (pinned || pageable) && s->variant == YB_VARIANT_TB2 && s->persist && s->zchunk2p > 0 &&
                       s->probes.empty() && !s->qskip && s->g.nzg == s->g.nz && !s->peer[0].on &&
                       !s->peer[1].on && nsteps >= 4 && wait_value_fn() != nullptr && memcpy3d_fn() != nullptr &&
                       std::getenv("YB_NO_DRAIN") == nullptr;
@@ -1490,7 +1575,13 @@ int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   if (trace) YB_CU(cudaEventRecord(tev[1], s->stream));
   s->step_index += 2 * nsw;
   s->steps += 2 * nsw;
-  if (int rc = enqueue_band_readback(s, d, trace ? &tev : nullptr)) return rc;
+  if (pinned) {
+    if (int rc = enqueue_band_readback(s, d, trace ? &tev : nullptr)) return rc;
+  } else {  // pageable buffers: through the staging ring, back when they hold the state
+    if (int rc = band_readback_pageable(s, d)) return rc;
+    if (trace)
+      for (int ty = 0; ty < s->nty; ++ty) YB_CU(cudaEventRecord(tev[2 + ty], s->xfer));
+  }
   s->streamed += 1;
   YB_CU(cudaEventRecord(s->xev[6], s->xfer));
   YB_CU(cudaStreamWaitEvent(s->stream, s->xev[6], 0));

@@ -5,6 +5,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <functional>
+#include <mutex>
+
 #include "yb_device.cuh"
 
 namespace yb {
@@ -314,4 +317,17 @@ namespace yb {
 bool host_is_pageable(const void* p);
 cudaError_t copy_h2d(void* dst, const void* src, size_t n, cudaStream_t st);
 cudaError_t copy_d2h(void* dst, const void* src, size_t n, cudaStream_t st);
+// The pinned staging ring of yb_xfer.cu, for transfers that stage pieces of their own shape
+// (the tile-row readback of yb_run_to_host into pageable memory): hold stage_lock() for the
+// whole transfer; stage_acquire(k) waits for chunk k's last DMA (its event, re-created on
+// `device`); record stage_event(k) behind the chunk's next DMA. par_for runs fn(0..n-1) over the
+// copy-thread pool (the caller's thread included).
+constexpr int kStageChunks = 4;
+constexpr size_t kStageBytes = size_t(32) << 20;
+std::mutex& stage_lock();
+cudaError_t stage_init();
+void* stage_buf(int k);
+cudaError_t stage_acquire(int k, int device);
+cudaEvent_t stage_event(int k);
+void par_for(int n, const std::function<void(int)>& fn);
 }  // namespace yb

@@ -165,6 +165,14 @@ struct Staging {
 
 }  // namespace
 
+std::mutex& stage_lock() { return Staging::get().m; }
+cudaError_t stage_init() { return Staging::get().init(); }
+void* stage_buf(int k) { return Staging::get().buf[k]; }
+cudaError_t stage_acquire(int k, int device) { return Staging::get().acquire(k, device); }
+cudaEvent_t stage_event(int k) { return Staging::get().ev[k]; }
+void par_for(int n, const std::function<void(int)>& fn) { CopyPool::get().run(n, fn); }
+static_assert(kStageChunks == Staging::kChunks && kStageBytes == Staging::kChunk, "staging ring shape");
+
 bool host_is_pageable(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {

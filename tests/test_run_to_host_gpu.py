@@ -5,7 +5,8 @@ polled by the copy stream). The result must be bit-identical to run +
 download — and to the C oracle — whatever the grid shape (ragged tiles,
 rows not a multiple of 8, one tile row), step count (odd, short, long),
 medium, sources and initial state, also on repeated calls on one handle
-(monotonic counters) and from pageable buffers (the non-streamed path)."""
+(monotonic counters) and from pageable buffers (streamed through the pinned
+staging ring; YB_NO_PAGEABLE_DRAIN=1 takes the phase-by-phase path)."""
 import numpy as np
 import pytest
 
@@ -112,7 +113,7 @@ def test_run_to_host_fallbacks(yb):
         setup(yb, s, nx, ny, nz, (2, -1), 4, True)
         s.run(steps)
         want = s.download()
-    for kind in ("pageable", "fused", "short"):
+    for kind in ("fused", "short"):
         variant = yb.VARIANT_FUSED if kind == "fused" else yb.VARIANT_TB2
         with yb.Simulation(nx, ny, nz, variant=variant) as s:
             setup(yb, s, nx, ny, nz, (2, -1), 4, True)
@@ -120,7 +121,36 @@ def test_run_to_host_fallbacks(yb):
                 s.run(steps - 3)
                 got = s.run_to_host(3, out=pinned_like(yb, nx, ny, nz))
             else:
-                got = s.run_to_host(steps, out=None if kind == "pageable" else pinned_like(yb, nx, ny, nz))
+                got = s.run_to_host(steps, out=pinned_like(yb, nx, ny, nz))
             assert s.info()["streamed_readbacks"] == 0, kind
         for c in range(6):
             assert np.array_equal(bits(got[c]), bits(want[c])), (kind, c)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_run_to_host_pageable_streams_through_staging(yb, case, monkeypatch):
+    """Pageable destination buffers (std::vector storage of a drop-in caller): the tile rows go
+    through the pinned staging ring while the rows above still sweep; same bits as run + download,
+    also with the staged path switched off."""
+    nx, ny, nz, steps, medium, fseed, src = case
+    with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2) as s:
+        setup(yb, s, nx, ny, nz, medium, fseed, src)
+        s.run(steps)
+        want = s.download()
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("YB_NO_PAGEABLE_DRAIN", "1")
+        with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2) as s:
+            setup(yb, s, nx, ny, nz, medium, fseed, src)
+            got = s.run_to_host(steps)  # fresh numpy arrays: pageable
+            assert s.info()["streamed_readbacks"] == (0 if off else 1)
+            got2 = s.run_to_host(4) if not off else None  # the ring and the counters are reusable
+        for c in range(6):
+            assert np.array_equal(bits(got[c]), bits(want[c])), (case, off, c)
+        if got2 is not None:
+            with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2) as s:
+                setup(yb, s, nx, ny, nz, medium, fseed, src)
+                s.run(steps + 4)
+                want2 = s.download()
+            for c in range(6):
+                assert np.array_equal(bits(got2[c]), bits(want2[c])), (case, c)
