@@ -663,6 +663,13 @@ struct RunOptions {
   // extensions: the CUDA device and the step kernel (YB_VARIANT_*; TB2 = the fastest)
   int device = 0;
   int kernel = YB_VARIANT_TB2;
+  /// When run() brings the state back into the host FieldSet that fields() returns. The reference's
+  /// FieldSet is the live state (runner.hpp:236); here it is a mirror of the device state.
+  /// Lazy: on the first fields() access after a run. Eager: as part of run() (yb_run_to_host: the
+  /// readback overlaps the last sweeps, also into this pageable storage). Auto (default): eager
+  /// for runs of at least 64 steps, until a readback was paid for and never looked at.
+  enum class Readback { Lazy, Eager, Auto };
+  Readback readback = Readback::Auto;
 };
 
 /// Per-cell coefficient selector (extension; the reference has none).
@@ -751,6 +758,10 @@ class Simulation {
   std::vector<ProbeRecord> run(long long n_steps) {
     if (n_steps < 0) throw std::invalid_argument("run: negative step count");
     push_if_dirty();
+    if (eager_unread_) auto_lazy_ = true;  // the last eager readback was never looked at
+    using RB = typename RunOptions<Real>::Readback;
+    const bool eager = !opts_.after_step && n_steps > 0 &&
+                       (opts_.readback == RB::Eager || (opts_.readback == RB::Auto && n_steps >= 64 && !auto_lazy_));
     const double t0 = now();
     std::vector<ProbeRecord> records;
     long long t = step_;
@@ -771,7 +782,13 @@ class Simulation {
         }
       }
       load_sources(t, n);
-      detail::check(yb_advance(h_, n));
+      if (eager) {  // one chunk (no after_step): advance and read back in one overlapped call
+        float* d6[6];
+        for (Comp c : kAllComps) d6[comp_index(c)] = mirror_.field(c).data();
+        detail::check(yb_run_to_host(h_, n, d6));
+      } else {
+        detail::check(yb_advance(h_, n));
+      }
       t += n;
       step_ = t;
       if (opts_.after_step) {
@@ -783,7 +800,9 @@ class Simulation {
     }
     if (!opts_.probes.empty()) drain_probes(records);
     detail::check(yb_synchronize(h_));
-    have_mirror_ = false;
+    have_mirror_ = eager;
+    eager_unread_ = eager;
+    if (eager) mirror_.step_index = step_;
     stats_.total_seconds += now() - t0;
     stats_.steps += n_steps;
     yb_info inf{};
@@ -850,7 +869,9 @@ class Simulation {
     have_mirror_ = false;
   }
   void sync_mirror() {
+    eager_unread_ = false;  // the caller looks at the state after its runs
     if (have_mirror_) return;
+    auto_lazy_ = false;
     float* d6[6];
     for (Comp c : kAllComps) d6[comp_index(c)] = mirror_.field(c).data();
     detail::check(yb_download_fields(h_, d6));
@@ -906,6 +927,7 @@ class Simulation {
   yb_sim* h_ = nullptr;
   long long step_ = 0;
   bool have_mirror_ = false, dirty_ = false;
+  bool eager_unread_ = false, auto_lazy_ = false;  // RunOptions::Readback::Auto bookkeeping
   RunStats stats_;
 };
 

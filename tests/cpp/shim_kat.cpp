@@ -6,6 +6,7 @@
 #include "yeeb200/yeeblock.hpp"
 
 #include <cstdio>
+#include <utility>
 #include <cstdlib>
 
 using namespace yeeblock;
@@ -206,6 +207,45 @@ int main() {
     sim.snapshot_h();
     sim.fields().hx(2, 1, 1) = 0.5f;
     CHECK(sim.total_energy() == 1.5);
+  }
+  // RunOptions::Readback (extension): the host FieldSet after run() is the same whether it is read
+  // back lazily (first fields() access), eagerly inside run() (the streamed readback into this
+  // pageable storage) or by the Auto policy — across consecutive runs, with and without a look at
+  // the fields in between, and after host-side writes.
+  {
+    GridSpec<float> g;
+    g.nx = 96, g.ny = 40, g.nz = 24;
+    g.dx.assign(g.nx, 1.0f), g.dy.assign(g.ny, 1.0f), g.dz.assign(g.nz, 1.0f);
+    g.dt = static_cast<float>(stable_dt(g, 0.99));
+    FieldSet<float> init(g.dims());
+    for (Comp c : kAllComps)
+      for (std::size_t q = 0; q < init.field(c).size(); ++q)
+        init.field(c).data()[q] = std::sin(0.11f * q + comp_index(c));
+    using RB = RunOptions<float>::Readback;
+    std::string digest[3][3];
+    int p = 0;
+    for (RB mode : {RB::Lazy, RB::Eager, RB::Auto}) {
+      RunOptions<float> o;
+      o.quiescent_skip = false;
+      o.readback = mode;
+      Simulation<float> sim(g, o);
+      sim.fields() = init;
+      sim.run(70);
+      digest[p][0] = field_digest_hex(std::as_const(sim).fields());
+      sim.run(66);  // no look at the fields after this one ...
+      sim.run(64);  // ... so Auto stops reading back eagerly here
+      digest[p][1] = field_digest_hex(std::as_const(sim).fields());
+      sim.fields().ez(5, 6, 7) += 1.0f;  // host-side write: uploaded by the next run
+      sim.run(65);
+      digest[p][2] = field_digest_hex(std::as_const(sim).fields());
+      CHECK(std::as_const(sim).fields().step_index == 70 + 66 + 64 + 65);
+      ++p;
+    }
+    for (int q = 0; q < 3; ++q) {
+      CHECK(digest[0][q] == digest[1][q]);
+      CHECK(digest[0][q] == digest[2][q]);
+    }
+    CHECK(digest[0][0] != digest[0][1]);
   }
   if (failures) {
     std::fprintf(stderr, "%d failure(s)\n", failures);
