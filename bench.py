@@ -240,8 +240,9 @@ def shim_pageable_e2e(cfg, variant, device):
         return {"unavailable": (r.stderr or r.stdout).strip().splitlines()[-1:] or ["yb_e2e failed"]}
     out = json.loads(r.stdout.strip().splitlines()[-1])
     out["path"] = ("C++ drop-in: Simulation<float>(grid, layout, Variant, RunOptions) -> set_cell_coefficients "
-                   "(std::vector) -> run(config steps) (uploads the host FieldSet) -> fields() read back; "
-                   "pageable host memory")
+                   "(std::vector) -> run(config steps) (uploads the host FieldSet if it was written; "
+                   "RunOptions::readback Auto: the state streams back into the FieldSet's std::vector storage "
+                   "through the pinned staging ring while the last sweeps run) -> fields(); pageable host memory")
     return out
 
 
