@@ -165,6 +165,7 @@ struct yb_sim {
   bool pending_full = false;  // ... whose boundary launch already covered every plane
   bool persist = true;        // multi-sweep two-step launches (YB_TB2_PERSIST=0: off)
   int pf2 = 0;                // two-step L2 prefetch distance in planes (YB_TB2_PF)
+  int xblock = 4;             // multi-sweep item order: column blocks of this many tiles (YB_TB2_XBLOCK; 0: row-major)
   bool qskip = false;         // yb_set_quiescent_skip
   bool q_valid = false;       // quiescent map matches the state buffers
   unsigned* qbits = nullptr;  // quiescent map (tiles x words)
@@ -626,6 +627,7 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
     a.done = s->done;
     a.epoch = s->epoch;
     a.srcs = s->srcs_dev;
+    a.xblock = s->xblock;
     if (s->drain) {  // streamed readback: skewed last sweeps, band counters (set up by yb_run_to_host)
       a.diag = s->diag_dev;
       a.ndiag = s->ndiag;
@@ -665,7 +667,31 @@ int step_tb2(yb_sim* s, ZPart z, int zchunk, bool flip, int nsweeps = 1) {
     tp = &s->timers[s->timers_used++];
     YB_CU(cudaEventRecord(tp->a, st));
   }
+#ifdef YB_TB2_STAMP
+  unsigned long long* stamp_dev = nullptr;
+  const char* stamp_file = std::getenv("YB_TB2_STAMP_FILE");
+  const size_t stamp_n = 2 * (size_t)a.nitems * nsweeps;
+  if (stamp_file && nsweeps > 1) {
+    YB_CU(cudaMalloc(&stamp_dev, stamp_n * 8));
+    YB_CU(cudaMemsetAsync(stamp_dev, 0, stamp_n * 8, st));
+    a.stamp = stamp_dev;
+  }
+#endif
   YB_CU(yb::launch_tb2(a, s->tm2[s->cur], s->tm2[nxt], mask, grid, smem, st));
+#ifdef YB_TB2_STAMP
+  if (stamp_dev) {
+    std::vector<unsigned long long> h(stamp_n);
+    YB_CU(cudaStreamSynchronize(st));
+    YB_CU(cudaMemcpy(h.data(), stamp_dev, stamp_n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(stamp_dev);
+    if (FILE* f = std::fopen(stamp_file, "wb")) {
+      const int hdr[6] = {a.nitems, nsweeps, a.ntx, a.nty, a.zchunk, s->g.nz};
+      std::fwrite(hdr, sizeof hdr, 1, f);
+      std::fwrite(h.data(), 8, stamp_n, f);
+      std::fclose(f);
+    }
+  }
+#endif
   s->last_grid = grid.x;
   base += (unsigned long long)a.nitems * nsweeps + grid.x;
   if (nsweeps > 1) s->epoch += (unsigned)nsweeps;
@@ -844,6 +870,7 @@ int yb_create(const yb_desc* d, yb_sim** out) {
   if (const char* e = std::getenv("YB_STPOL")) s->store_policy = std::atoi(e);
   if (const char* e = std::getenv("YB_TB2_PERSIST")) s->persist = std::atoi(e) != 0;
   if (const char* e = std::getenv("YB_TB2_PF")) s->pf2 = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("YB_TB2_XBLOCK")) s->xblock = std::max(0, std::atoi(e));
   Geo& g = s->g;
   g.nx = d->nx;
   g.ny = d->ny;

@@ -173,6 +173,16 @@ struct FusedArgs {
   int ndiagh;
   const unsigned* upband;
   unsigned up_need;
+  // Multi-sweep launches hand out a sweep's tiles in columns xblock tiles wide (within a z-chunk:
+  // column block, then tile row, then tile column), not row by row. Persistent CTAs take items at
+  // a steady rate (one every item_time / CTAs: ~1.7 planes of progress on config 4), so two items
+  // q queue positions apart run ~1.7 q planes apart, and L2 keeps the rows they share for only
+  // ~6-9 planes: row-major order puts y-neighbours ntx (8) positions apart (measured median 11.7
+  // planes, tools/stamp_drift.py), a 2-wide column 2. 0 or >= ntx: row-major.
+  int xblock;
+#ifdef YB_TB2_STAMP  // measurement builds: globaltimer at each item's first and last load (tools/stamp_drift.py)
+  unsigned long long* stamp;
+#endif
 };
 
 constexpr int kChainMax = 8;

@@ -217,6 +217,19 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
+// Position q of a sweep's sweep-major part -> item (FusedArgs::xblock): z-chunk, then column
+// block of xblock tiles, then tile row, then tile column within the block.
+__device__ __forceinline__ int block_order(const FusedArgs& a, int q, int T) {
+  const int W = a.xblock;
+  if (W <= 0 || W >= a.ntx) return q;
+  const int ch = q / T, r = q - ch * T;
+  const int per = W * a.nty;                   // items of a full column block
+  const int b = min(r / per, (a.ntx - 1) / W);  // the last block may be narrower
+  const int r2 = r - b * per, wb = min(W, a.ntx - b * W);
+  const int ty = r2 / wb, tx = b * W + (r2 - ty * wb);
+  return ch * T + ty * a.ntx + tx;
+}
+
 // Streamed readback order (FusedArgs::diag): work item v of a multi-sweep
 // launch -> (sweep, item); sweeps before skew0 sweep-major, the rest along
 // y-skewed diagonals d = 2*(sweep - skew0) + tile row, sweeps ascending within
@@ -239,7 +252,7 @@ __device__ __noinline__ void skew_item(const FusedArgs& a, unsigned long long v,
     v = head - 1 - v;
   } else if (v < flat) {
     sw = (int)(v / (unsigned long long)a.nitems);
-    it = (int)(v - (unsigned long long)sw * a.nitems);
+    it = block_order(a, (int)(v - (unsigned long long)sw * a.nitems), T);
     return;
   } else {
     v -= flat;
@@ -871,6 +884,7 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
           } else {
             sw = (int)(v / (unsigned long long)a.nitems);
             it = (int)(v - (unsigned long long)sw * a.nitems);
+            if (MODE == 2) it = block_order(a, it, T);
           }
         }
         item_q[p_seq % kQ] = it;
@@ -900,6 +914,9 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
         }
         p_sweep = sw;
         p_slab = sl;
+#ifdef YB_TB2_STAMP
+        if (MODE == 2 && a.stamp) a.stamp[2 * ((size_t)sw * a.nitems + it)] = globaltimer_ns();
+#endif
         const Item pi = make_item(A, A.g, it, T, a.ntx);
         if (QS) {  // quiescent item: input box all +0, no source in either step -> skip
           const int tl = it % T;
@@ -949,6 +966,9 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
           for (int q2 = 6; q2 < NARR; ++q2) tma_prefetch_3d(&M.m[q2], x0 - 4, y0 - 1, z + a.pf);
         }
       }
+#ifdef YB_TB2_STAMP
+      if (MODE == 2 && a.stamp && p_e + 1 == p_nE) a.stamp[2 * ((size_t)p_sweep * a.nitems + p_item) + 1] = globaltimer_ns();
+#endif
       if (++p_e == p_nE) p_item = -1;
     }
   }

@@ -634,3 +634,43 @@ def test_cell_coeffs_batched_equals_single(yb, oracle):
     with yb.Simulation(nx, ny, nz) as sim:
         with pytest.raises(yb.YeeInvalidArgument):
             sim.set_cell_coeffs_many({yb.CA: ca, 7: cb})
+
+
+@pytest.mark.parametrize("shape", [(700, 40, 24), (1300, 40, 20), (1030, 72, 40)])
+@pytest.mark.parametrize("xblock", ["default", "0", "1", "3"])
+def test_multisweep_column_block_order(yb, oracle, shape, xblock, monkeypatch):
+    """Multi-sweep launches hand a sweep's tiles out in column blocks (FusedArgs::xblock, 4 tiles
+    wide by default; the last block may be narrower): any width gives the bits of the one-step
+    kernel and of the oracle — grids with 6 / 11 / 9 tile columns, plain runs and both streamed
+    calls (whose skewed orders keep the block order in their sweep-major part)."""
+    torch = pytest.importorskip("torch")
+    nx, ny, nz = shape
+    steps = 24
+    if xblock != "default":
+        monkeypatch.setenv("YB_TB2_XBLOCK", xblock)
+    monkeypatch.setenv("YB_UP_STREAM", "1")
+    ca, cb, da, db = oracle.cell_coeffs(nx, ny, nz, 2, 2)
+    want = oracle.fill_fields(nx, ny, nz, 3)
+    start = [a.copy() for a in want]
+    oracle.run(nx, ny, nz, want, oracle.Coeffs(nx, ny, nz, ca=ca, cb=cb, da=da, db=db), steps)
+
+    def pin(a):
+        t = torch.empty(a.shape, dtype=torch.float32).pin_memory()
+        t.numpy()[...] = a
+        return t.numpy()
+
+    cells = {q: pin(a.reshape(nz, ny, nx)) for q, a in enumerate((ca, cb, da, db))}
+    pf = [pin(a) for a in start]
+    out = [torch.empty(a.shape, dtype=torch.float32).pin_memory().numpy() for a in start]
+    with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2) as s:
+        s.set_cell_coeffs_many(cells)
+        s.upload(start)
+        s.run(steps)
+        assert s.info()["kernel_launches"] == 1
+        got = s.download()
+    with yb.Simulation(nx, ny, nz, variant=yb.VARIANT_TB2) as s:
+        got2 = s.run_streamed(steps, cells, pf, out=out)
+        assert s.info()["streamed_uploads"] == 1
+    for c in range(6):
+        assert np.array_equal(got[c].view(np.uint32), want[c].view(np.uint32)), (shape, xblock, c)
+        assert np.array_equal(got2[c].view(np.uint32), want[c].view(np.uint32)), (shape, xblock, c)
