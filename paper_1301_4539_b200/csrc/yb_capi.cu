@@ -255,8 +255,9 @@ yb::Fields fields_of(const yb_sim* s, int b) {
 }
 
 // L2 promotion per kernel, measured (Gcell/s, 3 runs each): the one-step kernel's maps gain with
-// 64 B (config 2 96.4 -> 98.6, config 3 87.3 -> 90.6 vs 256 B); the two-step kernel's are best
-// or equal with 256 B (config 4 187.1 vs 184.7 with 64 B).
+// 64 B (config 2 96.4 -> 98.6, config 3 87.3 -> 90.6 vs 256 B); the two-step kernel's were best
+// or equal with 256 B in row-major item order (config 4 187.1 vs 184.7 with 64 B); see prepare_fused
+// for wide grids in column-block order.
 constexpr CUtensorMapL2promotion kPromoFused = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
 int encode_map(CUtensorMap* m, const Geo& g, float* base, int box_rows = yb::kBY, int box_cols = yb::kBX,
                CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
@@ -359,15 +360,22 @@ int prepare_fused(yb_sim* s) {
     s->zchunk4 = std::min(std::max(zc4, 1), s->g.nz);
   }
   if (s->variant == YB_VARIANT_TB2 || s->variant == YB_VARIANT_TB4) {
+    // Wide grids (more than 4 tile columns: the sweep's tiles go out in column blocks, so a
+    // block's outer x-halo columns miss L2) fetch those columns with 64 B promotion instead of
+    // 256 B: config 4 198.8 -> 199.9, config 5 156.5 -> 158.0; up to 4 columns 256 B stays
+    // (config 3 162.1 vs 161.2).
+    const CUtensorMapL2promotion promo2 =
+        tx > 4 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     for (int b = 0; b < 2; ++b) {
       int q = 0;
       for (int c = 0; c < 6; ++c)
-        if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->buf[b][c], yb::tb2_short(c) ? yb::kTB2RowsE : yb::kTB2BY))
+        if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->buf[b][c], yb::tb2_short(c) ? yb::kTB2RowsE : yb::kTB2BY,
+                                yb::kBX, promo2))
           return rc;
       for (int a = 0; a < 4; ++a)
         if (s->cell[a])
-          if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->cell[a],
-                                  a < 2 ? yb::kTB2RowsCA : yb::kTB2RowsDA))
+          if (int rc = encode_map(&s->tm2[b].m[q++], s->g, s->cell[a], a < 2 ? yb::kTB2RowsCA : yb::kTB2RowsDA,
+                                  yb::kBX, promo2))
             return rc;
     }
     int S2 = 3;
