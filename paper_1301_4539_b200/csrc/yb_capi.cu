@@ -2575,6 +2575,7 @@ int yb_peer_run(yb_sim* const* sims, int n, int64_t nsteps) {
       a.epoch = s->epoch;
       a.srcs = s->srcs_dev;
       a.no_faces = 0;
+      a.xblock = s->xblock;
       a.store_policy = 1;
       a.co = coef_args(s);
       for (int q = 0; q < 6; ++q) {
@@ -2592,6 +2593,7 @@ int yb_peer_run(yb_sim* const* sims, int n, int64_t nsteps) {
     c.pf = s0->pf2;
     c.ntx = s0->ntx;
     c.nty = s0->nty;
+    c.xblock = s0->xblock;
     c.nsweeps = K;
     c.nitems = c.chain_off[n];
     c.sched = s0->sched;

@@ -865,7 +865,7 @@ __device__ __forceinline__ void tb2_body(const FusedArgs& a, const TMaps& tm, co
             sw = (int)(v / tot);
             const int r = (int)(v - (unsigned long long)sw * tot);
             while (sl + 1 < a.nchain && r >= a.chain_off[sl + 1]) ++sl;
-            it = r - a.chain_off[sl];
+            it = block_order(a, r - a.chain_off[sl], T);  // within a chunk: column blocks, as MODE 2
           }
         } else if (!MS) {
           it = v < (unsigned long long)a.nitems ? (int)v : -1;
