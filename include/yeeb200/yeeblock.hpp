@@ -667,7 +667,8 @@ struct RunOptions {
   /// FieldSet is the live state (runner.hpp:236); here it is a mirror of the device state.
   /// Lazy: on the first fields() access after a run. Eager: as part of run() (yb_run_to_host: the
   /// readback overlaps the last sweeps, also into this pageable storage). Auto (default): eager
-  /// for runs of at least 64 steps, until a readback was paid for and never looked at.
+  /// for runs of at least 64 steps where that overlap is possible (two-step kernel, no probes,
+  /// quiescent_skip off), until a readback was paid for and never looked at.
   enum class Readback { Lazy, Eager, Auto };
   Readback readback = Readback::Auto;
 };
@@ -760,8 +761,12 @@ class Simulation {
     push_if_dirty();
     if (eager_unread_) auto_lazy_ = true;  // the last eager readback was never looked at
     using RB = typename RunOptions<Real>::Readback;
+    // Auto: only where the readback can overlap the run (yb_run_to_host streams with the two-step
+    // kernel, no probes, quiescent skip off); elsewhere an eager readback is just an early one
+    const bool streams = opts_.kernel == YB_VARIANT_TB2 && opts_.probes.empty() && !opts_.quiescent_skip;
     const bool eager = !opts_.after_step && n_steps > 0 &&
-                       (opts_.readback == RB::Eager || (opts_.readback == RB::Auto && n_steps >= 64 && !auto_lazy_));
+                       (opts_.readback == RB::Eager ||
+                        (opts_.readback == RB::Auto && streams && n_steps >= 64 && !auto_lazy_));
     const double t0 = now();
     std::vector<ProbeRecord> records;
     long long t = step_;
