@@ -198,6 +198,19 @@ struct ChainSlab {
 // [4] value needed.
 enum { WAIT_DEP = 1, WAIT_PEER_KERNEL = 2, WAIT_PEER = 3, WAIT_UPLOAD = 4 };
 
+// Position q of a sweep's sweep-major order -> item (FusedArgs::xblock): z-chunk, then column
+// block of xblock tiles, then tile row, then tile column within the block (T = tiles per chunk).
+__device__ __forceinline__ int block_order(const FusedArgs& a, int q, int T) {
+  const int W = a.xblock;
+  if (W <= 0 || W >= a.ntx) return q;
+  const int ch = q / T, r = q - ch * T;
+  const int per = W * a.nty;                   // items of a full column block
+  const int b = min(r / per, (a.ntx - 1) / W);  // the last block may be narrower
+  const int r2 = r - b * per, wb = min(W, a.ntx - b * W);
+  const int ty = r2 / wb, tx = b * W + (r2 - ty * wb);
+  return ch * T + ty * a.ntx + tx;
+}
+
 // planes [kz0, kz1) of z-chunk c of a launch
 __device__ __forceinline__ void chunk_planes(const FusedArgs& a, int c, int& kz0, int& kz1) {
   if (c < a.nch0) {

@@ -217,19 +217,6 @@ __device__ __noinline__ void wait_neighbours(const FusedArgs& a, int item, int s
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-// Position q of a sweep's sweep-major part -> item (FusedArgs::xblock): z-chunk, then column
-// block of xblock tiles, then tile row, then tile column within the block.
-__device__ __forceinline__ int block_order(const FusedArgs& a, int q, int T) {
-  const int W = a.xblock;
-  if (W <= 0 || W >= a.ntx) return q;
-  const int ch = q / T, r = q - ch * T;
-  const int per = W * a.nty;                   // items of a full column block
-  const int b = min(r / per, (a.ntx - 1) / W);  // the last block may be narrower
-  const int r2 = r - b * per, wb = min(W, a.ntx - b * W);
-  const int ty = r2 / wb, tx = b * W + (r2 - ty * wb);
-  return ch * T + ty * a.ntx + tx;
-}
-
 // Streamed readback order (FusedArgs::diag): work item v of a multi-sweep
 // launch -> (sweep, item); sweeps before skew0 sweep-major, the rest along
 // y-skewed diagonals d = 2*(sweep - skew0) + tile row, sweeps ascending within
