@@ -1588,8 +1588,9 @@ int yb_run_to_host(yb_sim* s, int64_t nsteps, float* const* d) {
   // over PCIe at ~52 GB/s is ~40 two-step sweeps of the kernel at ~190
   // Gcell/s, ~32 at ~160 with four coefficient arrays), at most what the tile
   // rows allow (a row leads the next by half a sweep); modelled and measured
-  // with tools/drain_phases.py (config 4: K = 40 of 100).
-  int K = popcount4(cell_mask(s)) > 2 ? 32 : 40;
+  // with tools/drain_phases.py / tools/drain_k.sh (config 4 with the round-2 kernel: K = 32 / 40 / 48 / 56
+  // -> 0.700 / 0.688 / 0.678 / 0.677 s end to end; 52 of 100).
+  int K = popcount4(cell_mask(s)) > 2 ? 32 : 52;
   if (const char* e = std::getenv("YB_DRAIN_K")) K = std::atoi(e);
   K = std::max(1, std::min({K, nsw, s->nty / 2 + 1}));
   if (int rc = ensure_drain(s, K)) return rc;
@@ -1721,7 +1722,7 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
   // row by tile row; ~45 GB/s of pitched copies against ~185 / ~155 Gcell/s sweeps) plus two —
   // skewed sweeps are ~15% slower (a tile row's y-halo rows miss L2), so no deeper than needed.
   const bool heavy = popcount4(cell_mask(s)) > 2;
-  int K = heavy ? 32 : 40;
+  int K = heavy ? 32 : 52;
   if (const char* e = std::getenv("YB_DRAIN_K")) K = std::atoi(e);
   const double cells1 = (double)s->g.nx * s->g.ny * s->g.nz;
   const double up_s = (ncoef * cells1 + (in6 ? 6.0 * cells1 : 0.0)) * 4.0 / 45e9;
