@@ -1773,7 +1773,16 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
   s->upstream = false;
   s->up_base = need;
   if (rc) return rc;
-  // the launch is in flight (its first-sweep items poll the row words): now the copies
+  // the launch is in flight (its first-sweep items poll the row words): now the copies. Should one
+  // fail to enqueue, every row word is released (the run's result is then undefined, the call
+  // returns the error) so that the launch does not spin until its deadline.
+  auto release_rows = [&](int rc) {
+    std::vector<unsigned> w((size_t)s->nty, need);
+    cudaMemcpyAsync(s->upband_dev, w.data(), w.size() * sizeof(unsigned), cudaMemcpyHostToDevice, s->xfer);
+    cudaStreamSynchronize(s->xfer);
+    cudaStreamSynchronize(s->stream);
+    return rc;
+  };
   // (one copy stream: the arrays alternating over two streams measured no faster)
   for (int ty = 0; ty < s->nty; ++ty) {
     const int j0 = ty * yb::kTB2Rows;
@@ -1781,7 +1790,8 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
     for (int i = 0; i < ncoef; ++i) {
       const int j1 = last ? ce[1] : std::min(j0 + yb::kTB2Rows, ce[1]);
       if (j1 > j0)
-        if (int rc = copy_rows(s, s->cell[which[i]], const_cast<float*>(cells[i]), ce, j0, j1, true, s->xfer)) return rc;
+        if (int rc = copy_rows(s, s->cell[which[i]], const_cast<float*>(cells[i]), ce, j0, j1, true, s->xfer))
+          return release_rows(rc);
     }
     if (in6)
       for (int c = 0; c < 6; ++c) {
@@ -1789,10 +1799,11 @@ int yb_run_streamed(yb_sim* s, int64_t nsteps, int ncoef, const int* which, cons
         comp_ext(s->g, c, e);
         const int j1 = last ? e[1] : std::min(j0 + yb::kTB2Rows, e[1]);
         if (j1 > j0)
-          if (int rc = copy_rows(s, s->buf[cur0][c], const_cast<float*>(in6[c]), e, j0, j1, true, s->xfer)) return rc;
+          if (int rc = copy_rows(s, s->buf[cur0][c], const_cast<float*>(in6[c]), e, j0, j1, true, s->xfer))
+            return release_rows(rc);
       }
     if (CUresult r = wr(xs, reinterpret_cast<CUdeviceptr>(s->upband_dev + ty), need, 0))
-      return fail(YB_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", (int)r);
+      return release_rows(fail(YB_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", (int)r));
     if (trace) YB_CU(cudaEventRecord(uev[ty], s->xfer));
   }
   s->step_index += 2 * nsw;
