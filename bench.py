@@ -466,6 +466,8 @@ def main():
                 cell_arrays = {q: med[q] for q in want}
             e_steps = cfg_steps
 
+            flow = {}  # what the last one-call run did (yb_info counters)
+
             def run_e2e(qskip, upload_fields=True, streamed=True, up_streamed=True):
                 s2 = make_sim()
                 if table is not None:
@@ -501,8 +503,10 @@ def main():
                     s2.download(out=host_out)
                 dt = time.perf_counter() - t0
                 skipped = s2.info()["skipped_items"]
-                if one_call and e_steps % 2 == 0 and 8 <= e_steps <= 2048 and ny >= 25 and nx >= 1024:
-                    assert s2.info()["streamed_uploads"] == 1, "yb_run_streamed fell back to the phase-by-phase path"
+                if one_call:  # reported, not asserted: the call falls back to the phases where it cannot stream
+                    inf = s2.info()
+                    flow["streamed_uploads"] = int(inf["streamed_uploads"])
+                    flow["streamed_readbacks"] = int(inf["streamed_readbacks"])
                 if dist:  # no neighbour may still be storing into this slab's (IPC-mapped) memory
                     torch.cuda.synchronize()
                     dist.barrier()
@@ -526,12 +530,14 @@ def main():
             # best of two runs (each on a fresh handle): host-side jitter (page-cache / pinned-memory
             # state) moves single e2e runs by several percent
             dt = min(run_e2e(False, upload_fields=not zero_start)[0] for _ in range(2))
+            headline_flow = dict(flow)
             # the same flow with the readback after the run (yb_advance + yb_download_fields)
             ds = run_e2e(False, upload_fields=not zero_start, streamed=False)[0] if world == 1 else None
             h2d = coef_b + (0 if zero_start else field_b)
             e2e = {"value": cells_total * e_steps / dt / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": h2d / e_steps, "d2h_bytes_per_step": d2h / e_steps,
                    "steps": e_steps, "wall_s": dt, "per_gpu_bytes": True, "runs": "best of 2",
+                   "streamed": headline_flow,
                    "path": ("Simulation: set_cell_coeffs (pinned host) -> run(config steps) from the zero-initialised "
                             "state -> download all six fields (pinned host)" if zero_start else
                             "Simulation: set_cell_coeffs + upload all six fields (pinned host) -> run(config steps) "
